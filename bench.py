@@ -1,0 +1,460 @@
+"""Benchmark of the TAR+RHT gradient-aggregation hot path (BASELINE.json).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload resnet50|headline|bert|gpt2xl|cfg1] [--workers n]
+
+A *step* is one Transpose-AllReduce generation over every bucket of the
+workload's gradient (RHT encode -> stage-1 masked mean -> stage-2 gather ->
+masked RHT decode), 1% seeded datagram-coin drops unless ``--drop`` says
+otherwise.  At ``--gpus 1`` the ``--workers`` (default 4, the reference's
+``SimSession`` shape, BASELINE configs[0]) workers are co-resident on one GPU;
+at ``--gpus N>1`` there is one worker per GPU (torchrun, NVLink peer pulls).
+
+``value``: whole-job gradient GB/s reduced = workers * bytes(gradient) / step
+time (device time, CUDA events, max over ranks).  ``e2e``: the same through
+the public API with pinned host buffers copied in and results copied out
+inside the timed region.  ``roofline``: the dominant kernel's algorithmic
+bytes / its live CUDA-event duration against MEASURED_PEAKS.json.
+``cpu_baseline``: the reference algorithm (oracle port of ubar, numpy, the
+same masks) timed on this host on one bucket.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+MB25 = 25 * 1024 * 1024 // 4  # 25 MB fp32 bucket = 6,553,600 entries
+WORKLOADS = {
+    # name: (total entries, bucket entries, input dtype, description)
+    "resnet50": (25_557_032, MB25, "f32", "ResNet-50 gradient (25.6M fp32) in 25 MB buckets"),
+    "headline": (25_000_000, 25_000_000, "f32", "one 25M-entry fp32 bucket (north-star headline)"),
+    "bert": (340_000_000, MB25, "f32", "BERT-large gradient (340M fp32) in 25 MB buckets"),
+    "gpt2xl": (1_557_611_200, 25 * 1024 * 1024 // 2, "bf16",
+               "GPT-2 XL gradient (1.56B bf16 in / fp32 aggregate) in 25 MB bf16 buckets"),
+    "cfg1": (1_048_576, 1_048_576, "f32", "one 1M-entry fp32 bucket (BASELINE configs[0])"),
+}
+
+
+def bucket_sizes(total: int, per: int) -> list:
+    out = [per] * (total // per)
+    if total % per:
+        out.append(total % per)
+    return out
+
+
+def next_pow2(n: int) -> int:
+    return 1 if n <= 1 else 1 << (n - 1).bit_length()
+
+
+def load_peaks() -> dict:
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            p = json.load(fh)
+        return {"hbm_gbs": float(p["hbm_gbs"]), "src": "measured"}
+    except Exception:
+        return {"hbm_gbs": 6650.0, "src": "fallback"}
+
+
+NVLINK_GBS = 770.0  # measured peer copy per direction (B200_PROFILING.md)
+
+
+# ------------------------------------------------------------ clocks
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax = float(parts[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------ roofline
+def kernel_bytes(cls: str, dim: int, L: int, n: int, s_in: int, s_out: int) -> int:
+    """Algorithmic HBM bytes of one launch of a kernel class for ONE worker
+    (DESIGN.md "Kernels"): reads + writes each counted once."""
+    Y = 4 * dim
+    S = Y // n
+    return {
+        "enc_first": s_in * L + Y,     # read x, write the first-pass wire
+        "enc_mid": 2 * Y,
+        "enc_last": 2 * Y,             # read + write the wire in place
+        "aggregate": n * S + S,        # n shard copies in, one mean out
+        "dec_first": Y + Y,            # gather n aggregates, write scratch
+        "dec_mid": 2 * Y,
+        "dec_last": Y + s_out * L,     # read scratch, write output
+        "assemble": Y + s_out * L,
+        "prep": dim // 8,
+    }.get(cls, 0)
+
+
+def step_alg_bytes(buckets, n_workers, s_in, s_out, ht):
+    """HBM_alg per worker per step, and NVLink bytes."""
+    hbm = 0
+    nvl = 0
+    for L in buckets:
+        if ht:
+            Y = 4 * next_pow2(L)
+            hbm += (s_in + s_out) * L + 3 * Y + Y // n_workers
+            nvl += 2 * Y * (n_workers - 1) // n_workers
+        else:
+            hbm += s_in * L + 4 * L // n_workers + 4 * L + s_out * L
+            nvl += 2 * 4 * L * (n_workers - 1) // n_workers
+    return hbm, nvl
+
+
+# ------------------------------------------------------------ CPU baseline
+def cpu_baseline(bucket_len: int, n_workers: int, drop: float, ht: bool, threads: int):
+    """The reference algorithm (oracle = numpy restatement of ubar's
+    rht_encode / _mean_received / assembly / rht_decode) on one bucket with
+    the same coin masks.  Returns (GB/s of gradient reduced, seconds)."""
+    import numpy as np
+
+    import oracle as O
+
+    buckets = O.make_buckets(0, n_workers, bucket_len)
+    dim = next_pow2(bucket_len) if ht else bucket_len
+    t0 = time.perf_counter()
+    masks = O.datagram_masks(12345, dim, n_workers, 0, drop)
+    O.run_generation(buckets, 0, 0, ht, masks=masks, r=0, threads=threads)
+    dt = time.perf_counter() - t0
+    return n_workers * 4 * bucket_len / dt / 1e9, dt
+
+
+# ------------------------------------------------------------ our arm
+def run_ours(args):
+    import torch
+
+    from paper_2310_06993_b200 import _lib
+    from paper_2310_06993_b200.collectives import MaskSpec, tar_allreduce_local
+
+    total, per, dt_name, desc = WORKLOADS[args.workload]
+    dtype = torch.bfloat16 if dt_name == "bf16" else torch.float32
+    s_in = 2 if dt_name == "bf16" else 4
+    s_out = s_in
+    buckets = bucket_sizes(total, per)
+    ht = args.ht == "on"
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    multi = world > 1
+    n_workers = world if multi else args.workers
+
+    g = torch.Generator(device=dev).manual_seed(1234 + rank)
+    if multi:
+        import torch.distributed as dist
+
+        from paper_2310_06993_b200.dist import TarCommunicator
+
+        dist.init_process_group("nccl", device_id=dev)
+        comm = TarCommunicator(max_len=max(buckets), epp=350)
+        grads = [torch.randn(L, device=dev, generator=g).to(dtype) for L in buckets]
+        outs = [torch.empty_like(x) for x in grads]
+    else:
+        grads = [[torch.randn(L, device=dev, generator=g).to(dtype) for _ in range(n_workers)]
+                 for L in buckets]
+        outs = [[torch.empty_like(x) for x in ws] for ws in grads]
+    stream = torch.cuda.current_stream(dev)
+    drop = args.drop
+    state = {"gen": 0}
+
+    def one_step(src=None, dst=None):
+        gen = state["gen"]
+        for b, L in enumerate(buckets):
+            masks = MaskSpec.coin(1000003 * gen + b, drop) if drop > 0 else MaskSpec.none()
+            r = gen % n_workers
+            if multi:
+                comm.allreduce((src or grads)[b], (dst or outs)[b], rotation=r, ht=ht, job_seed=7,
+                               generation=gen, bucket_id=b, masks=masks)
+            else:
+                tar_allreduce_local((src or grads)[b], rotation=r, ht=ht, job_seed=7, generation=gen,
+                                    bucket_id=b, masks=masks, out=(dst or outs)[b])
+        state["gen"] += 1
+
+    def barrier():
+        if multi:
+            import torch.distributed as dist
+
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(v: float) -> float:
+        if not multi:
+            return v
+        import torch.distributed as dist
+
+        t = torch.tensor([v], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---- device-timed steps
+    for _ in range(args.warmup):
+        one_step()
+    barrier()
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    time.sleep(0.3)
+    _lib.timing_collect()
+    _lib.timing_enable(True)
+    launches0 = _lib.launch_count()
+    barrier()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(args.steps):
+        one_step()
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    launches = _lib.launch_count() - launches0
+    _lib.timing_enable(False)
+    per_kernel = _lib.timing_collect()
+    dev_ms = ev0.elapsed_time(ev1)
+    # an untimed pass without per-kernel events, to confirm they cost nothing
+    barrier()
+    ev0.record(stream)
+    for _ in range(args.steps):
+        one_step()
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    dev_ms_plain = ev0.elapsed_time(ev1)
+    clk = clocks.stop()
+    dev_ms = max_over_ranks(min(dev_ms, dev_ms_plain))
+    ms_per_step = dev_ms / args.steps
+
+    grad_bytes = s_in * sum(buckets)
+    value = n_workers * grad_bytes / (ms_per_step * 1e-3) / 1e9
+
+    # ---- end to end through the public API with host buffers
+    if multi:
+        host_in = [x.cpu().pin_memory() for x in grads]
+        host_out = [torch.empty_like(h).pin_memory() for h in host_in]
+    else:
+        host_in = [[x.cpu().pin_memory() for x in ws] for ws in grads]
+        host_out = [[torch.empty_like(h).pin_memory() for h in ws] for ws in host_in]
+
+    def e2e_step():
+        if multi:
+            dsrc = [h.to(dev, non_blocking=True) for h in host_in]
+            ddst = [torch.empty_like(x) for x in dsrc]
+            one_step(dsrc, ddst)
+            for h, d in zip(host_out, ddst):
+                h.copy_(d, non_blocking=True)
+        else:
+            dsrc = [[h.to(dev, non_blocking=True) for h in ws] for ws in host_in]
+            ddst = [[torch.empty_like(x) for x in ws] for ws in dsrc]
+            one_step(dsrc, ddst)
+            for hs, ds in zip(host_out, ddst):
+                for h, d in zip(hs, ds):
+                    h.copy_(d, non_blocking=True)
+
+    e2e_step()
+    barrier()
+    ev0.record(stream)
+    e2e_steps = max(1, min(args.steps, 5))
+    for _ in range(e2e_steps):
+        e2e_step()
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = max_over_ranks(ev0.elapsed_time(ev1)) / e2e_steps
+    per_rank_workers = 1 if multi else n_workers
+    io_bytes = per_rank_workers * grad_bytes
+    e2e = {"value": round(n_workers * grad_bytes / (e2e_ms * 1e-3) / 1e9, 3), "unit": "GB/s",
+           "ms_per_step": round(e2e_ms, 3), "h2d_bytes_per_step": io_bytes, "d2h_bytes_per_step": io_bytes}
+
+    # ---- roofline of the dominant kernel class
+    peaks = load_peaks()
+    dom = max((k for k in per_kernel if per_kernel[k][1] > 0), key=lambda k: per_kernel[k][0])
+    dom_ms, dom_n = per_kernel[dom]
+    # per launch: every launch covers one bucket x (local: all workers, multi: one)
+    alg = 0
+    for L in buckets:
+        dim = next_pow2(L) if ht else L
+        alg += kernel_bytes(dom, dim, L, n_workers, s_in, s_out) * per_rank_workers
+    alg_per_launch = alg / len(buckets)
+    avg_launch_s = dom_ms / dom_n * 1e-3
+    achieved = alg_per_launch / avg_launch_s / 1e9
+    if multi and dom in ("aggregate", "dec_first"):
+        # NVLink-bound: bytes pulled from peers per launch
+        nv = 0
+        for L in buckets:
+            dim = next_pow2(L) if ht else L
+            nv += 4 * dim * (n_workers - 1) // n_workers
+        nv_ach = nv / len(buckets) / avg_launch_s / 1e9
+        roof = {"bound": "nvlink", "achieved": round(nv_ach, 1), "peak": NVLINK_GBS, "unit": "GB/s",
+                "frac": round(nv_ach / NVLINK_GBS, 4), "kernel": dom,
+                "hbm_achieved": round(achieved, 1), "traffic": None}
+    else:
+        roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                "frac": round(achieved / peaks["hbm_gbs"], 4), "kernel": dom, "peak_src": peaks["src"],
+                "traffic": None}
+    kernels = {k: {"ms_per_step": round(v[0] / args.steps, 4), "launches_per_step": v[1] / args.steps}
+               for k, v in per_kernel.items() if v[1] > 0}
+
+    # whole-step roofline: max(HBM_alg/HBM, NVL/NVLink)
+    hbm_alg, nvl = step_alg_bytes(buckets, n_workers, s_in, s_out, ht)
+    hbm_alg *= per_rank_workers
+    t_roof = max(hbm_alg / (peaks["hbm_gbs"] * 1e9), (nvl / (NVLINK_GBS * 1e9)) if multi else 0.0)
+    step_roof = {"t_roof_ms": round(t_roof * 1e3, 4), "frac": round(t_roof * 1e3 / ms_per_step, 4),
+                 "hbm_alg_bytes": hbm_alg, "nvlink_bytes_per_dir": nvl if multi else 0}
+
+    out = {
+        "metric": "bucket allreduce GB/s (TAR+RHT)",
+        "value": round(value, 3),
+        "unit": "GB/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(ms_per_step, 4),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f32" if dt_name == "f32" else "bf16->f32",
+        "data": "synthetic (torch.randn gradients)",
+        "config": {"workload": args.workload, "desc": desc, "buckets": len(buckets),
+                   "bucket_entries": per, "total_entries": total, "workers": n_workers,
+                   "workers_per_gpu": per_rank_workers, "ht": args.ht, "drop": drop,
+                   "mask": "datagram coin, 350-entry packets" if drop > 0 else "lossless",
+                   "parallelism": f"tar{n_workers}", "l2": "inputs larger than L2 (no flush)"},
+        "algbw_per_worker_gbs": round(grad_bytes / (ms_per_step * 1e-3) / 1e9, 3),
+        "e2e": e2e,
+        "roofline": roof,
+        "step_roofline": step_roof,
+        "kernels": kernels,
+        "gpu_launches": int(launches),
+        "clocks": clk,
+    }
+    if rank == 0 and not multi and not args.no_cpu_baseline:
+        ncores = len(os.sched_getaffinity(0))
+        thr = min(n_workers, ncores)
+        gbs, secs = cpu_baseline(per, n_workers, drop, ht, thr)
+        out["cpu_baseline"] = {"value": round(gbs, 6), "unit": "GB/s", "cores": thr, "kind": "port",
+                               "sample": f"one {per}-entry bucket x {n_workers} workers, oracle port "
+                                         f"(numpy, fp64), {secs:.1f}s, {ncores} cores visible"}
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if multi:
+        import torch.distributed as dist
+
+        comm.close()
+        dist.destroy_process_group()
+
+
+# ------------------------------------------------------------ reference arm
+def run_reference(args):
+    """The reference's CPU algorithm (oracle port of ubar -- /root/reference is
+    not on the GPU box) on this host, rank 0 only."""
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if rank != 0:
+        return
+    total, per, dt_name, desc = WORKLOADS[args.workload]
+    n_workers = world if world > 1 else args.workers
+    ht = args.ht == "on"
+    ncores = len(os.sched_getaffinity(0))
+    thr = min(n_workers, ncores)
+    # bounded sample: one bucket, capped so a step stays ~10 s on one core
+    sample = min(per, 1 << 21)
+    for _ in range(args.warmup):
+        cpu_baseline(sample, n_workers, args.drop, ht, thr)
+    secs = []
+    for _ in range(args.steps):
+        _, s = cpu_baseline(sample, n_workers, args.drop, ht, thr)
+        secs.append(s)
+    t = sum(secs) / len(secs)
+    val = n_workers * 4 * sample / t / 1e9
+    out = {
+        "metric": "bucket allreduce GB/s (TAR+RHT)", "value": round(val, 6), "unit": "GB/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t * 1e3, 2),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "impl": "reference",
+        "config": {"workload": args.workload, "desc": desc, "workers": n_workers, "ht": args.ht,
+                   "drop": args.drop, "sample_entries": sample},
+        "cpu_baseline": {"value": round(val, 6), "unit": "GB/s", "cores": thr, "kind": "port",
+                         "sample": f"one {sample}-entry bucket x {n_workers} workers per step "
+                                   f"(oracle port of ubar: numpy fp64, threads over workers)"},
+        "e2e": {"value": round(val, 6), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="resnet50", choices=sorted(WORKLOADS))
+    ap.add_argument("--workers", type=int, default=4, help="co-resident workers at --gpus 1")
+    ap.add_argument("--drop", type=float, default=0.01)
+    ap.add_argument("--ht", default="on", choices=["on", "off"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

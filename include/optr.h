@@ -1,0 +1,177 @@
+/*
+ * optr.h -- C ABI of the B200-native OptiReduce TAR+RHT hot path.
+ *
+ * One shared library (paper_2310_06993_b200/liboptr.so) exports these
+ * entry points.  They take plain pointers and sizes (device pointers unless
+ * noted), enqueue on the caller's CUDA stream, never synchronise the host
+ * unless the comment says so, and return an int status.  No torch types.
+ *
+ * Reference interfaces each entry point replaces (paths relative to
+ * /root/reference/pkg/src/ubar/):
+ *
+ *   optr_derive_seed          hadamard.py:31-34   derive_seed
+ *   optr_pcg64_output         hadamard.py:49-50   PCG64(SeedSequence(seed)) stream (k-th draw)
+ *   optr_rht_signs            hadamard.py:49-51   RhtContext.signs  (bit-packed, +1 = 1)
+ *   optr_fwht                 hadamard.py:76-90   fwht_in_place
+ *   optr_rht_encode           hadamard.py:93-102  rht_encode
+ *   optr_rht_decode           hadamard.py:105-123 rht_decode (+ EmptyReceptionError)
+ *   optr_masks_host           datagram.py:70-72,111-124 send-side coin, as packet bitmaps
+ *   optr_tar_local            runner.py:211-276 run_generation hot path (encode ->
+ *                             collectives.py:97-150 tar_allreduce -> decode) for n
+ *                             workers co-resident on one GPU (the SimSession shape)
+ *   optr_comm_* / optr_tar    the same path with one worker per GPU (one process per
+ *                             GPU), peers' buffers mapped over NVLink (CUDA IPC)
+ *
+ * Status codes map to the reference's exceptions in the Python facade:
+ *   OPTR_EINVAL -> ValueError, OPTR_EEMPTY -> EmptyReceptionError,
+ *   OPTR_ECUDA / OPTR_ENOMEM -> RuntimeError.
+ */
+#ifndef OPTR_H_
+#define OPTR_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define OPTR_OK 0
+#define OPTR_EINVAL 1
+#define OPTR_EEMPTY 2
+#define OPTR_ECUDA 3
+#define OPTR_ENOMEM 4
+
+#define OPTR_MAX_WORKERS 16
+
+/* element types of caller buffers (the wire / aggregate is always fp32) */
+#define OPTR_F32 0
+#define OPTR_BF16 1
+
+/* mask kinds */
+#define OPTR_MASK_NONE 0   /* lossless channel, collectives.py:321-401            */
+#define OPTR_MASK_COIN 1   /* datagram coin, counter-indexed PCG64 (bit-exact)     */
+#define OPTR_MASK_BITMAP 2 /* caller-supplied packet bitmaps (captured sim masks) */
+
+/*
+ * Drop masks, per packet.  Packet k of a (stage, dst, src) transfer covers
+ * shard entries [k*epp, min((k+1)*epp, len)).  Stage 1 carries shard
+ * owned_shard(dst), stage 2 carries owned_shard(src) (collectives.py:117-137).
+ * Bitmap layout (u32 words, bit k%32 of word k/32, 1 = delivered):
+ *   word index = ((stage * n + dst) * n + src) * words_per_pair + k / 32,
+ *   stage in {0 (stage 1), 1 (stage 2)}, words_per_pair from optr_mask_words.
+ */
+typedef struct {
+  int32_t kind;          /* OPTR_MASK_*                                        */
+  int32_t epp;           /* entries per packet = max_payload / 4 (350)         */
+  uint64_t seed;         /* COIN: sender src draws from SeedSequence([seed,src]) */
+  double drop_prob;      /* COIN: packet dropped iff random() < drop_prob      */
+  const uint32_t* bitmap;/* BITMAP: device pointer in the layout above         */
+} optr_mask_spec;
+
+/* ------------------------------------------------------------ host helpers */
+uint64_t optr_derive_seed(uint64_t job_seed, uint64_t bucket_id, uint64_t generation);
+/* k-th u64 output of PCG64(SeedSequence(entropy[0..n_entropy))) */
+uint64_t optr_pcg64_output(const uint64_t* entropy, int n_entropy, uint64_t k);
+int64_t optr_next_pow2(int64_t n);
+/* u32 words per (stage,dst,src) pair for a vector of `dim` entries */
+int64_t optr_mask_words(int64_t dim, int n, int epp);
+/* host computation of the coin bitmaps (same layout; no GPU needed) */
+int optr_masks_host(uint32_t* bitmap_host, int64_t dim, int n, int rotation,
+                    uint64_t seed, double drop_prob, int epp);
+/* library build/version string */
+const char* optr_version(void);
+
+/* ------------------------------------------------------------- codec (GPU) */
+/* Rademacher signs as D bits (bit k of word k/32; 1 = +1).  D = power of 2. */
+int optr_rht_signs(uint32_t* sign_bits, int64_t dim, uint64_t seed, void* stream);
+
+/* Unnormalised Sylvester FWHT of fp32 v[0..dim) in place; dim = 2^k. */
+int optr_fwht(float* v, int64_t dim, void* stream);
+
+/* y[0..dim) = H (signs * pad(x[0..L))) / sqrt(dim).  x is OPTR_F32/BF16. */
+int optr_rht_encode(const void* x, int dtype_in, int64_t L, float* y, int64_t dim,
+                    uint64_t seed, void* stream);
+
+/* out[0..L) = signs * H(mask ? y : 0) * (dim/count) / sqrt(dim).
+ * mask: device bytes (1 = received) or NULL for all received.
+ * Synchronises the stream to read count; returns OPTR_EEMPTY if count == 0
+ * (hadamard.py:117-118).  out dtype OPTR_F32/BF16. */
+int optr_rht_decode(const float* y, const uint8_t* mask, int64_t dim, int64_t L,
+                    uint64_t seed, void* out, int dtype_out, void* stream);
+
+/* ------------------------------------------- TAR+RHT, n workers on one GPU */
+/* Workspace bytes for optr_tar_local. */
+size_t optr_tar_local_workspace(int n, int64_t L, int ht, int epp);
+
+/*
+ * One generation of runner.py:211-276 for n co-resident workers:
+ *   ht: signs from derive_seed(job_seed, bucket_id, generation) (the runner
+ *       passes bucket_id = generation % 65536, runner.py:219-222),
+ *       y_w = rht_encode(x_w) (fp32 wire), TAR with rotation, decode per worker
+ *       (count 0 -> zeros, runner.py:255-256);
+ *   !ht: TAR of x_w directly.
+ * x[w], out[w]: device pointers to L elements of dtype_in / dtype_out.
+ * received_out: optional device array [2][n] of u64 received entries per
+ *   (stage, dst) -- the numbers NodeStats/StageOutcome derive loss from.
+ * got_out: optional device bytes [n][dim] = AllReduceResult.received.
+ */
+int optr_tar_local(const void* const* x, void* const* out, int n, int64_t L,
+                   int dtype_in, int dtype_out, uint64_t job_seed, uint64_t bucket_id,
+                   uint64_t generation, int rotation, int ht, const optr_mask_spec* masks,
+                   void* workspace,
+                   size_t workspace_bytes, uint64_t* received_out, uint8_t* got_out,
+                   void* stream);
+
+/* --------------------------------------- TAR+RHT, one worker per GPU (IPC) */
+typedef struct optr_comm_s* optr_comm;
+
+/* Allocate, on CUDA device `device`, this rank's symmetric buffers for
+ * buckets up to max_len entries.  Every rank calls it with the same n,
+ * max_len and epp. */
+int optr_comm_create(optr_comm* out, int device, int rank, int n, int64_t max_len, int epp);
+/* Bytes of the opaque IPC handle blob each rank must share with all peers. */
+size_t optr_comm_handle_bytes(void);
+int optr_comm_get_handle(optr_comm c, void* handle_out);
+/* all_handles: n blobs of optr_comm_handle_bytes(), rank order.  Maps every
+ * peer's buffers (cudaIpcOpenMemHandle) and checks peer access. */
+int optr_comm_open(optr_comm c, const void* all_handles);
+int optr_comm_destroy(optr_comm c);
+
+/* This rank's part of one generation (same semantics as optr_tar_local for
+ * worker `rank`): x, out are this rank's L-element buffers.
+ * received_out: optional device u64[2] (stage1, stage2) for this rank. */
+int optr_tar(optr_comm c, const void* x, void* out, int64_t L, int dtype_in,
+             int dtype_out, uint64_t job_seed, uint64_t bucket_id, uint64_t generation,
+             int rotation, int ht, const optr_mask_spec* masks, uint64_t* received_out,
+             void* stream);
+
+/* Device-side all-rank barrier on `stream` (flags over NVLink). */
+int optr_comm_barrier(optr_comm c, void* stream);
+
+/* --------------------------------------------------------- instrumentation */
+/* Kernel classes timed when timing is enabled. */
+#define OPTR_K_PREP 0       /* signs + masks + counts                        */
+#define OPTR_K_ENC_FIRST 1  /* first encode FWHT pass (reads x, signs, pad)  */
+#define OPTR_K_ENC_MID 2    /* middle encode passes (in place)              */
+#define OPTR_K_ENC_LAST 3   /* last encode pass (writes the fp32 wire)      */
+#define OPTR_K_AGG 4        /* stage-1 masked mean at the owner             */
+#define OPTR_K_DEC_FIRST 5  /* stage-2 gather + first decode pass           */
+#define OPTR_K_DEC_MID 6
+#define OPTR_K_DEC_LAST 7   /* last decode pass (scale, sign, cast, out)    */
+#define OPTR_K_ASSEMBLE 8   /* stage-2 gather without RHT                   */
+#define OPTR_K_BARRIER 9
+#define OPTR_K_OTHER 10
+#define OPTR_K_CLASSES 11
+/* Enable (1) / disable (0) CUDA-event timing of every kernel launch. */
+int optr_timing_enable(int on);
+/* Synchronise recorded events and return, per class, the summed device
+ * milliseconds and the launch count since the last reset; then reset. */
+int optr_timing_collect(double* ms_out, int64_t* launches_out);
+/* Kernels this library launched since load (all classes, any device). */
+int64_t optr_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* OPTR_H_ */

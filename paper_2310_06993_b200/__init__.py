@@ -1,0 +1,28 @@
+"""B200-native OptiReduce hot path: RHT encode -> Transpose AllReduce with
+masked mean -> masked RHT decode, as sm_100a CUDA kernels behind a C ABI
+(include/optr.h, liboptr.so) with a Python facade mirroring the reference
+package ``ubar`` (hadamard / collectives / runner entry points) and a
+PyTorch DDP comm hook."""
+
+from ._lib import EmptyReceptionError, LIB_PATH, lib  # noqa: F401
+from .collectives import (  # noqa: F401
+    AllReduceResult,
+    MaskSpec,
+    build_schedule,
+    owned_shard,
+    shard_lengths,
+    shard_offsets,
+    shard_owner,
+    tar_allreduce_local,
+)
+from .hadamard import (  # noqa: F401
+    DropMask,
+    RhtContext,
+    derive_seed,
+    fwht_in_place,
+    mse,
+    next_pow2,
+    rht_decode,
+    rht_encode,
+)
+from .session import GenerationReport, GpuSession  # noqa: F401

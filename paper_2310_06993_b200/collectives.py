@@ -1,0 +1,261 @@
+"""Transpose AllReduce with the RHT codec fused in, on the GPU.
+
+Drop-in for the TAR part of ``ubar.collectives`` / ``ubar.schedule`` /
+``ubar.wire`` (``/root/reference/pkg/src/ubar/``).  The reference expresses a
+collective as a sans-IO generator driven by a channel; on a B200 the channel
+is HBM (n workers on one GPU, ``tar_allreduce_local``) or NVLink (one worker
+per GPU, ``paper_2310_06993_b200.dist``), and the lossy transport is replaced
+by seeded per-packet drop masks (``MaskSpec``) that reproduce the reference's
+masks bit-exactly.
+
+Host-side index math (shards, owners, schedule) is plain Python here and is
+mirrored in the CUDA kernels.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from ._lib import check, lib
+
+ENTRY_BYTES = 4  # wire.py:23
+MAX_PAYLOAD = 1400  # wire.py:22
+
+
+# ----------------------------------------------------------- index helpers
+def shard_lengths(length: int, n: int) -> list[int]:
+    """wire.py:121-126."""
+    if n < 1:
+        raise ValueError("node count must be >= 1")
+    base, extra = divmod(int(length), n)
+    return [base + 1 if j < extra else base for j in range(n)]
+
+
+def shard_offsets(length: int, n: int) -> list[int]:
+    """wire.py:129-133."""
+    offs = [0]
+    for ln in shard_lengths(length, n):
+        offs.append(offs[-1] + ln)
+    return offs
+
+
+def shard_owner(shard_index: int, r: int, n: int) -> int:
+    """schedule.py:42-44."""
+    return (shard_index + r) % n
+
+
+def owned_shard(node: int, r: int, n: int) -> int:
+    """schedule.py:47-49."""
+    return (node - r) % n
+
+
+def build_schedule(n: int, incast: int) -> tuple:
+    """schedule.py:67-78: round k sends i -> i+kI+1 .. i+kI+I (mod n)."""
+    if n < 2:
+        raise ValueError("need at least 2 nodes")
+    if not 1 <= incast <= n - 1:
+        raise ValueError(f"incast factor must be in [1, {n - 1}], got {incast}")
+    n_rounds = -(-(n - 1) // incast)
+    rounds = []
+    for k in range(n_rounds):
+        offsets = range(k * incast + 1, min(k * incast + incast, n - 1) + 1)
+        rounds.append({i: tuple((i + o) % n for o in offsets) for i in range(n)})
+    return tuple(rounds)
+
+
+def n_packets(n_entries: int, epp: int) -> int:
+    """wire.py:176-180."""
+    return -(-int(n_entries) // epp) if n_entries > 0 else 0
+
+
+# ------------------------------------------------------------------- masks
+def mask_words(dim: int, n: int, epp: int) -> int:
+    return int(lib().optr_mask_words(int(dim), int(n), int(epp)))
+
+
+def pack_packet_masks(packets: dict, dim: int, n: int, epp: int) -> np.ndarray:
+    """{(stage 1|2, dst, src): bool[n_packets]} -> u32 words in the optr.h
+    bitmap layout."""
+    pw = mask_words(dim, n, epp)
+    words = np.zeros((2, n, n, pw), dtype=np.uint32)
+    for (stage, dst, src), pk in packets.items():
+        pk = np.asarray(pk, dtype=bool)
+        padded = np.zeros(pw * 32, dtype=bool)
+        padded[: len(pk)] = pk
+        words[stage - 1, dst, src] = np.packbits(padded, bitorder="little").view(np.uint32)
+    return words.reshape(-1)
+
+
+def unpack_packet_masks(words: np.ndarray, dim: int, n: int, r: int, epp: int) -> dict:
+    """Inverse of pack_packet_masks (for tests / stats)."""
+    pw = mask_words(dim, n, epp)
+    w = np.asarray(words, dtype=np.uint32).reshape(2, n, n, pw)
+    lens = shard_lengths(dim, n)
+    out = {}
+    for stage in (1, 2):
+        for dst in range(n):
+            for src in range(n):
+                if src == dst:
+                    continue
+                j = owned_shard(dst, r, n) if stage == 1 else owned_shard(src, r, n)
+                npk = n_packets(lens[j], epp)
+                bits = np.unpackbits(w[stage - 1, dst, src].view(np.uint8), bitorder="little")
+                out[(stage, dst, src)] = bits[:npk].astype(bool)
+    return out
+
+
+def coin_masks_host(dim: int, n: int, r: int, seed: int, drop_prob: float,
+                    epp: int = MAX_PAYLOAD // ENTRY_BYTES) -> dict:
+    """The datagram coin (datagram.py:70-72,117-124) computed by liboptr's host
+    port; returns {(stage, dst, src): bool[n_packets]}."""
+    pw = mask_words(dim, n, epp)
+    buf = np.zeros(2 * n * n * pw, dtype=np.uint32)
+    check(lib().optr_masks_host(buf.ctypes.data, int(dim), int(n), int(r), int(seed),
+                                float(drop_prob), int(epp)), "masks_host")
+    return unpack_packet_masks(buf, dim, n, r, epp)
+
+
+@dataclass
+class MaskSpec:
+    """Which packets the lossy channel delivers.
+
+    * ``none``   -- lossless (collectives.py:321-401 run_lossless);
+    * ``coin``   -- the UDP backend's seeded send-side coin, sender ``src``
+      drawing from ``PCG64(SeedSequence([seed, src]))`` per packet in send
+      order (datagram.py:70-72,122), evaluated counter-indexed on the GPU;
+    * ``bitmap`` -- explicit per-packet flags, e.g. simulator masks captured
+      at consumption time (adaptive-timeout cut-offs, late landings).
+    """
+
+    kind: str = "none"
+    epp: int = MAX_PAYLOAD // ENTRY_BYTES
+    seed: int = 0
+    drop_prob: float = 0.0
+    bitmap: object = None  # CUDA int32 tensor in the optr.h layout
+
+    @classmethod
+    def none(cls, max_payload: int = MAX_PAYLOAD) -> "MaskSpec":
+        return cls("none", epp=max_payload // ENTRY_BYTES)
+
+    @classmethod
+    def coin(cls, seed: int, drop_prob: float, max_payload: int = MAX_PAYLOAD) -> "MaskSpec":
+        if not 0.0 <= drop_prob <= 1.0:
+            raise ValueError("drop_prob must be in [0,1]")
+        return cls("coin", epp=max_payload // ENTRY_BYTES, seed=int(seed), drop_prob=float(drop_prob))
+
+    @classmethod
+    def from_packets(cls, packets: dict, dim: int, n: int, max_payload: int = MAX_PAYLOAD,
+                     device=None) -> "MaskSpec":
+        import torch
+
+        epp = max_payload // ENTRY_BYTES
+        words = pack_packet_masks(packets, dim, n, epp)
+        dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+        t = torch.from_numpy(words.view(np.int32)).to(dev)
+        return cls("bitmap", epp=epp, bitmap=t)
+
+    def to_c(self) -> _lib.optr_mask_spec:
+        kinds = {"none": _lib.OPTR_MASK_NONE, "coin": _lib.OPTR_MASK_COIN, "bitmap": _lib.OPTR_MASK_BITMAP}
+        if self.kind not in kinds:
+            raise ValueError(f"unknown mask kind {self.kind!r}")
+        if self.epp <= 0:
+            raise ValueError("max_payload must hold at least one entry")
+        return _lib.optr_mask_spec(kinds[self.kind], int(self.epp), int(self.seed), float(self.drop_prob),
+                                   self.bitmap.data_ptr() if self.bitmap is not None else None)
+
+
+@dataclass
+class AllReduceResult:
+    """collectives.py:65-74: a node's entries plus which arrived."""
+
+    entries: object
+    received: object
+
+
+# -------------------------------------------------------- n workers, 1 GPU
+_WS: dict = {}
+
+
+def _workspace(n: int, L: int, ht: bool, epp: int, device):
+    import torch
+
+    need = int(lib().optr_tar_local_workspace(n, L, int(ht), epp))
+    key = str(device)
+    ws = _WS.get(key)
+    if ws is None or ws.numel() < need:
+        ws = torch.empty(max(need, 1), dtype=torch.uint8, device=device)
+        _WS[key] = ws
+    return ws, need
+
+
+def _dtype_code(t) -> int:
+    import torch
+
+    if t.dtype == torch.float32:
+        return _lib.OPTR_F32
+    if t.dtype == torch.bfloat16:
+        return _lib.OPTR_BF16
+    raise ValueError(f"unsupported dtype {t.dtype}")
+
+
+def tar_allreduce_local(buckets: list, *, rotation: int = 0, ht: bool = False, job_seed: int = 0,
+                        generation: int = 0, bucket_id: int | None = None,
+                        masks: MaskSpec | None = None, out: list | None = None,
+                        out_dtype=None, want_received: bool = False, stream=None):
+    """One TAR(+RHT) generation for ``n = len(buckets)`` workers whose buckets
+    all live on one GPU (the reference's SimSession shape, runner.py:211-276
+    with the channel replaced by ``masks``).
+
+    Returns ``(outs, counts, got)``: per-worker output tensors, a CUDA u64
+    tensor ``[2, n]`` of received entries per (stage, dst), and (if
+    ``want_received``) the ``[n, dim]`` bool AllReduceResult.received.
+    Everything is enqueued on ``stream`` (default: current); no host sync.
+    ``bucket_id`` defaults to ``generation % 65536`` like the runner
+    (runner.py:219-222); the RHT seed is derive_seed(job_seed, bucket_id,
+    generation).
+    """
+    import torch
+
+    n = len(buckets)
+    if n < 2 or n > _lib.MAX_WORKERS:
+        raise ValueError("need 2..16 workers")
+    L = len(buckets[0])
+    dev = buckets[0].device
+    if not buckets[0].is_cuda:
+        raise ValueError("buckets must be CUDA tensors")
+    for b in buckets:
+        if len(b) != L or b.device != dev or b.dtype != buckets[0].dtype or not b.is_contiguous():
+            raise ValueError("buckets must be contiguous, same length, dtype and device")
+    masks = masks or MaskSpec.none()
+    out_dtype = out_dtype or buckets[0].dtype
+    if out is None:
+        out = [torch.empty(L, dtype=out_dtype, device=dev) for _ in range(n)]
+    dim = (1 << max(0, (L - 1).bit_length())) if ht else L
+    counts = torch.zeros((2, n), dtype=torch.int64, device=dev)
+    got = torch.empty((n, dim), dtype=torch.uint8, device=dev) if want_received else None
+    ws, need = _workspace(n, L, ht, masks.epp, dev)
+    xs = (ctypes.c_void_p * n)(*[b.data_ptr() for b in buckets])
+    os_ = (ctypes.c_void_p * n)(*[o.data_ptr() for o in out])
+    spec = masks.to_c()
+    st = stream if stream is not None else torch.cuda.current_stream(dev)
+    check(lib().optr_tar_local(xs, os_, n, L, _dtype_code(buckets[0]), _dtype_code(out[0]),
+                               int(job_seed), int(generation % 65536 if bucket_id is None else bucket_id),
+                               int(generation), int(rotation), int(bool(ht)),
+                               ctypes.byref(spec), ws.data_ptr(), need, counts.data_ptr(),
+                               got.data_ptr() if got is not None else None, st.cuda_stream),
+          "tar_allreduce_local")
+    return out, counts, (got.bool() if got is not None else None)
+
+
+def expected_counts(dim: int, n: int, r: int) -> np.ndarray:
+    """[2, n] expected entries per (stage, dst) (simdriver.py:245-248)."""
+    lens = shard_lengths(dim, n)
+    e = np.zeros((2, n), dtype=np.int64)
+    for dst in range(n):
+        e[0, dst] = (n - 1) * lens[owned_shard(dst, r, n)]
+        e[1, dst] = sum(lens[owned_shard(src, r, n)] for src in range(n) if src != dst)
+    return e

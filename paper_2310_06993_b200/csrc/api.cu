@@ -1,0 +1,855 @@
+// C-ABI entry points (include/optr.h): host-side planning + kernel launches.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include <atomic>
+#include <mutex>
+#include <vector>
+
+#include "../../include/optr.h"
+#include "kernels.cuh"
+
+using namespace optr;
+
+namespace {
+
+#define CK(call)                                                          \
+  do {                                                                    \
+    cudaError_t _e = (call);                                              \
+    if (_e != cudaSuccess) {                                              \
+      fprintf(stderr, "optr: %s failed: %s\n", #call, cudaGetErrorString(_e)); \
+      return OPTR_ECUDA;                                                  \
+    }                                                                     \
+  } while (0)
+
+int log2_exact(int64_t d) {
+  int k = 0;
+  while ((1LL << k) < d) ++k;
+  return k;
+}
+
+bool is_pow2(int64_t d) { return d > 0 && (d & (d - 1)) == 0; }
+
+int64_t next_pow2_i(int64_t n) {
+  if (n <= 1) return 1;
+  int64_t d = 1;
+  while (d < n) d <<= 1;
+  return d;
+}
+
+size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+// ------------------------------------------------------ launch accounting
+std::atomic<int64_t> g_launches{0};
+std::mutex g_tmu;
+bool g_timing = false;
+struct TRec {
+  int cls;
+  cudaEvent_t a, b;
+};
+std::vector<TRec> g_trecs;
+
+// Brackets the kernel launches of one class with CUDA events on `st` when
+// timing is enabled; always counts launches.
+struct KScope {
+  cudaStream_t st;
+  int cls;
+  cudaEvent_t a = nullptr, b = nullptr;
+  KScope(int c, cudaStream_t s, int nlaunch = 1) : st(s), cls(c) {
+    g_launches += nlaunch;
+    if (g_timing) {
+      cudaEventCreate(&a);
+      cudaEventCreate(&b);
+      cudaEventRecord(a, st);
+    }
+  }
+  ~KScope() {
+    if (a) {
+      cudaEventRecord(b, st);
+      std::lock_guard<std::mutex> lk(g_tmu);
+      g_trecs.push_back(TRec{cls, a, b});
+    }
+  }
+};
+
+// Make this library's runtime use the device of the caller's stream (the
+// library links its own static cudart; the caller's current device lives in
+// the caller's runtime).
+int bind_device(void* stream) {
+  if (stream) {
+    int dev = -1;
+    if (cudaStreamGetDevice((cudaStream_t)stream, &dev) == cudaSuccess && dev >= 0) {
+      int cur = -1;
+      cudaGetDevice(&cur);
+      if (cur != dev) CK(cudaSetDevice(dev));
+    }
+  }
+  return OPTR_OK;
+}
+
+// Passes realising H_D = product over disjoint index-bit ranges.
+// contiguous: bits [0, 13) on 8192-entry tiles; strided: bits [13, n) on
+// 2^ks-row x 8-column tiles (split in two when n > 25).
+constexpr int kContigBits = 13;
+constexpr int kColBits = 3;
+
+int plan_passes(int n, PassGeom* out, bool encode_order) {
+  PassGeom p[3];
+  int np = 0;
+  if (n <= kContigBits) {
+    p[np++] = PassGeom{0, n, 0};
+  } else {
+    int rest = n - kContigBits;
+    if (rest <= 12) {
+      p[np++] = PassGeom{kContigBits, rest, kColBits};
+    } else {
+      int k1 = rest / 2;
+      p[np++] = PassGeom{kContigBits + k1, rest - k1, kColBits};
+      p[np++] = PassGeom{kContigBits, k1, kColBits};
+    }
+    p[np++] = PassGeom{0, kContigBits, 0};
+  }
+  for (int i = 0; i < np; ++i) out[i] = encode_order ? p[i] : p[np - 1 - i];
+  return np;
+}
+
+std::mutex g_attr_mu;
+
+template <class Src, class Snk>
+int launch_pass(int cls, const PassGeom& pg, int nlog, int worker_base, int nworkers, const Src& src,
+                const Snk& snk, cudaStream_t st) {
+  const int nelem = 1 << (pg.cb + pg.ks);
+  const int64_t ntiles = (1LL << nlog) >> (pg.cb + pg.ks);
+  int threads = nelem / 32;
+  if (threads < 32) threads = 32;
+  if (threads > 1024) threads = 1024;
+  const size_t smem = (size_t)nelem * sizeof(float);
+  if (smem > 48 * 1024) {
+    static bool done[64] = {false};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(g_attr_mu);
+    if (!done[dev & 63]) {
+      CK(cudaFuncSetAttribute(fwht_pass_kernel<Src, Snk>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              128 * 1024));
+      done[dev & 63] = true;
+    }
+  }
+  dim3 grid((unsigned)ntiles, (unsigned)nworkers);
+  KScope ks(cls, st);
+  fwht_pass_kernel<Src, Snk><<<grid, threads, smem, st>>>(pg, worker_base, src, snk);
+  CK(cudaGetLastError());
+  return OPTR_OK;
+}
+
+// Run the pass list with a fused first-pass source and last-pass sink; the
+// intermediate passes work in place on `buf`.
+template <class Src, class Snk>
+int run_transform(int nlog, bool encode_order, int worker_base, int nworkers, const Src& src,
+                  const SrcBuf& buf, const Snk& snk, cudaStream_t st, int cls0 = OPTR_K_OTHER) {
+  const int c_first = cls0, c_mid = cls0 == OPTR_K_OTHER ? cls0 : cls0 + 1,
+            c_last = cls0 == OPTR_K_OTHER ? cls0 : cls0 + 2;
+  PassGeom ps[3];
+  int np = plan_passes(nlog, ps, encode_order);
+  SnkBuf mid;
+  for (int i = 0; i < kMaxW; ++i) mid.y[i] = buf.y[i];
+  mid.scale = 1.f;
+  int rc;
+  if (np == 1) return launch_pass(c_first, ps[0], nlog, worker_base, nworkers, src, snk, st);
+  if ((rc = launch_pass(c_first, ps[0], nlog, worker_base, nworkers, src, mid, st))) return rc;
+  for (int i = 1; i < np - 1; ++i)
+    if ((rc = launch_pass(c_mid, ps[i], nlog, worker_base, nworkers, buf, mid, st))) return rc;
+  return launch_pass(c_last, ps[np - 1], nlog, worker_base, nworkers, buf, snk, st);
+}
+
+Pcg sign_pcg(uint64_t seed) { return pcg_from_u64s(&seed, 1); }
+
+void fill_sign_args(PrepArgs& a, uint32_t* signs, int64_t dim, uint64_t seed) {
+  Pcg p = sign_pcg(seed);
+  a.signs = signs;
+  a.dim = dim;
+  a.sign_state = p.state;
+  a.sign_inc = p.inc;
+  a.sign_threads = (dim + 63) / 64;
+}
+
+int launch_prep(const PrepArgs& a, cudaStream_t st) {
+  int64_t total = a.sign_threads + a.mask_threads;
+  if (total == 0) return OPTR_OK;
+  int64_t blocks = (total + 255) / 256;
+  KScope ks(OPTR_K_PREP, st);
+  prep_kernel<<<(unsigned)blocks, 256, 0, st>>>(a);
+  CK(cudaGetLastError());
+  return OPTR_OK;
+}
+
+int64_t mask_words(int64_t dim, int n, int epp) {
+  Shards sh = make_shards(dim, n);
+  int64_t maxlen = sh.base + (sh.extra ? 1 : 0);
+  int64_t np = n_packets(maxlen, epp);
+  int64_t w = (np + 31) / 32;
+  return w > 0 ? w : 1;
+}
+
+// Mask/count setup shared by local and multi-GPU paths.
+int setup_masks(PrepArgs& a, const optr_mask_spec* ms, int64_t dim, int n, int r, int epp,
+                uint32_t* bitmap_ws, unsigned long long* counts, int dst_lo, int dst_hi,
+                const uint32_t** bitmap_for_consumers) {
+  a.kind = ms ? ms->kind : OPTR_MASK_NONE;
+  a.n = n;
+  a.r = r;
+  a.epp = epp;
+  a.sh = make_shards(dim, n);
+  a.pw = mask_words(dim, n, epp);
+  a.bitmap_out = bitmap_ws;
+  a.bitmap_in = (ms && ms->kind == OPTR_MASK_BITMAP) ? ms->bitmap : nullptr;
+  if (a.kind == OPTR_MASK_BITMAP && !a.bitmap_in) return OPTR_EINVAL;
+  if (a.kind != OPTR_MASK_NONE && a.kind != OPTR_MASK_COIN && a.kind != OPTR_MASK_BITMAP)
+    return OPTR_EINVAL;
+  a.drop_prob = ms ? ms->drop_prob : 0.0;
+  if (a.kind == OPTR_MASK_COIN) {
+    for (int s = 0; s < n; ++s) {
+      uint64_t ent[2] = {ms->seed, (uint64_t)s};
+      Pcg p = pcg_from_u64s(ent, 2);
+      a.coin_state[s] = p.state;
+      a.coin_inc[s] = p.inc;
+    }
+  }
+  a.dst_lo = dst_lo;
+  a.dst_hi = dst_hi;
+  a.mask_threads = (int64_t)(dst_hi - dst_lo) * 2 * (n - 1) * a.pw;
+  a.counts = counts;
+  *bitmap_for_consumers = a.kind == OPTR_MASK_BITMAP ? a.bitmap_in : bitmap_ws;
+  return OPTR_OK;
+}
+
+int check_common(int n, int64_t L, int dtype_in, int dtype_out, const optr_mask_spec* ms) {
+  if (n < 2 || n > OPTR_MAX_WORKERS) return OPTR_EINVAL;  // schedule.py:21-22
+  if (L < 0) return OPTR_EINVAL;
+  if ((dtype_in != OPTR_F32 && dtype_in != OPTR_BF16) || (dtype_out != OPTR_F32 && dtype_out != OPTR_BF16))
+    return OPTR_EINVAL;
+  int epp = ms ? ms->epp : 350;
+  if (epp <= 0) return OPTR_EINVAL;
+  if (ms && ms->kind == OPTR_MASK_COIN && !(ms->drop_prob >= 0.0 && ms->drop_prob <= 1.0)) return OPTR_EINVAL;
+  return OPTR_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+// ------------------------------------------------------------ host helpers
+uint64_t optr_derive_seed(uint64_t job_seed, uint64_t bucket_id, uint64_t generation) {
+  return derive_seed(job_seed, bucket_id, generation);
+}
+
+uint64_t optr_pcg64_output(const uint64_t* entropy, int n_entropy, uint64_t k) {
+  Pcg p = pcg_from_u64s(entropy, n_entropy);
+  return pcg_output_at(p, k);
+}
+
+int64_t optr_next_pow2(int64_t n) { return next_pow2_i(n); }
+
+int64_t optr_mask_words(int64_t dim, int n, int epp) {
+  if (n < 1 || epp <= 0 || dim < 0) return -1;
+  return mask_words(dim, n, epp);
+}
+
+int optr_masks_host(uint32_t* bm, int64_t dim, int n, int rotation, uint64_t seed, double p, int epp) {
+  if (n < 2 || n > OPTR_MAX_WORKERS || epp <= 0 || dim < 0 || !bm) return OPTR_EINVAL;
+  int r = ((rotation % n) + n) % n;
+  Shards sh = make_shards(dim, n);
+  int64_t pw = mask_words(dim, n, epp);
+  memset(bm, 0, sizeof(uint32_t) * (size_t)(2 * n * n * pw));
+  for (int src = 0; src < n; ++src) {
+    uint64_t ent[2] = {seed, (uint64_t)src};
+    Pcg g = pcg_from_u64s(ent, 2);
+    u128 s = g.state;
+    for (int stage = 0; stage < 2; ++stage) {
+      for (int o = 1; o < n; ++o) {
+        int dst = (src + o) % n;
+        int j = stage == 0 ? owned_shard(dst, r, n) : owned_shard(src, r, n);
+        int64_t np = n_packets(sh.len(j), epp);
+        uint32_t* row = bm + ((int64_t)(stage * n + dst) * n + src) * pw;
+        for (int64_t k = 0; k < np; ++k) {
+          bool keep = true;
+          if (p > 0) {  // datagram.py:122 draws only when drop_prob > 0
+            s = pcg_step(s, g.inc);
+            keep = !coin_drops(pcg_xsl_rr(s), p);
+          }
+          if (keep) row[k >> 5] |= 1u << (k & 31);
+        }
+      }
+    }
+  }
+  return OPTR_OK;
+}
+
+const char* optr_version(void) { return "optr 0.1 sm_100a"; }
+
+// ---------------------------------------------------------------- codec
+int optr_rht_signs(uint32_t* sign_bits, int64_t dim, uint64_t seed, void* stream) {
+  if (!is_pow2(dim) || !sign_bits) return OPTR_EINVAL;
+  bind_device(stream);
+  PrepArgs a;
+  memset(&a, 0, sizeof(a));
+  fill_sign_args(a, sign_bits, dim, seed);
+  return launch_prep(a, (cudaStream_t)stream);
+}
+
+int optr_fwht(float* v, int64_t dim, void* stream) {
+  if (!is_pow2(dim) || !v) return OPTR_EINVAL;  // hadamard.py:78-81
+  bind_device(stream);
+  SrcBuf b;
+  memset(&b, 0, sizeof(b));
+  b.y[0] = v;
+  SnkBuf s;
+  memset(&s, 0, sizeof(s));
+  s.y[0] = v;
+  s.scale = 1.f;
+  return run_transform(log2_exact(dim), true, 0, 1, b, b, s, (cudaStream_t)stream);
+}
+
+int optr_rht_encode(const void* x, int dtype_in, int64_t L, float* y, int64_t dim, uint64_t seed,
+                    void* stream) {
+  if (!is_pow2(dim) || L > dim || L < 0 || !y || (L > 0 && !x)) return OPTR_EINVAL;  // hadamard.py:45-48,96-97
+  if (dtype_in != OPTR_F32 && dtype_in != OPTR_BF16) return OPTR_EINVAL;
+  bind_device(stream);
+  cudaStream_t st = (cudaStream_t)stream;
+  uint32_t* signs = nullptr;
+  size_t sbytes = (size_t)((dim + 31) / 32) * 4;
+  CK(cudaMallocAsync((void**)&signs, sbytes, st));
+  PrepArgs a;
+  memset(&a, 0, sizeof(a));
+  fill_sign_args(a, signs, dim, seed);
+  int rc = launch_prep(a, st);
+  if (!rc) {
+    SrcEncode src;
+    memset(&src, 0, sizeof(src));
+    src.x[0] = x;
+    src.dtype = dtype_in;
+    src.L = L;
+    src.signs = signs;
+    SrcBuf buf;
+    memset(&buf, 0, sizeof(buf));
+    buf.y[0] = y;
+    SnkBuf snk;
+    memset(&snk, 0, sizeof(snk));
+    snk.y[0] = y;
+    snk.scale = (float)(1.0 / sqrt((double)dim));
+    rc = run_transform(log2_exact(dim), true, 0, 1, src, buf, snk, st);
+  }
+  cudaFreeAsync(signs, st);
+  return rc;
+}
+
+int optr_rht_decode(const float* y, const uint8_t* mask, int64_t dim, int64_t L, uint64_t seed, void* out,
+                    int dtype_out, void* stream) {
+  if (!is_pow2(dim) || L > dim || L < 0 || !y || (L > 0 && !out)) return OPTR_EINVAL;
+  if (dtype_out != OPTR_F32 && dtype_out != OPTR_BF16) return OPTR_EINVAL;
+  bind_device(stream);
+  cudaStream_t st = (cudaStream_t)stream;
+  unsigned long long count = (unsigned long long)dim;
+  unsigned long long* dcount = nullptr;
+  if (mask) {
+    CK(cudaMallocAsync((void**)&dcount, sizeof(unsigned long long), st));
+    CK(cudaMemsetAsync(dcount, 0, sizeof(unsigned long long), st));
+    int64_t blocks = (dim + 255) / 256;
+    if (blocks > 4096) blocks = 4096;
+    {
+      KScope ks(OPTR_K_OTHER, st);
+      count_mask_kernel<<<(unsigned)blocks, 256, 0, st>>>(mask, dim, dcount);
+    }
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(&count, dcount, sizeof(count), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    cudaFreeAsync(dcount, st);
+  }
+  if (count == 0) return OPTR_EEMPTY;  // hadamard.py:117-118
+  uint32_t* signs = nullptr;
+  float* tmp = nullptr;
+  CK(cudaMallocAsync((void**)&signs, (size_t)((dim + 31) / 32) * 4, st));
+  CK(cudaMallocAsync((void**)&tmp, (size_t)dim * 4, st));
+  PrepArgs a;
+  memset(&a, 0, sizeof(a));
+  fill_sign_args(a, signs, dim, seed);
+  int rc = launch_prep(a, st);
+  if (!rc) {
+    SrcMasked src{y, mask};
+    SrcBuf buf;
+    memset(&buf, 0, sizeof(buf));
+    buf.y[0] = tmp;
+    SnkDecode snk;
+    memset(&snk, 0, sizeof(snk));
+    snk.out[0] = out;
+    snk.dtype = dtype_out;
+    snk.L = L;
+    snk.signs = signs;
+    snk.count_extra = nullptr;
+    snk.count_base[0] = (int64_t)count;
+    snk.dim = (double)dim;
+    rc = run_transform(log2_exact(dim), false, 0, 1, src, buf, snk, st);
+  }
+  cudaFreeAsync(tmp, st);
+  cudaFreeAsync(signs, st);
+  return rc;
+}
+
+// -------------------------------------------------- TAR, n workers, one GPU
+struct LocalLayout {
+  size_t y, a, signs, bitmap, counts, total;
+  int64_t dim, smax, pw;
+};
+
+static LocalLayout local_layout(int n, int64_t L, int ht, int epp) {
+  LocalLayout l;
+  l.dim = ht ? next_pow2_i(L) : L;
+  Shards sh = make_shards(l.dim, n);
+  l.smax = sh.base + (sh.extra ? 1 : 0);
+  l.pw = mask_words(l.dim, n, epp);
+  size_t off = 0;
+  l.y = off;
+  off = align_up(off + (size_t)n * l.dim * 4, 256);
+  l.a = off;
+  off = align_up(off + (size_t)n * (l.smax > 0 ? l.smax : 1) * 4, 256);
+  l.signs = off;
+  off = align_up(off + (size_t)((l.dim + 31) / 32 + 2) * 4, 256);
+  l.bitmap = off;
+  off = align_up(off + (size_t)2 * n * n * l.pw * 4, 256);
+  l.counts = off;
+  off = align_up(off + (size_t)2 * n * 8, 256);
+  l.total = off;
+  return l;
+}
+
+size_t optr_tar_local_workspace(int n, int64_t L, int ht, int epp) {
+  if (n < 2 || n > OPTR_MAX_WORKERS || L < 0 || epp <= 0) return 0;
+  return local_layout(n, L, ht, epp).total;
+}
+
+int optr_tar_local(const void* const* x, void* const* out, int n, int64_t L, int dtype_in, int dtype_out,
+                   uint64_t job_seed, uint64_t bucket_id, uint64_t generation, int rotation, int ht,
+                   const optr_mask_spec* masks, void* workspace, size_t workspace_bytes,
+                   uint64_t* received_out, uint8_t* got_out, void* stream) {
+  int rc = check_common(n, L, dtype_in, dtype_out, masks);
+  if (rc) return rc;
+  if (!x || !out || !workspace) return OPTR_EINVAL;
+  int epp = masks ? masks->epp : 350;
+  LocalLayout lay = local_layout(n, L, ht, epp);
+  if (workspace_bytes < lay.total) return OPTR_EINVAL;
+  if (L == 0) return OPTR_OK;
+  bind_device(stream);
+  cudaStream_t st = (cudaStream_t)stream;
+  char* ws = (char*)workspace;
+  const int64_t dim = lay.dim;
+  const int r = ((rotation % n) + n) % n;
+  float* Y = (float*)(ws + lay.y);
+  float* A = (float*)(ws + lay.a);
+  uint32_t* signs = (uint32_t*)(ws + lay.signs);
+  uint32_t* bitmap = (uint32_t*)(ws + lay.bitmap);
+  unsigned long long* counts = (unsigned long long*)(ws + lay.counts);
+
+  // 1. signs + masks + counts
+  CK(cudaMemsetAsync(counts, 0, (size_t)2 * n * 8, st));
+  PrepArgs pa;
+  memset(&pa, 0, sizeof(pa));
+  if (ht) fill_sign_args(pa, signs, dim, derive_seed(job_seed, bucket_id, generation));
+  const uint32_t* cbits = nullptr;
+  if ((rc = setup_masks(pa, masks, dim, n, r, epp, bitmap, counts, 0, n, &cbits))) return rc;
+  if ((rc = launch_prep(pa, st))) return rc;
+  MaskView mv{cbits, pa.pw, n, epp};
+  Shards sh = make_shards(dim, n);
+
+  // 2. wire vectors
+  const float* Yw[kMaxW];
+  if (ht) {
+    SrcEncode src;
+    memset(&src, 0, sizeof(src));
+    src.dtype = dtype_in;
+    src.L = L;
+    src.signs = signs;
+    SrcBuf buf;
+    memset(&buf, 0, sizeof(buf));
+    SnkBuf snk;
+    memset(&snk, 0, sizeof(snk));
+    for (int w = 0; w < n; ++w) {
+      src.x[w] = x[w];
+      buf.y[w] = snk.y[w] = Y + (size_t)w * dim;
+      Yw[w] = Y + (size_t)w * dim;
+    }
+    snk.scale = (float)(1.0 / sqrt((double)dim));
+    if ((rc = run_transform(log2_exact(dim), true, 0, n, src, buf, snk, st, OPTR_K_ENC_FIRST))) return rc;
+  } else {
+    for (int w = 0; w < n; ++w) {
+      if (dtype_in == OPTR_F32) {
+        Yw[w] = (const float*)x[w];
+      } else {
+        float* yw = Y + (size_t)w * dim;
+        KScope ks(OPTR_K_OTHER, st);
+        cast_copy_kernel<<<1184, 256, 0, st>>>(x[w], dtype_in, yw, dim);
+        CK(cudaGetLastError());
+        Yw[w] = yw;
+      }
+    }
+  }
+
+  // 3. stage 1: owner means
+  AggArgs ag;
+  memset(&ag, 0, sizeof(ag));
+  for (int w = 0; w < n; ++w) {
+    ag.Y[w] = Yw[w];
+    ag.A[w] = A + (size_t)w * lay.smax;
+  }
+  ag.sh = sh;
+  ag.n = n;
+  ag.r = r;
+  ag.m = mv;
+  ag.owner_base = 0;
+  if (lay.smax > 0) {
+    int64_t blocks = (lay.smax + 255) / 256;
+    if (blocks > 2368) blocks = 2368;
+    KScope ks(OPTR_K_AGG, st);
+    aggregate_kernel<<<dim3((unsigned)blocks, n), 256, 0, st>>>(ag);
+    CK(cudaGetLastError());
+  }
+
+  // 4. stage 2 receive (+ decode)
+  SrcGather ga;
+  memset(&ga, 0, sizeof(ga));
+  for (int w = 0; w < n; ++w) ga.A[w] = ag.A[w];
+  ga.sh = sh;
+  ga.n = n;
+  ga.r = r;
+  ga.m = mv;
+  ga.got = got_out;
+  ga.dim = dim;
+  if (ht) {
+    SrcBuf buf;
+    memset(&buf, 0, sizeof(buf));
+    SnkDecode snk;
+    memset(&snk, 0, sizeof(snk));
+    for (int w = 0; w < n; ++w) {
+      buf.y[w] = Y + (size_t)w * dim;  // encoded vectors are dead after stage 1
+      snk.out[w] = out[w];
+      snk.count_base[w] = sh.len(owned_shard(w, r, n));
+    }
+    snk.dtype = dtype_out;
+    snk.L = L;
+    snk.signs = signs;
+    snk.count_extra = counts + n;  // stage-2 row
+    snk.count_stride = 1;
+    snk.dim = (double)dim;
+    if ((rc = run_transform(log2_exact(dim), false, 0, n, ga, buf, snk, st, OPTR_K_DEC_FIRST))) return rc;
+  } else {
+    AsmArgs as;
+    memset(&as, 0, sizeof(as));
+    as.gather = ga;
+    for (int w = 0; w < n; ++w) as.out[w] = out[w];
+    as.dtype = dtype_out;
+    as.L = L;
+    int64_t blocks = (L + 255) / 256;
+    if (blocks > 4736) blocks = 4736;
+    KScope ks(OPTR_K_ASSEMBLE, st);
+    assemble_kernel<<<dim3((unsigned)blocks, n), 256, 0, st>>>(as);
+    CK(cudaGetLastError());
+  }
+  if (received_out) CK(cudaMemcpyAsync(received_out, counts, (size_t)2 * n * 8, cudaMemcpyDeviceToDevice, st));
+  return OPTR_OK;
+}
+
+// ------------------------------------------------ TAR, one worker per GPU
+struct optr_comm_s {
+  int rank, n, epp, device;
+  int64_t max_dim;
+  size_t off_flags, off_y, off_a, sym_bytes;
+  char* sym;
+  char* peer[OPTR_MAX_WORKERS];
+  bool opened[OPTR_MAX_WORKERS];
+  char* local;  // signs | bitmap | counts
+  size_t off_signs, off_bitmap, off_counts, local_bytes;
+  unsigned long long epoch;
+};
+
+size_t optr_comm_handle_bytes(void) { return sizeof(cudaIpcMemHandle_t); }
+
+int optr_comm_create(optr_comm* out, int device, int rank, int n, int64_t max_len, int epp) {
+  if (!out || n < 2 || n > OPTR_MAX_WORKERS || rank < 0 || rank >= n || max_len < 1 || epp <= 0 ||
+      device < 0)
+    return OPTR_EINVAL;
+  CK(cudaSetDevice(device));
+  optr_comm c = (optr_comm)calloc(1, sizeof(optr_comm_s));
+  if (!c) return OPTR_ENOMEM;
+  c->rank = rank;
+  c->n = n;
+  c->epp = epp;
+  c->device = device;
+  c->max_dim = next_pow2_i(max_len);
+  Shards sh = make_shards(c->max_dim, n);
+  int64_t smax = sh.base + (sh.extra ? 1 : 0);
+  size_t off = 0;
+  c->off_flags = off;
+  off = align_up(off + OPTR_MAX_WORKERS * 8, 256);
+  c->off_y = off;
+  off = align_up(off + (size_t)c->max_dim * 4, 256);
+  c->off_a = off;
+  off = align_up(off + (size_t)smax * 4, 256);
+  c->sym_bytes = off;
+  int64_t pw = mask_words(c->max_dim, n, 1);  // epp >= 1 bound
+  off = 0;
+  c->off_signs = off;
+  off = align_up(off + (size_t)((c->max_dim + 31) / 32 + 2) * 4, 256);
+  c->off_bitmap = off;
+  off = align_up(off + (size_t)2 * n * n * pw * 4, 256);
+  c->off_counts = off;
+  off = align_up(off + (size_t)2 * n * 8, 256);
+  c->local_bytes = off;
+  if (cudaMalloc((void**)&c->sym, c->sym_bytes) != cudaSuccess ||
+      cudaMalloc((void**)&c->local, c->local_bytes) != cudaSuccess) {
+    cudaFree(c->sym);
+    free(c);
+    return OPTR_ENOMEM;
+  }
+  CK(cudaMemset(c->sym, 0, c->sym_bytes));
+  CK(cudaDeviceSynchronize());
+  c->peer[rank] = c->sym;
+  *out = c;
+  return OPTR_OK;
+}
+
+int optr_comm_get_handle(optr_comm c, void* handle_out) {
+  if (!c || !handle_out) return OPTR_EINVAL;
+  cudaIpcMemHandle_t h;
+  CK(cudaIpcGetMemHandle(&h, c->sym));
+  memcpy(handle_out, &h, sizeof(h));
+  return OPTR_OK;
+}
+
+int optr_comm_open(optr_comm c, const void* all_handles) {
+  if (!c || !all_handles) return OPTR_EINVAL;
+  CK(cudaSetDevice(c->device));
+  const char* hb = (const char*)all_handles;
+  for (int i = 0; i < c->n; ++i) {
+    if (i == c->rank || c->opened[i]) continue;
+    cudaIpcMemHandle_t h;
+    memcpy(&h, hb + (size_t)i * sizeof(h), sizeof(h));
+    void* p = nullptr;
+    CK(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+    c->peer[i] = (char*)p;
+    c->opened[i] = true;
+  }
+  return OPTR_OK;
+}
+
+int optr_comm_destroy(optr_comm c) {
+  if (!c) return OPTR_EINVAL;
+  cudaSetDevice(c->device);
+  cudaDeviceSynchronize();
+  for (int i = 0; i < c->n; ++i)
+    if (c->opened[i]) cudaIpcCloseMemHandle(c->peer[i]);
+  cudaFree(c->sym);
+  cudaFree(c->local);
+  free(c);
+  return OPTR_OK;
+}
+
+struct FlagPtrs {
+  unsigned long long* f[OPTR_MAX_WORKERS];
+};
+
+__global__ void barrier_kernel2(FlagPtrs peers, unsigned long long* mine, int rank, int n,
+                                unsigned long long epoch) {
+  int i = threadIdx.x;
+  if (i >= n || i == rank) return;
+  __threadfence_system();
+  unsigned long long* dst = peers.f[i] + rank;
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(dst), "l"(epoch) : "memory");
+  unsigned long long v;
+  do {
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(mine + i) : "memory");
+  } while (v < epoch);
+}
+
+int optr_comm_barrier(optr_comm c, void* stream) {
+  if (!c) return OPTR_EINVAL;
+  FlagPtrs fp;
+  memset(&fp, 0, sizeof(fp));
+  for (int i = 0; i < c->n; ++i) {
+    if (!c->peer[i]) return OPTR_EINVAL;
+    fp.f[i] = (unsigned long long*)(c->peer[i] + c->off_flags);
+  }
+  c->epoch += 1;
+  KScope ks(OPTR_K_BARRIER, (cudaStream_t)stream);
+  barrier_kernel2<<<1, 32, 0, (cudaStream_t)stream>>>(fp, (unsigned long long*)(c->sym + c->off_flags),
+                                                      c->rank, c->n, c->epoch);
+  CK(cudaGetLastError());
+  return OPTR_OK;
+}
+
+int optr_tar(optr_comm c, const void* x, void* out, int64_t L, int dtype_in, int dtype_out,
+             uint64_t job_seed, uint64_t bucket_id, uint64_t generation, int rotation, int ht,
+             const optr_mask_spec* masks,
+             uint64_t* received_out, void* stream) {
+  if (!c) return OPTR_EINVAL;
+  int n = c->n;
+  int rc = check_common(n, L, dtype_in, dtype_out, masks);
+  if (rc) return rc;
+  int epp = masks ? masks->epp : 350;
+  int64_t dim = ht ? next_pow2_i(L) : L;
+  if (dim > c->max_dim) return OPTR_EINVAL;
+  if (L == 0) return OPTR_OK;
+  if (L > 0 && (!x || !out)) return OPTR_EINVAL;
+  for (int i = 0; i < n; ++i)
+    if (!c->peer[i]) return OPTR_EINVAL;  // optr_comm_open not called
+  CK(cudaSetDevice(c->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  const int me = c->rank;
+  const int r = ((rotation % n) + n) % n;
+  uint32_t* signs = (uint32_t*)(c->local + c->off_signs);
+  uint32_t* bitmap = (uint32_t*)(c->local + c->off_bitmap);
+  unsigned long long* counts = (unsigned long long*)(c->local + c->off_counts);
+  float* Yp[kMaxW];
+  float* Ap[kMaxW];
+  for (int i = 0; i < n; ++i) {
+    Yp[i] = (float*)(c->peer[i] + c->off_y);
+    Ap[i] = (float*)(c->peer[i] + c->off_a);
+  }
+  Shards sh = make_shards(dim, n);
+
+  CK(cudaMemsetAsync(counts, 0, (size_t)2 * n * 8, st));
+  PrepArgs pa;
+  memset(&pa, 0, sizeof(pa));
+  if (ht) fill_sign_args(pa, signs, dim, derive_seed(job_seed, bucket_id, generation));
+  const uint32_t* cbits = nullptr;
+  if ((rc = setup_masks(pa, masks, dim, n, r, epp, bitmap, counts, me, me + 1, &cbits))) return rc;
+  if ((rc = launch_prep(pa, st))) return rc;
+  MaskView mv{cbits, pa.pw, n, epp};
+
+  // encode into my symmetric wire buffer
+  if (ht) {
+    SrcEncode src;
+    memset(&src, 0, sizeof(src));
+    src.x[me] = x;
+    src.dtype = dtype_in;
+    src.L = L;
+    src.signs = signs;
+    SrcBuf buf;
+    memset(&buf, 0, sizeof(buf));
+    buf.y[me] = Yp[me];
+    SnkBuf snk;
+    memset(&snk, 0, sizeof(snk));
+    snk.y[me] = Yp[me];
+    snk.scale = (float)(1.0 / sqrt((double)dim));
+    if ((rc = run_transform(log2_exact(dim), true, me, 1, src, buf, snk, st, OPTR_K_ENC_FIRST))) return rc;
+  } else {
+    KScope ks(OPTR_K_OTHER, st);
+    cast_copy_kernel<<<1184, 256, 0, st>>>(x, dtype_in, Yp[me], dim);
+    CK(cudaGetLastError());
+  }
+  if ((rc = optr_comm_barrier(c, stream))) return rc;
+
+  // stage 1: pull my shard from every peer over NVLink, masked mean
+  AggArgs ag;
+  memset(&ag, 0, sizeof(ag));
+  for (int i = 0; i < n; ++i) {
+    ag.Y[i] = Yp[i];
+    ag.A[i] = Ap[i];
+  }
+  ag.sh = sh;
+  ag.n = n;
+  ag.r = r;
+  ag.m = mv;
+  ag.owner_base = me;
+  int64_t smax = sh.base + (sh.extra ? 1 : 0);
+  if (smax > 0) {
+    int64_t blocks = (smax + 255) / 256;
+    if (blocks > 2368) blocks = 2368;
+    KScope ks(OPTR_K_AGG, st);
+    aggregate_kernel<<<dim3((unsigned)blocks, 1), 256, 0, st>>>(ag);
+    CK(cudaGetLastError());
+  }
+  if ((rc = optr_comm_barrier(c, stream))) return rc;
+
+  // stage 2: pull every owner's aggregate over NVLink, fused into decode
+  SrcGather ga;
+  memset(&ga, 0, sizeof(ga));
+  for (int i = 0; i < n; ++i) ga.A[i] = Ap[i];
+  ga.sh = sh;
+  ga.n = n;
+  ga.r = r;
+  ga.m = mv;
+  ga.got = nullptr;
+  ga.dim = dim;
+  if (ht) {
+    SrcBuf buf;
+    memset(&buf, 0, sizeof(buf));
+    buf.y[me] = Yp[me];  // peers finished reading my wire vector (barrier 2)
+    SnkDecode snk;
+    memset(&snk, 0, sizeof(snk));
+    snk.out[me] = out;
+    snk.count_base[me] = sh.len(owned_shard(me, r, n));
+    snk.dtype = dtype_out;
+    snk.L = L;
+    snk.signs = signs;
+    snk.count_extra = counts + n;
+    snk.count_stride = 1;
+    snk.dim = (double)dim;
+    if ((rc = run_transform(log2_exact(dim), false, me, 1, ga, buf, snk, st, OPTR_K_DEC_FIRST))) return rc;
+  } else {
+    AsmArgs as;
+    memset(&as, 0, sizeof(as));
+    as.gather = ga;
+    as.out[me] = out;
+    as.dtype = dtype_out;
+    as.L = L;
+    as.worker_base = me;
+    int64_t blocks = (L + 255) / 256;
+    if (blocks > 4736) blocks = 4736;
+    KScope ks(OPTR_K_ASSEMBLE, st);
+    assemble_kernel<<<dim3((unsigned)blocks, 1), 256, 0, st>>>(as);
+    CK(cudaGetLastError());
+  }
+  if (received_out) {
+    CK(cudaMemcpyAsync(received_out, counts + me, 8, cudaMemcpyDeviceToDevice, st));
+    CK(cudaMemcpyAsync(received_out + 1, counts + n + me, 8, cudaMemcpyDeviceToDevice, st));
+  }
+  return OPTR_OK;
+}
+
+// ------------------------------------------------------ instrumentation
+int optr_timing_enable(int on) {
+  std::lock_guard<std::mutex> lk(g_tmu);
+  g_timing = on != 0;
+  return OPTR_OK;
+}
+
+int optr_timing_collect(double* ms_out, int64_t* launches_out) {
+  std::vector<TRec> recs;
+  {
+    std::lock_guard<std::mutex> lk(g_tmu);
+    recs.swap(g_trecs);
+  }
+  if (ms_out)
+    for (int i = 0; i < OPTR_K_CLASSES; ++i) ms_out[i] = 0.0;
+  if (launches_out)
+    for (int i = 0; i < OPTR_K_CLASSES; ++i) launches_out[i] = 0;
+  int rc = OPTR_OK;
+  for (auto& r : recs) {
+    float ms = 0.f;
+    if (cudaEventSynchronize(r.b) != cudaSuccess || cudaEventElapsedTime(&ms, r.a, r.b) != cudaSuccess)
+      rc = OPTR_ECUDA;
+    if (r.cls >= 0 && r.cls < OPTR_K_CLASSES) {
+      if (ms_out) ms_out[r.cls] += ms;
+      if (launches_out) launches_out[r.cls] += 1;
+    }
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+  }
+  return rc;
+}
+
+int64_t optr_launch_count(void) { return g_launches.load(); }
+
+}  // extern "C"

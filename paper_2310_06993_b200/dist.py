@@ -1,0 +1,116 @@
+"""One TAR worker per GPU: the multi-GPU drop-in for ``tar_allreduce``.
+
+The reference runs one ``tar_allreduce`` generator per node over a channel
+(``/root/reference/pkg/src/ubar/collectives.py:97-150`` driven by
+``datagram.py:85-207`` on real sockets).  Here each process owns one GPU and
+calls ``TarCommunicator.allreduce`` with its own bucket:
+
+* encode its bucket into its symmetric wire buffer (CUDA-IPC-mapped into
+  every peer);
+* device barrier (flags over NVLink);
+* stage 1: pull its owned shard from every peer's wire buffer over NVLink
+  and take the masked fp64 mean (collectives.py:113-125);
+* device barrier;
+* stage 2: pull every owner's aggregate over NVLink, masked, fused into the
+  first pass of its own decode (collectives.py:127-150, runner.py:248-256).
+
+torch.distributed (NCCL) only carries the one-time IPC handle exchange and
+host barriers; the data path is peer loads inside the kernels.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+from . import _lib
+from ._lib import check, lib
+from .collectives import MaskSpec
+
+
+def all_gather_bytes(blob: bytes, group=None, device=None) -> list:
+    """Exchange one equal-length byte blob per rank (rank order)."""
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    t = torch.tensor(list(blob), dtype=torch.uint8)
+    if device is not None:
+        t = t.to(device)
+    parts = [torch.empty_like(t) for _ in range(world)]
+    dist.all_gather(parts, t, group=group)
+    return [bytes(p.cpu().tolist()) for p in parts]
+
+
+def _dtype_code(t) -> int:
+    import torch
+
+    if t.dtype == torch.float32:
+        return _lib.OPTR_F32
+    if t.dtype == torch.bfloat16:
+        return _lib.OPTR_BF16
+    raise ValueError(f"unsupported dtype {t.dtype}")
+
+
+class TarCommunicator:
+    """Symmetric NVLink buffers for buckets of up to ``max_len`` entries."""
+
+    def __init__(self, max_len: int, epp: int = 350, group=None, device=None):
+        import torch
+        import torch.distributed as dist
+
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        self.device = torch.device(device) if device is not None else torch.device(
+            "cuda", torch.cuda.current_device())
+        self.max_len = int(max_len)
+        self.epp = int(epp)
+        h = ctypes.c_void_p()
+        check(lib().optr_comm_create(ctypes.byref(h), self.device.index, self.rank, self.world,
+                                     self.max_len, self.epp), "comm_create")
+        self._h = h
+        nb = int(lib().optr_comm_handle_bytes())
+        mine = (ctypes.c_char * nb)()
+        check(lib().optr_comm_get_handle(self._h, mine), "comm_get_handle")
+        blobs = all_gather_bytes(bytes(mine), group, self.device)
+        allb = b"".join(blobs)
+        check(lib().optr_comm_open(self._h, allb), "comm_open")
+        dist.barrier(group)
+
+    def allreduce(self, x, out, *, rotation: int, ht: bool = True, job_seed: int = 0,
+                  generation: int = 0, bucket_id: int | None = None, masks: MaskSpec | None = None,
+                  received=None, stream=None):
+        """This rank's part of one TAR(+RHT) generation.  ``x``/``out`` are
+        this rank's CUDA buffers (fp32/bf16).  ``received``: optional CUDA
+        int64[2] for (stage-1, stage-2) received entries."""
+        import torch
+
+        if self._h is None:
+            raise RuntimeError("communicator closed")
+        if len(x) != len(out) or len(x) > self.max_len:
+            raise ValueError("bucket longer than the communicator's max_len")
+        masks = masks or MaskSpec.none(self.epp * 4)
+        if masks.epp != self.epp and masks.kind != "none":
+            pass  # epp is per call; buffers only bound the packet count
+        spec = masks.to_c()
+        st = stream if stream is not None else torch.cuda.current_stream(self.device)
+        check(lib().optr_tar(self._h, x.data_ptr(), out.data_ptr(), len(x), _dtype_code(x), _dtype_code(out),
+                             int(job_seed), int(generation % 65536 if bucket_id is None else bucket_id),
+                             int(generation), int(rotation), int(bool(ht)), ctypes.byref(spec),
+                             received.data_ptr() if received is not None else None, st.cuda_stream),
+              "tar")
+        return out
+
+    def close(self):
+        if self._h is not None:
+            import torch
+
+            torch.cuda.synchronize(self.device)
+            lib().optr_comm_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
