@@ -6,6 +6,7 @@
 #include <string.h>
 
 #include <atomic>
+#include <type_traits>
 #include <mutex>
 #include <vector>
 
@@ -100,49 +101,104 @@ int plan_passes(int n, PassGeom* out, bool encode_order) {
   PassGeom p[3];
   int np = 0;
   if (n <= kContigBits) {
-    p[np++] = PassGeom{0, n, 0};
+    p[np++] = PassGeom{0, n, 0, 1};
   } else {
     int rest = n - kContigBits;
     if (rest <= 12) {
-      p[np++] = PassGeom{kContigBits, rest, kColBits};
+      p[np++] = PassGeom{kContigBits, rest, kColBits, 0};
     } else {
       int k1 = rest / 2;
-      p[np++] = PassGeom{kContigBits + k1, rest - k1, kColBits};
-      p[np++] = PassGeom{kContigBits, k1, kColBits};
+      p[np++] = PassGeom{kContigBits + k1, rest - k1, kColBits, 0};
+      p[np++] = PassGeom{kContigBits, k1, kColBits, 0};
     }
-    p[np++] = PassGeom{0, kContigBits, 0};
+    p[np++] = PassGeom{0, kContigBits, 0, 0};
   }
-  for (int i = 0; i < np; ++i) out[i] = encode_order ? p[i] : p[np - 1 - i];
+  for (int i = 0; i < np; ++i) {
+    p[i].ntiles = (1LL << n) >> (p[i].cb + p[i].ks);
+    out[i] = encode_order ? p[i] : p[np - 1 - i];
+  }
   return np;
 }
 
 std::mutex g_attr_mu;
 
+// one-time per-device setup: PCG jump table in constant memory
+int ensure_device_init() {
+  static bool done[64] = {false};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(g_attr_mu);
+  if (!done[dev & 63]) {
+    JumpTable t = make_jump_table();
+    CK(cudaMemcpyToSymbol(c_jump, &t, sizeof(t)));
+    done[dev & 63] = true;
+  }
+  return OPTR_OK;
+}
+
+template <class K>
+int set_smem_attr(K kernel, size_t smem) {
+  if (smem <= 48 * 1024) return OPTR_OK;
+  CK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  return OPTR_OK;
+}
+
+constexpr int64_t kMaxGrid = 148 * 16;
+
+template <int T, int CB, class Src, class Snk>
+int launch_rtile(int cls, const PassGeom& pg, int worker_base, int nworkers, const Src& src, const Snk& snk,
+                 cudaStream_t st) {
+  const size_t smem = sizeof(float) << T;
+  int rc = set_smem_attr(rtile_kernel<T, CB, Src, Snk>, smem);
+  if (rc) return rc;
+  const int64_t gx = pg.ntiles < kMaxGrid ? pg.ntiles : kMaxGrid;
+  KScope ks(cls, st);
+  rtile_kernel<T, CB, Src, Snk><<<dim3((unsigned)gx, (unsigned)nworkers), 1 << (T - 5), smem, st>>>(
+      pg, worker_base, src, snk);
+  CK(cudaGetLastError());
+  return OPTR_OK;
+}
+
+template <class Src, class Snk>
+int launch_smem(int cls, const PassGeom& pg, int worker_base, int nworkers, const Src& src, const Snk& snk,
+                cudaStream_t st) {
+  const int nelem = 1 << (pg.cb + pg.ks);
+  const size_t smem = (size_t)nelem * sizeof(float);
+  int rc = set_smem_attr(smem_tile_kernel<Src, Snk>, smem);
+  if (rc) return rc;
+  const int64_t gx = pg.ntiles < kMaxGrid ? pg.ntiles : kMaxGrid;
+  int threads = nelem / 32;
+  if (threads < 32) threads = 32;
+  if (threads > 256) threads = 256;
+  KScope ks(cls, st);
+  smem_tile_kernel<Src, Snk><<<dim3((unsigned)gx, (unsigned)nworkers), threads, smem, st>>>(pg, worker_base, src,
+                                                                                            snk);
+  CK(cudaGetLastError());
+  return OPTR_OK;
+}
+
+template <class S>
+constexpr bool kStridedSrc = std::is_same<S, SrcEncode>::value || std::is_same<S, SrcBuf>::value;
+
 template <class Src, class Snk>
 int launch_pass(int cls, const PassGeom& pg, int nlog, int worker_base, int nworkers, const Src& src,
                 const Snk& snk, cudaStream_t st) {
-  const int nelem = 1 << (pg.cb + pg.ks);
-  const int64_t ntiles = (1LL << nlog) >> (pg.cb + pg.ks);
-  int threads = nelem / 32;
-  if (threads < 32) threads = 32;
-  if (threads > 1024) threads = 1024;
-  const size_t smem = (size_t)nelem * sizeof(float);
-  if (smem > 48 * 1024) {
-    static bool done[64] = {false};
-    int dev = 0;
-    cudaGetDevice(&dev);
-    std::lock_guard<std::mutex> lk(g_attr_mu);
-    if (!done[dev & 63]) {
-      CK(cudaFuncSetAttribute(fwht_pass_kernel<Src, Snk>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              128 * 1024));
-      done[dev & 63] = true;
+  (void)nlog;
+  const int T = pg.cb + pg.ks;
+  if (pg.cb == 0 && T == 13) return launch_rtile<13, 0>(cls, pg, worker_base, nworkers, src, snk, st);
+  if constexpr (kStridedSrc<Src>) {
+    if (pg.cb == 3) {
+      switch (T) {
+        case 11: return launch_rtile<11, 3>(cls, pg, worker_base, nworkers, src, snk, st);
+        case 12: return launch_rtile<12, 3>(cls, pg, worker_base, nworkers, src, snk, st);
+        case 13: return launch_rtile<13, 3>(cls, pg, worker_base, nworkers, src, snk, st);
+        case 14: return launch_rtile<14, 3>(cls, pg, worker_base, nworkers, src, snk, st);
+        case 15: return launch_rtile<15, 3>(cls, pg, worker_base, nworkers, src, snk, st);
+        default: break;
+      }
     }
   }
-  dim3 grid((unsigned)ntiles, (unsigned)nworkers);
-  KScope ks(cls, st);
-  fwht_pass_kernel<Src, Snk><<<grid, threads, smem, st>>>(pg, worker_base, src, snk);
-  CK(cudaGetLastError());
-  return OPTR_OK;
+  return launch_smem(cls, pg, worker_base, nworkers, src, snk, st);
 }
 
 // Run the pass list with a fused first-pass source and last-pass sink; the
@@ -165,6 +221,29 @@ int run_transform(int nlog, bool encode_order, int worker_base, int nworkers, co
   return launch_pass(c_last, ps[np - 1], nlog, worker_base, nworkers, buf, snk, st);
 }
 
+
+// float4 path of the aggregate needs every shard offset and buffer 16B-aligned
+bool agg_vec_ok(const AggArgs& a) {
+  if (a.sh.extra != 0 || (a.sh.base & 3) != 0) return false;
+  for (int i = 0; i < a.n; ++i)
+    if (((uintptr_t)a.Y[i] & 15) || ((uintptr_t)a.A[i] & 15)) return false;
+  return true;
+}
+
+int launch_aggregate(const AggArgs& ag, int nowners, int64_t smax, cudaStream_t st) {
+  if (smax <= 0) return OPTR_OK;
+  int64_t blocks = (smax / 4 + 255) / 256;
+  if (blocks < 1) blocks = 1;
+  if (blocks > kMaxGrid) blocks = kMaxGrid;
+  KScope ks(OPTR_K_AGG, st);
+  if (agg_vec_ok(ag))
+    aggregate_kernel<true><<<dim3((unsigned)blocks, nowners), 256, 0, st>>>(ag);
+  else
+    aggregate_kernel<false><<<dim3((unsigned)blocks, nowners), 256, 0, st>>>(ag);
+  CK(cudaGetLastError());
+  return OPTR_OK;
+}
+
 Pcg sign_pcg(uint64_t seed) { return pcg_from_u64s(&seed, 1); }
 
 void fill_sign_args(PrepArgs& a, uint32_t* signs, int64_t dim, uint64_t seed) {
@@ -173,12 +252,14 @@ void fill_sign_args(PrepArgs& a, uint32_t* signs, int64_t dim, uint64_t seed) {
   a.dim = dim;
   a.sign_state = p.state;
   a.sign_inc = p.inc;
-  a.sign_threads = (dim + 63) / 64;
+  a.sign_threads = (dim + kSignsPerThread - 1) / kSignsPerThread;
 }
 
 int launch_prep(const PrepArgs& a, cudaStream_t st) {
   int64_t total = a.sign_threads + a.mask_threads;
   if (total == 0) return OPTR_OK;
+  int rc = ensure_device_init();
+  if (rc) return rc;
   int64_t blocks = (total + 255) / 256;
   KScope ks(OPTR_K_PREP, st);
   prep_kernel<<<(unsigned)blocks, 256, 0, st>>>(a);
@@ -508,13 +589,7 @@ int optr_tar_local(const void* const* x, void* const* out, int n, int64_t L, int
   ag.r = r;
   ag.m = mv;
   ag.owner_base = 0;
-  if (lay.smax > 0) {
-    int64_t blocks = (lay.smax + 255) / 256;
-    if (blocks > 2368) blocks = 2368;
-    KScope ks(OPTR_K_AGG, st);
-    aggregate_kernel<<<dim3((unsigned)blocks, n), 256, 0, st>>>(ag);
-    CK(cudaGetLastError());
-  }
+  if ((rc = launch_aggregate(ag, n, lay.smax, st))) return rc;
 
   // 4. stage 2 receive (+ decode)
   SrcGather ga;
@@ -763,13 +838,7 @@ int optr_tar(optr_comm c, const void* x, void* out, int64_t L, int dtype_in, int
   ag.m = mv;
   ag.owner_base = me;
   int64_t smax = sh.base + (sh.extra ? 1 : 0);
-  if (smax > 0) {
-    int64_t blocks = (smax + 255) / 256;
-    if (blocks > 2368) blocks = 2368;
-    KScope ks(OPTR_K_AGG, st);
-    aggregate_kernel<<<dim3((unsigned)blocks, 1), 256, 0, st>>>(ag);
-    CK(cudaGetLastError());
-  }
+  if ((rc = launch_aggregate(ag, 1, smax, st))) return rc;
   if ((rc = optr_comm_barrier(c, stream))) return rc;
 
   // stage 2: pull every owner's aggregate over NVLink, fused into decode

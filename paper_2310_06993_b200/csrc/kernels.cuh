@@ -3,10 +3,13 @@
 //   prep_kernel       Rademacher sign bits (hadamard.py:49-51), drop-mask packet
 //                     bitmaps (datagram.py:70-72,117-124 coin or caller bitmaps),
 //                     per-(stage,dst) received counts (simdriver.py:328-341).
-//   fwht_pass_kernel  one tile pass of the Sylvester FWHT (hadamard.py:76-90),
-//                     H_D = prod of passes over disjoint index-bit ranges, with
-//                     the encode sign/pad/cast fused into the first pass and the
-//                     decode gather/mask/scale/sign/truncate fused into the ends.
+//   rtile_kernel      one pass of the Sylvester FWHT (hadamard.py:76-90) over a
+//                     2^T-entry tile held in registers (32 per thread) with two
+//                     shared-memory transposes; H_D is the product of passes over
+//                     disjoint index-bit ranges.  The encode sign/pad/cast is fused
+//                     into the first pass, the decode gather/mask/scale/sign/
+//                     truncate/cast into the first and last passes.
+//   smem_tile_kernel  the same for small tiles (D < 2^10), shared-memory rounds.
 //   aggregate_kernel  TAR stage-1 owner mean (collectives.py:77-94,125): fp64
 //                     accumulate in ascending node order under stage-1 masks.
 //   assemble_kernel   TAR stage-2 assembly without RHT (collectives.py:140-150).
@@ -33,10 +36,13 @@ struct Shards {
   __host__ __device__ __forceinline__ int64_t off(int j) const {
     return (int64_t)j * base + (j < extra ? j : extra);
   }
+  // shard containing entry g (g < total): estimate in double, then correct
   __host__ __device__ __forceinline__ int of(int64_t g) const {
-    int64_t big = extra * (base + 1);
-    if (g < big) return (int)(g / (base + 1));
-    return (int)(extra + (g - big) / base);
+    int j = (int)((double)g / (double)(base + 1));
+    if (j > n - 1) j = n - 1;
+    while (j > 0 && off(j) > g) --j;
+    while (j < n - 1 && off(j + 1) <= g) ++j;
+    return j;
   }
 };
 
@@ -64,19 +70,69 @@ struct MaskView {
   int64_t pw;  // u32 words per pair
   int n;
   int epp;
-  __device__ __forceinline__ bool get(int stage, int dst, int src, int64_t pkt) const {
-    const uint32_t* p = bits + ((int64_t)(stage * n + dst) * n + src) * pw;
-    return (__ldg(p + (pkt >> 5)) >> (pkt & 31)) & 1u;
+  __device__ __forceinline__ const uint32_t* row(int stage, int dst, int src) const {
+    return bits + ((int64_t)(stage * n + dst) * n + src) * pw;
   }
 };
 
+__device__ __forceinline__ bool row_bit(const uint32_t* row, uint32_t pkt) {
+  return (__ldg(row + (pkt >> 5)) >> (pkt & 31)) & 1u;
+}
+
+// packet index of entries e..e+3 of a shard (epp = entries per packet)
+struct Pkt4 {
+  uint32_t p[4];
+};
+__device__ __forceinline__ Pkt4 pkt4(uint32_t e, uint32_t epp) {
+  Pkt4 r;
+  uint32_t p0 = e / epp;
+  uint32_t rem = e - p0 * epp;
+  if (epp >= 4) {
+#pragma unroll
+    for (int m = 0; m < 4; ++m) r.p[m] = p0 + (rem + m >= epp ? 1u : 0u);
+  } else {
+#pragma unroll
+    for (int m = 0; m < 4; ++m) r.p[m] = p0 + (rem + m) / epp;
+  }
+  return r;
+}
+
 // -------------------------------------------------------------------- prep
+// LCG jump table: advancing 2^i steps maps s -> A_i s + inc * G_i.
+struct JumpTable {
+  u128 a[64];
+  u128 g[64];
+};
+__constant__ JumpTable c_jump;
+
+inline JumpTable make_jump_table() {
+  JumpTable t;
+  u128 a = pcg_mult(), g = 1;
+  for (int i = 0; i < 64; ++i) {
+    t.a[i] = a;
+    t.g[i] = g;
+    g = g * (a + 1);
+    a = a * a;
+  }
+  return t;
+}
+
+// state after k steps from s (table-driven; uniform loop over the bit index
+// so the constant-bank reads broadcast across the warp)
+__device__ __forceinline__ u128 jump(u128 s, u128 inc, uint64_t k) {
+  int top = 64 - __clzll((long long)(k | 1));
+  for (int i = 0; i < top; ++i) {
+    if ((k >> i) & 1) s = c_jump.a[i] * s + inc * c_jump.g[i];
+  }
+  return s;
+}
+
 struct PrepArgs {
-  // signs
+  // signs: each thread writes 4 words = 128 signs = 64 PCG outputs
   uint32_t* signs;
   int64_t dim;
   u128 sign_state, sign_inc;
-  int64_t sign_threads;  // dim/64 rounded up (0 = no signs)
+  int64_t sign_threads;
   // masks
   int kind;
   int n, r, epp;
@@ -92,6 +148,8 @@ struct PrepArgs {
   unsigned long long* counts;  // [2][n] received entries per (stage,dst)
 };
 
+constexpr int kSignsPerThread = 128;
+
 // Running packet index of sender `src`'s first packet to `dst` in `stage`
 // (datagram.py:117-124 draws one coin per packet in send order: stage 1 to
 // dst = src+1..src+n-1 (schedule.py:67-78) then stage 2 the same order).
@@ -100,39 +158,38 @@ __device__ __forceinline__ uint64_t coin_base(const PrepArgs& a, int stage, int 
   int o = ((dst - src) % n + n) % n;
   uint64_t base = 0;
   if (stage == 0) {
-    for (int k = 1; k < o; ++k)
-      base += n_packets(a.sh.len(owned_shard((src + k) % n, a.r, n)), a.epp);
+    for (int k = 1; k < o; ++k) base += n_packets(a.sh.len(owned_shard((src + k) % n, a.r, n)), a.epp);
   } else {
-    for (int k = 1; k < n; ++k)
-      base += n_packets(a.sh.len(owned_shard((src + k) % n, a.r, n)), a.epp);
+    for (int k = 1; k < n; ++k) base += n_packets(a.sh.len(owned_shard((src + k) % n, a.r, n)), a.epp);
     base += (uint64_t)(o - 1) * n_packets(a.sh.len(owned_shard(src, a.r, n)), a.epp);
   }
   return base;
 }
 
-__global__ void prep_kernel(PrepArgs a) {
+__global__ void __launch_bounds__(256) prep_kernel(const __grid_constant__ PrepArgs a) {
   int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t < a.sign_threads) {
-    // 64 signs = 32 consecutive PCG64 outputs starting at output 32t
-    int64_t k0 = t * 64;
-    u128 s = pcg_advance(a.sign_state, a.sign_inc, (uint64_t)(t * 32) + 1);
-    uint32_t w0 = 0, w1 = 0;
-#pragma unroll 4
-    for (int i = 0; i < 32; ++i) {
-      uint64_t out = pcg_xsl_rr(s);
-      uint32_t b0 = (uint32_t)((out >> 31) & 1u), b1 = (uint32_t)(out >> 63);
-      int bit = 2 * i;
-      if (bit < 32) {
-        w0 |= (b0 << bit) | (b1 << (bit + 1));
-      } else {
-        w1 |= (b0 << (bit - 32)) | (b1 << (bit - 31));
+    // signs 128t .. 128t+127 = outputs 64t .. 64t+63; Lemire bit of u32 halves
+    u128 s = jump(a.sign_state, a.sign_inc, (uint64_t)t * 64 + 1);
+    const int64_t nwords = (a.dim + 31) >> 5;
+    const int64_t w0 = t * 4;
+#pragma unroll
+    for (int wd = 0; wd < 4; ++wd) {
+      uint32_t word = 0;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        uint64_t out = pcg_xsl_rr(s);
+        word |= (uint32_t)((out >> 31) & 1u) << (2 * i);
+        word |= (uint32_t)(out >> 63) << (2 * i + 1);
+        s = pcg_step(s, a.sign_inc);
       }
-      s = pcg_step(s, a.sign_inc);
+      int64_t wi = w0 + wd;
+      if (wi < nwords) {
+        int64_t valid = a.dim - wi * 32;  // zero the bits past dim
+        if (valid < 32) word &= (1u << valid) - 1u;
+        a.signs[wi] = word;
+      }
     }
-    int64_t wi = k0 >> 5;
-    int64_t nwords = (a.dim + 31) >> 5;
-    if (wi < nwords) a.signs[wi] = w0;
-    if (wi + 1 < nwords) a.signs[wi + 1] = w1;
     return;
   }
   t -= a.sign_threads;
@@ -158,7 +215,7 @@ __global__ void prep_kernel(PrepArgs a) {
   if (a.kind == OPTR_MASK_COIN) {
     if (cnt > 0) {
       uint64_t k = coin_base(a, stage, src, dst) + (uint64_t)p0;
-      u128 s = pcg_advance(a.coin_state[src], a.coin_inc[src], k + 1);
+      u128 s = jump(a.coin_state[src], a.coin_inc[src], k + 1);
       for (int i = 0; i < cnt; ++i) {
         if (!coin_drops(pcg_xsl_rr(s), a.drop_prob)) bits |= 1u << i;
         s = pcg_step(s, a.coin_inc[src]);
@@ -180,12 +237,457 @@ __global__ void prep_kernel(PrepArgs a) {
   }
 }
 
-// ------------------------------------------------------------ FWHT tiles
+// ------------------------------------------------------ element helpers
+__device__ __forceinline__ float load_elem(const void* p, int dtype, int64_t g) {
+  if (dtype == OPTR_BF16) return __bfloat162float(((const __nv_bfloat16*)p)[g]);
+  return ((const float*)p)[g];
+}
+__device__ __forceinline__ void store_elem(void* p, int dtype, int64_t g, float v) {
+  if (dtype == OPTR_BF16)
+    ((__nv_bfloat16*)p)[g] = __float2bfloat16_rn(v);
+  else
+    ((float*)p)[g] = v;
+}
+__device__ __forceinline__ float sgn(uint32_t word, int bit, float v) {
+  return ((word >> bit) & 1u) ? v : -v;
+}
+__device__ __forceinline__ float4 ld4(const float* p) { return *reinterpret_cast<const float4*>(p); }
+__device__ __forceinline__ float4 ldg4(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
+__device__ __forceinline__ void st4(float* p, float4 v) { *reinterpret_cast<float4*>(p) = v; }
+
+// --------------------------------------------------- sources and sinks
+// Each parameter struct binds to one worker (`bind(w)`) to give a small
+// register-resident view with load4 / store{1,2,4} on global indices.
+
+// pad(x) * signs   (hadamard.py:98-100)
+struct SrcEncode {
+  const void* x[kMaxW];
+  int dtype;
+  int64_t L;
+  const uint32_t* signs;
+  struct B {
+    const void* x;
+    int dtype;
+    int64_t L;
+    const uint32_t* signs;
+    __device__ __forceinline__ void begin_tile(int64_t, int64_t) {}
+    __device__ __forceinline__ float load1(int64_t g) const {
+      if (g >= L) return 0.f;
+      return sgn(__ldg(signs + (g >> 5)), (int)(g & 31), load_elem(x, dtype, g));
+    }
+    __device__ __forceinline__ float4 load4(int64_t g) const {
+      if (g + 4 <= L) {
+        float4 v;
+        if (dtype == OPTR_F32) {
+          v = ldg4((const float*)x + g);
+        } else {
+          uint2 u = __ldg(reinterpret_cast<const uint2*>((const __nv_bfloat16*)x + g));
+          __nv_bfloat162 a = *reinterpret_cast<__nv_bfloat162*>(&u.x);
+          __nv_bfloat162 b = *reinterpret_cast<__nv_bfloat162*>(&u.y);
+          float2 fa = __bfloat1622float2(a), fb = __bfloat1622float2(b);
+          v = make_float4(fa.x, fa.y, fb.x, fb.y);
+        }
+        uint32_t w = __ldg(signs + (g >> 5));
+        int b0 = (int)(g & 31);
+        v.x = sgn(w, b0, v.x);
+        v.y = sgn(w, b0 + 1, v.y);
+        v.z = sgn(w, b0 + 2, v.z);
+        v.w = sgn(w, b0 + 3, v.w);
+        return v;
+      }
+      return make_float4(load1(g), load1(g + 1), load1(g + 2), load1(g + 3));
+    }
+  };
+  __device__ __forceinline__ B bind(int w) const { return B{x[w], dtype, L, signs}; }
+};
+
+struct SrcBuf {
+  float* y[kMaxW];
+  struct B {
+    const float* y;
+    __device__ __forceinline__ void begin_tile(int64_t, int64_t) {}
+    __device__ __forceinline__ float load1(int64_t g) const { return y[g]; }
+    __device__ __forceinline__ float4 load4(int64_t g) const { return ld4(y + g); }
+  };
+  __device__ __forceinline__ B bind(int w) const { return B{y[w]}; }
+};
+
+// where(mask, y, 0) with a byte mask (hadamard.py:120)
+struct SrcMasked {
+  const float* y;
+  const uint8_t* mask;
+  struct B {
+    const float* y;
+    const uint8_t* mask;
+    __device__ __forceinline__ void begin_tile(int64_t, int64_t) {}
+    __device__ __forceinline__ float load1(int64_t g) const {
+      return (mask == nullptr || mask[g]) ? y[g] : 0.f;
+    }
+    __device__ __forceinline__ float4 load4(int64_t g) const {
+      return make_float4(load1(g), load1(g + 1), load1(g + 2), load1(g + 3));
+    }
+  };
+  __device__ __forceinline__ B bind(int) const { return B{y, mask}; }
+};
+
+// TAR stage-2 receive of worker q (collectives.py:140-150): own shard from
+// its own aggregate, peer shards from the owner's aggregate (peer-mapped in
+// the multi-GPU path) under the stage-2 mask, zero-filled misses.
+struct SrcGather {
+  const float* A[kMaxW];
+  Shards sh;
+  int n, r;
+  MaskView m;
+  uint8_t* got;  // optional [n][dim]
+  int64_t dim;
+  struct B {
+    const SrcGather* p;  // param space
+    int q;
+    // tile-uniform shard (fast path)
+    int uj;
+    const float* ua;
+    const uint32_t* urow;
+    int64_t uoff;
+    __device__ __forceinline__ void begin_tile(int64_t g0, int64_t g1) {
+      int j0 = p->sh.of(g0), j1 = p->sh.of(g1);
+      uj = j0 == j1 ? j0 : -1;
+      if (uj >= 0) {
+        int owner = shard_owner(uj, p->r, p->n);
+        uoff = p->sh.off(uj);
+        ua = p->A[owner] - uoff;
+        urow = owner == q ? nullptr : p->m.row(1, q, owner);
+      }
+    }
+    __device__ __forceinline__ float load1(int64_t g) const {
+      int j = p->sh.of(g);
+      int64_t e = g - p->sh.off(j);
+      int owner = shard_owner(j, p->r, p->n);
+      bool ok = owner == q ? true : row_bit(p->m.row(1, q, owner), (uint32_t)e / (uint32_t)p->m.epp);
+      if (p->got) p->got[(int64_t)q * p->dim + g] = ok ? 1 : 0;
+      return ok ? p->A[owner][e] : 0.f;
+    }
+    __device__ __forceinline__ float4 load4(int64_t g) const {
+      if (uj >= 0 && ((g - uoff) & 3) == 0) {
+        float4 v = ldg4(ua + g);
+        if (urow) {
+          Pkt4 pk = pkt4((uint32_t)(g - uoff), (uint32_t)p->m.epp);
+          bool k0 = row_bit(urow, pk.p[0]), k1 = row_bit(urow, pk.p[1]);
+          bool k2 = row_bit(urow, pk.p[2]), k3 = row_bit(urow, pk.p[3]);
+          v.x = k0 ? v.x : 0.f;
+          v.y = k1 ? v.y : 0.f;
+          v.z = k2 ? v.z : 0.f;
+          v.w = k3 ? v.w : 0.f;
+          if (p->got) {
+            uchar4 gb = make_uchar4(k0, k1, k2, k3);
+            *reinterpret_cast<uchar4*>(p->got + (int64_t)q * p->dim + g) = gb;
+          }
+        } else if (p->got) {
+          *reinterpret_cast<uchar4*>(p->got + (int64_t)q * p->dim + g) = make_uchar4(1, 1, 1, 1);
+        }
+        return v;
+      }
+      return make_float4(load1(g), load1(g + 1), load1(g + 2), load1(g + 3));
+    }
+  };
+  __device__ __forceinline__ B bind(int q) const {
+    B b;
+    b.p = this;
+    b.q = q;
+    b.uj = -1;
+    b.ua = nullptr;
+    b.urow = nullptr;
+    b.uoff = 0;
+    return b;
+  }
+};
+
+struct SnkBuf {
+  float* y[kMaxW];
+  float scale;
+  struct B {
+    float* y;
+    float scale;
+    __device__ __forceinline__ void store1(int64_t g, float v) const { y[g] = v * scale; }
+    __device__ __forceinline__ void store2(int64_t g, float a, float b) const {
+      *reinterpret_cast<float2*>(y + g) = make_float2(a * scale, b * scale);
+    }
+    __device__ __forceinline__ void store4(int64_t g, float4 v) const {
+      st4(y + g, make_float4(v.x * scale, v.y * scale, v.z * scale, v.w * scale));
+    }
+  };
+  __device__ __forceinline__ B bind(int w) const { return B{y[w], scale}; }
+};
+
+// signs * v * (dim/count)/sqrt(dim), truncated to L, cast (hadamard.py:116-123,
+// runner.py:253-256: count 0 -> zeros).
+struct SnkDecode {
+  void* out[kMaxW];
+  int dtype;
+  int64_t L;
+  const uint32_t* signs;
+  const unsigned long long* count_extra;  // device: + received entries (may be null)
+  int64_t count_base[kMaxW];              // host-known part of count
+  int count_stride;
+  double dim;
+  struct B {
+    void* out;
+    int dtype;
+    int64_t L;
+    const uint32_t* signs;
+    float scale;
+    __device__ __forceinline__ void store1(int64_t g, float v) const {
+      if (g >= L) return;
+      store_elem(out, dtype, g, sgn(__ldg(signs + (g >> 5)), (int)(g & 31), v * scale));
+    }
+    __device__ __forceinline__ void store2(int64_t g, float a, float b) const {
+      if (g + 2 <= L) {
+        uint32_t w = __ldg(signs + (g >> 5));
+        int b0 = (int)(g & 31);
+        a = sgn(w, b0, a * scale);
+        b = sgn(w, b0 + 1, b * scale);
+        if (dtype == OPTR_F32)
+          *reinterpret_cast<float2*>((float*)out + g) = make_float2(a, b);
+        else
+          *reinterpret_cast<__nv_bfloat162*>((__nv_bfloat16*)out + g) = __floats2bfloat162_rn(a, b);
+        return;
+      }
+      store1(g, a);
+      store1(g + 1, b);
+    }
+    __device__ __forceinline__ void store4(int64_t g, float4 v) const {
+      if (g + 4 <= L) {
+        uint32_t w = __ldg(signs + (g >> 5));
+        int b0 = (int)(g & 31);
+        v.x = sgn(w, b0, v.x * scale);
+        v.y = sgn(w, b0 + 1, v.y * scale);
+        v.z = sgn(w, b0 + 2, v.z * scale);
+        v.w = sgn(w, b0 + 3, v.w * scale);
+        if (dtype == OPTR_F32) {
+          st4((float*)out + g, v);
+        } else {
+          __nv_bfloat162 a = __floats2bfloat162_rn(v.x, v.y), b = __floats2bfloat162_rn(v.z, v.w);
+          uint2 u;
+          u.x = *reinterpret_cast<uint32_t*>(&a);
+          u.y = *reinterpret_cast<uint32_t*>(&b);
+          *reinterpret_cast<uint2*>((__nv_bfloat16*)out + g) = u;
+        }
+        return;
+      }
+      store1(g, v.x);
+      store1(g + 1, v.y);
+      store1(g + 2, v.z);
+      store1(g + 3, v.w);
+    }
+  };
+  __device__ __forceinline__ B bind(int w) const {
+    unsigned long long c = (unsigned long long)count_base[w];
+    if (count_extra) c += count_extra[w * count_stride];
+    float s = c == 0 ? 0.f : (float)((dim / (double)c) / sqrt(dim));
+    return B{out[w], dtype, L, signs, s};
+  }
+};
+
+// ------------------------------------------------------------ tile geometry
+// A pass transforms index bits [lo, lo+ks) of the vector.  A tile holds
+// 2^(cb+ks) entries: tile bits [0,cb) are untransformed columns (vector bits
+// [0,cb), contiguous), tile bits [cb, cb+ks) are the transformed bits.  Tile
+// t covers column group t mod 2^(lo-cb) of outer block t >> (lo-cb).
+struct PassGeom {
+  int lo, ks, cb;
+  int64_t ntiles;
+};
+
+__device__ __forceinline__ int64_t tile_origin(const PassGeom& pg, int64_t t) {
+  const int cgb = pg.lo - pg.cb;
+  const int64_t cgroup = t & ((1LL << cgb) - 1);
+  const int64_t outer = t >> cgb;
+  return (outer << (pg.lo + pg.ks)) + (cgroup << pg.cb);
+}
+__device__ __forceinline__ int64_t tile_remap(const PassGeom& pg, int i) {
+  return ((int64_t)(i >> pg.cb) << pg.lo) | (int64_t)(i & ((1 << pg.cb) - 1));
+}
+
 // Shared-memory bank swizzle: XOR index bits 0-4 with bits 5-9.  Every
-// register round below maps warp lanes onto the lowest index bits outside
-// its butterfly range, which this swizzle makes conflict-free.
+// layout below maps warp lanes onto five tile bits < 10 that are distinct
+// mod 5, which this swizzle makes conflict-free.
 __device__ __forceinline__ int swz(int i) { return i ^ ((i >> 5) & 31); }
 
+// ---------------------------------------------- register-layout tile FWHT
+// Plan: round 0 holds tile bits {0,1,T-3,T-2,T-1} in registers (float4
+// global loads); each later round holds up to 5 more transform bits, moved
+// through shared memory; the last round also holds bits 0(,1) when it can,
+// for vector stores.  (Prototyped and checked in numpy.)
+struct RPlan {
+  int nr;
+  int pos[4][5];
+  unsigned xm[4];
+};
+
+__host__ __device__ constexpr RPlan make_rplan(int T, int CB) {
+  RPlan p{};
+  bool done[32] = {};
+  const int A[5] = {0, 1, T - 3, T - 2, T - 1};
+  unsigned x0 = 0;
+  for (int k = 0; k < 5; ++k) {
+    p.pos[0][k] = A[k];
+    if (A[k] >= CB) {
+      x0 |= 1u << k;
+      done[A[k]] = true;
+    }
+  }
+  p.xm[0] = x0;
+  p.nr = 1;
+  int rem[32] = {};
+  int nrem = 0;
+  for (int b = CB; b < T; ++b)
+    if (!done[b]) rem[nrem++] = b;
+  int ri = 0;
+  while (ri < nrem && p.nr < 4) {
+    int cur[5] = {};
+    int nc = 0;
+    while (nc < 5 && ri < nrem) cur[nc++] = rem[ri++];
+    const bool last = ri >= nrem;
+    int pos[5] = {};
+    int np = 0;
+    if (last) {
+      if (nc <= 3) {
+        pos[np++] = 0;
+        pos[np++] = 1;
+      } else if (nc == 4) {
+        pos[np++] = 0;
+      }
+    }
+    for (int c = 0; c < nc; ++c) pos[np++] = cur[c];
+    for (int b = 0; b < T && np < 5; ++b) {
+      bool in = false;
+      for (int q = 0; q < np; ++q) in = in || pos[q] == b;
+      if (!in) pos[np++] = b;
+    }
+    unsigned x = 0;
+    for (int k = 0; k < 5; ++k) {
+      p.pos[p.nr][k] = pos[k];
+      for (int c = 0; c < nc; ++c)
+        if (pos[k] == cur[c]) x |= 1u << k;
+    }
+    p.xm[p.nr] = x;
+    p.nr++;
+  }
+  return p;
+}
+
+// tile offset of register j in round r
+__host__ __device__ constexpr int roff(const RPlan& p, int r, int j) {
+  int o = 0;
+  for (int k = 0; k < 5; ++k)
+    if ((j >> k) & 1) o |= 1 << p.pos[r][k];
+  return o;
+}
+
+// tile offset contributed by the thread id in round r (thread bits ascend
+// over the positions not held in registers)
+template <int T>
+__device__ __forceinline__ int thread_base(const RPlan& p, int r, int tid) {
+  int o = 0, m = 0;
+#pragma unroll
+  for (int b = 0; b < T; ++b) {
+    bool in = false;
+#pragma unroll
+    for (int k = 0; k < 5; ++k) in = in || p.pos[r][k] == b;
+    if (!in) {
+      o |= ((tid >> m) & 1) << b;
+      ++m;
+    }
+  }
+  return o;
+}
+
+template <unsigned XM>
+__device__ __forceinline__ void bfly32(float (&v)[32]) {
+#pragma unroll
+  for (int k = 0; k < 5; ++k) {
+    if ((XM >> k) & 1u) {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        if (((j >> k) & 1) == 0) {
+          float a = v[j], b = v[j | (1 << k)];
+          v[j] = a + b;
+          v[j | (1 << k)] = a - b;
+        }
+      }
+    }
+  }
+}
+
+template <int T, int CB, class Src, class Snk>
+__global__ void __launch_bounds__(1 << (T - 5)) rtile_kernel(PassGeom pg, int worker_base, const __grid_constant__ Src src,
+                                                          const __grid_constant__ Snk snk) {
+  constexpr RPlan P = make_rplan(T, CB);
+  constexpr int NR = P.nr;
+  extern __shared__ float sm[];
+  const int tid = threadIdx.x;
+  const int w = worker_base + blockIdx.y;
+  auto s = src.bind(w);
+  const auto d = snk.bind(w);
+  const int b0 = thread_base<T>(P, 0, tid);
+  const int b1 = NR > 1 ? thread_base<T>(P, 1, tid) : 0;
+  const int b2 = NR > 2 ? thread_base<T>(P, 2, tid) : 0;
+  const int b3 = NR > 3 ? thread_base<T>(P, 3, tid) : 0;
+  for (int64_t t = blockIdx.x; t < pg.ntiles; t += gridDim.x) {
+    const int64_t g0 = tile_origin(pg, t);
+    s.begin_tile(g0, g0 + tile_remap(pg, (1 << T) - 1));
+    float v[32];
+#pragma unroll
+    for (int m = 0; m < 8; ++m) {
+      const float4 q = s.load4(g0 + tile_remap(pg, b0 + roff(P, 0, 4 * m)));
+      v[4 * m] = q.x;
+      v[4 * m + 1] = q.y;
+      v[4 * m + 2] = q.z;
+      v[4 * m + 3] = q.w;
+    }
+    bfly32<P.xm[0]>(v);
+    if constexpr (NR > 1) {
+      __syncthreads();
+#pragma unroll
+      for (int j = 0; j < 32; ++j) sm[swz(b0 + roff(P, 0, j))] = v[j];
+      __syncthreads();
+#pragma unroll
+      for (int j = 0; j < 32; ++j) v[j] = sm[swz(b1 + roff(P, 1, j))];
+      bfly32<P.xm[1]>(v);
+    }
+    if constexpr (NR > 2) {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) sm[swz(b1 + roff(P, 1, j))] = v[j];
+      __syncthreads();
+#pragma unroll
+      for (int j = 0; j < 32; ++j) v[j] = sm[swz(b2 + roff(P, 2, j))];
+      bfly32<P.xm[2]>(v);
+    }
+    if constexpr (NR > 3) {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) sm[swz(b2 + roff(P, 2, j))] = v[j];
+      __syncthreads();
+#pragma unroll
+      for (int j = 0; j < 32; ++j) v[j] = sm[swz(b3 + roff(P, 3, j))];
+      bfly32<P.xm[3]>(v);
+    }
+    constexpr int LR = NR - 1;
+    const int bl = LR == 0 ? b0 : (LR == 1 ? b1 : (LR == 2 ? b2 : b3));
+    if constexpr (P.pos[LR][0] == 0 && P.pos[LR][1] == 1) {
+#pragma unroll
+      for (int m = 0; m < 8; ++m)
+        d.store4(g0 + tile_remap(pg, bl + roff(P, LR, 4 * m)),
+                 make_float4(v[4 * m], v[4 * m + 1], v[4 * m + 2], v[4 * m + 3]));
+    } else if constexpr (P.pos[LR][0] == 0) {
+#pragma unroll
+      for (int m = 0; m < 16; ++m) d.store2(g0 + tile_remap(pg, bl + roff(P, LR, 2 * m)), v[2 * m], v[2 * m + 1]);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) d.store1(g0 + tile_remap(pg, bl + roff(P, LR, j)), v[j]);
+    }
+  }
+}
+
+// ------------------------------------------------ small tiles (shared mem)
 template <int E>
 __device__ __forceinline__ void butterfly(float (&v)[1 << E]) {
 #pragma unroll
@@ -201,7 +703,6 @@ __device__ __forceinline__ void butterfly(float (&v)[1 << E]) {
   }
 }
 
-// Butterflies over tile-index bits [b, b+E) for all 2^(nbits-E) groups.
 template <int E>
 __device__ __forceinline__ void smem_round(float* s, int b, int nelem, int tid, int nthr) {
   int ngroups = nelem >> E;
@@ -233,142 +734,22 @@ __device__ __forceinline__ void tile_fwht(float* s, int b, int nbits, int nelem)
   }
 }
 
-// Geometry of one pass: tile = 2^(cb+ks) elements; tile bits [0,cb) are
-// columns (index bits [0,cb) of the vector, not transformed here... but see
-// below), tile bits [cb,cb+ks) are the transformed index bits [lo, lo+ks).
-// Global index of tile element i in tile t:
-//   g = outer*2^(lo+ks) + row*2^lo + cgroup*2^cb + col,
-//   cgroup = t mod 2^(lo-cb), outer = t >> (lo-cb).
-struct PassGeom {
-  int lo, ks, cb;
-};
-
-__device__ __forceinline__ int64_t tile_global(const PassGeom& pg, int64_t t, int i) {
-  int64_t ncg_bits = pg.lo - pg.cb;
-  int64_t cgroup = t & ((1LL << ncg_bits) - 1);
-  int64_t outer = t >> ncg_bits;
-  int col = i & ((1 << pg.cb) - 1);
-  int64_t row = i >> pg.cb;
-  return (outer << (pg.lo + pg.ks)) + (row << pg.lo) + (cgroup << pg.cb) + col;
-}
-
-// ---- sources (first pass input) and sinks (last pass output)
-__device__ __forceinline__ float load_elem(const void* p, int dtype, int64_t g) {
-  if (dtype == OPTR_BF16) return __bfloat162float(((const __nv_bfloat16*)p)[g]);
-  return ((const float*)p)[g];
-}
-__device__ __forceinline__ void store_elem(void* p, int dtype, int64_t g, float v) {
-  if (dtype == OPTR_BF16)
-    ((__nv_bfloat16*)p)[g] = __float2bfloat16_rn(v);
-  else
-    ((float*)p)[g] = v;
-}
-__device__ __forceinline__ bool sign_pos(const uint32_t* signs, int64_t g) {
-  return (__ldg(signs + (g >> 5)) >> (g & 31)) & 1u;
-}
-
-// pad(x) * signs   (hadamard.py:98-100)
-struct SrcEncode {
-  const void* x[kMaxW];
-  int dtype;
-  int64_t L;
-  const uint32_t* signs;
-  __device__ __forceinline__ float load(int w, int64_t g) const {
-    if (g >= L) return 0.f;
-    float v = load_elem(x[w], dtype, g);
-    return sign_pos(signs, g) ? v : -v;
-  }
-};
-
-struct SrcBuf {
-  float* y[kMaxW];
-  __device__ __forceinline__ float load(int w, int64_t g) const { return y[w][g]; }
-};
-
-// where(mask, y, 0) with a byte mask (hadamard.py:120)
-struct SrcMasked {
-  const float* y;
-  const uint8_t* mask;
-  __device__ __forceinline__ float load(int, int64_t g) const {
-    return (mask == nullptr || mask[g]) ? y[g] : 0.f;
-  }
-};
-
-// TAR stage-2 receive of worker q (collectives.py:140-150): own shard from
-// its own aggregate, peer shards from the owner's aggregate under the
-// stage-2 mask, zero-filled misses.  Optionally records `received`.
-struct SrcGather {
-  const float* A[kMaxW];
-  Shards sh;
-  int n, r;
-  MaskView m;
-  uint8_t* got;  // optional [n][dim]
-  int64_t dim;
-  __device__ __forceinline__ float load(int q, int64_t g) const {
-    int j = sh.of(g);
-    int64_t e = g - sh.off(j);
-    int owner = shard_owner(j, r, n);
-    bool ok = owner == q ? true : m.get(1, q, owner, (int64_t)((uint32_t)e / (uint32_t)m.epp));
-    if (got) got[(int64_t)q * dim + g] = ok ? 1 : 0;
-    return ok ? A[owner][e] : 0.f;
-  }
-};
-
-struct SnkBuf {
-  float* y[kMaxW];
-  float scale;
-  __device__ __forceinline__ void store(int w, int64_t g, float v) const { y[w][g] = v * scale; }
-};
-
-// signs * v * (dim/count)/sqrt(dim), truncated to L, cast (hadamard.py:116-123,
-// runner.py:253-256: count 0 -> zeros).
-struct SnkDecode {
-  void* out[kMaxW];
-  int dtype;
-  int64_t L;
-  const uint32_t* signs;
-  const unsigned long long* count_extra;  // device: + received entries (may be null)
-  int64_t count_base[kMaxW];              // host-known part of count
-  int count_stride;                       // index of worker's count_extra entry
-  double dim;
-  __device__ __forceinline__ float scale_for(int w) const {
-    unsigned long long c = (unsigned long long)count_base[w];
-    if (count_extra) c += count_extra[w * count_stride];
-    if (c == 0) return 0.f;
-    return (float)((dim / (double)c) / sqrt(dim));
-  }
-  __device__ __forceinline__ void store(int w, int64_t g, float v, float scale) const {
-    if (g >= L) return;
-    float r = v * scale;
-    store_elem(out[w], dtype, g, sign_pos(signs, g) ? r : -r);
-  }
-};
-
-template <class S>
-struct HasScale {
-  static constexpr bool value = false;
-};
-template <>
-struct HasScale<SnkDecode> {
-  static constexpr bool value = true;
-};
-
 template <class Src, class Snk>
-__global__ void __launch_bounds__(1024) fwht_pass_kernel(PassGeom pg, int worker_base, Src src, Snk snk) {
+__global__ void __launch_bounds__(256) smem_tile_kernel(PassGeom pg, int worker_base, const __grid_constant__ Src src,
+                                                            const __grid_constant__ Snk snk) {
   extern __shared__ float smem[];
   const int nelem = 1 << (pg.cb + pg.ks);
-  const int64_t t = blockIdx.x;
   const int w = worker_base + blockIdx.y;
-  for (int i = threadIdx.x; i < nelem; i += blockDim.x) smem[swz(i)] = src.load(w, tile_global(pg, t, i));
-  __syncthreads();
-  tile_fwht(smem, pg.cb, pg.ks, nelem);
-  float scale = 1.f;
-  if constexpr (HasScale<Snk>::value) scale = snk.scale_for(w);
-  for (int i = threadIdx.x; i < nelem; i += blockDim.x) {
-    if constexpr (HasScale<Snk>::value)
-      snk.store(w, tile_global(pg, t, i), smem[swz(i)], scale);
-    else
-      snk.store(w, tile_global(pg, t, i), smem[swz(i)]);
+  auto s = src.bind(w);
+  const auto d = snk.bind(w);
+  for (int64_t t = blockIdx.x; t < pg.ntiles; t += gridDim.x) {
+    const int64_t g0 = tile_origin(pg, t);
+    s.begin_tile(g0, g0 + tile_remap(pg, nelem - 1));
+    __syncthreads();
+    for (int i = threadIdx.x; i < nelem; i += blockDim.x) smem[swz(i)] = s.load1(g0 + tile_remap(pg, i));
+    __syncthreads();
+    tile_fwht(smem, pg.cb, pg.ks, nelem);
+    for (int i = threadIdx.x; i < nelem; i += blockDim.x) d.store1(g0 + tile_remap(pg, i), smem[swz(i)]);
   }
 }
 
@@ -382,28 +763,79 @@ struct AggArgs {
   int owner_base;
 };
 
-// collectives.py:77-94 with own shard at its rank position, zero-filled misses
-// (acc += 0.0 keeps -0.0 + 0.0 semantics bit-identical to the reference).
-__global__ void __launch_bounds__(256) aggregate_kernel(AggArgs a) {
+// acc / cnt with cnt in 1..n: a power-of-two count divides exactly by
+// multiplying with its reciprocal; otherwise IEEE division (np.divide).
+__device__ __forceinline__ float mean_of(double acc, double cnt) {
+  unsigned c = (unsigned)cnt;
+  double q = (c & (c - 1)) == 0 ? acc * (1.0 / cnt) : acc / cnt;
+  return (float)q;
+}
+
+// collectives.py:77-94 with the own shard at its rank position and
+// zero-filled misses (acc += 0.0 keeps the reference's -0.0 + 0.0 behaviour).
+template <bool VEC>
+__global__ void __launch_bounds__(256) aggregate_kernel(const __grid_constant__ AggArgs a) {
   const int o = a.owner_base + blockIdx.y;
   const int j = owned_shard(o, a.r, a.n);
   const int64_t len = a.sh.len(j), off = a.sh.off(j);
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < len;
+  const int n = a.n;
+  const uint32_t epp = (uint32_t)a.m.epp;
+  float* out = a.A[o];
+  if (VEC) {
+    const int64_t n4 = len >> 2;
+    for (int64_t e4 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e4 < n4;
+         e4 += (int64_t)gridDim.x * blockDim.x) {
+      const int64_t e = e4 * 4;
+      const Pkt4 pk = pkt4((uint32_t)e, epp);
+      double acc[4] = {0.0, 0.0, 0.0, 0.0}, cnt[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+      for (int i = 0; i < kMaxW; ++i) {
+        if (i < n) {
+          const float4 v = ldg4(a.Y[i] + off + e);
+          if (i == o) {
+            acc[0] += (double)v.x;
+            acc[1] += (double)v.y;
+            acc[2] += (double)v.z;
+            acc[3] += (double)v.w;
+            cnt[0] += 1.0;
+            cnt[1] += 1.0;
+            cnt[2] += 1.0;
+            cnt[3] += 1.0;
+          } else {
+            const uint32_t* row = a.m.row(0, o, i);
+            const bool k0 = row_bit(row, pk.p[0]), k1 = row_bit(row, pk.p[1]);
+            const bool k2 = row_bit(row, pk.p[2]), k3 = row_bit(row, pk.p[3]);
+            acc[0] += k0 ? (double)v.x : 0.0;
+            acc[1] += k1 ? (double)v.y : 0.0;
+            acc[2] += k2 ? (double)v.z : 0.0;
+            acc[3] += k3 ? (double)v.w : 0.0;
+            cnt[0] += k0 ? 1.0 : 0.0;
+            cnt[1] += k1 ? 1.0 : 0.0;
+            cnt[2] += k2 ? 1.0 : 0.0;
+            cnt[3] += k3 ? 1.0 : 0.0;
+          }
+        }
+      }
+      st4(out + e, make_float4(mean_of(acc[0], cnt[0]), mean_of(acc[1], cnt[1]), mean_of(acc[2], cnt[2]),
+                               mean_of(acc[3], cnt[3])));
+    }
+  }
+  const int64_t start = VEC ? (len & ~3LL) : 0;
+  for (int64_t e = start + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < len;
        e += (int64_t)gridDim.x * blockDim.x) {
-    int64_t pkt = (int64_t)((uint64_t)e / (uint64_t)a.m.epp);
+    const uint32_t pkt = (uint32_t)e / epp;
     double acc = 0.0, cnt = 0.0;
-    for (int i = 0; i < a.n; ++i) {
+    for (int i = 0; i < n; ++i) {
       if (i == o) {
         acc += (double)a.Y[i][off + e];
         cnt += 1.0;
       } else {
-        bool ok = a.m.get(0, o, i, pkt);
-        float v = ok ? a.Y[i][off + e] : 0.f;
-        acc += (double)v;
+        const bool ok = row_bit(a.m.row(0, o, i), pkt);
+        acc += ok ? (double)a.Y[i][off + e] : 0.0;
         cnt += ok ? 1.0 : 0.0;
       }
     }
-    a.A[o][e] = (float)(acc / cnt);
+    out[e] = mean_of(acc, cnt);
   }
 }
 
@@ -416,24 +848,22 @@ struct AsmArgs {
   int worker_base;
 };
 
-__global__ void __launch_bounds__(256) assemble_kernel(AsmArgs a) {
+__global__ void __launch_bounds__(256) assemble_kernel(const __grid_constant__ AsmArgs a) {
   const int q = a.worker_base + blockIdx.y;
-  for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < a.L;
-       g += (int64_t)gridDim.x * blockDim.x)
-    store_elem(a.out[q], a.dtype, g, a.gather.load(q, g));
+  auto s = a.gather.bind(q);
+  for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < a.L; g += (int64_t)gridDim.x * blockDim.x)
+    store_elem(a.out[q], a.dtype, g, s.load1(g));
 }
 
 // fp32/bf16 -> fp32 copy (RHT off: the wire carries float32, runner.py:228)
 __global__ void cast_copy_kernel(const void* x, int dtype, float* y, int64_t n) {
-  for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < n;
-       g += (int64_t)gridDim.x * blockDim.x)
+  for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < n; g += (int64_t)gridDim.x * blockDim.x)
     y[g] = load_elem(x, dtype, g);
 }
 
 __global__ void count_mask_kernel(const uint8_t* mask, int64_t n, unsigned long long* out) {
   unsigned long long c = 0;
-  for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < n;
-       g += (int64_t)gridDim.x * blockDim.x)
+  for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < n; g += (int64_t)gridDim.x * blockDim.x)
     c += mask[g] ? 1 : 0;
   for (int o = 16; o; o >>= 1) c += __shfl_down_sync(0xffffffffu, c, o);
   if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, c);
