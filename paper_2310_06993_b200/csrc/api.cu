@@ -98,25 +98,27 @@ constexpr int kContigBits = 13;
 constexpr int kColBits = 3;
 
 int plan_passes(int n, PassGeom* out, bool encode_order) {
+  // contiguous pass on 2^c-entry tiles, strided passes of <= 11 row bits on
+  // 2^ks x 8 tiles (T = ks + 3 <= 14, so every tile fits one CTA's registers)
   PassGeom p[3];
   int np = 0;
   if (n <= kContigBits) {
     p[np++] = PassGeom{0, n, 0, 1};
+  } else if (n <= kContigBits + 11) {
+    p[np++] = PassGeom{kContigBits, n - kContigBits, kColBits, 0};
+    p[np++] = PassGeom{0, kContigBits, 0, 0};
+  } else if (n == kContigBits + 12) {
+    p[np++] = PassGeom{kContigBits + 1, n - kContigBits - 1, kColBits, 0};
+    p[np++] = PassGeom{0, kContigBits + 1, 0, 0};
   } else {
     int rest = n - kContigBits;
-    if (rest <= 12) {
-      p[np++] = PassGeom{kContigBits, rest, kColBits, 0};
-    } else {
-      int k1 = rest / 2;
-      p[np++] = PassGeom{kContigBits + k1, rest - k1, kColBits, 0};
-      p[np++] = PassGeom{kContigBits, k1, kColBits, 0};
-    }
+    int k1 = rest / 2;
+    p[np++] = PassGeom{kContigBits + k1, rest - k1, kColBits, 0};
+    p[np++] = PassGeom{kContigBits, k1, kColBits, 0};
     p[np++] = PassGeom{0, kContigBits, 0, 0};
   }
-  for (int i = 0; i < np; ++i) {
-    p[i].ntiles = (1LL << n) >> (p[i].cb + p[i].ks);
-    out[i] = encode_order ? p[i] : p[np - 1 - i];
-  }
+  for (int i = 0; i < np; ++i) p[i].ntiles = (1LL << n) >> (p[i].cb + p[i].ks);
+  for (int i = 0; i < np; ++i) out[i] = encode_order ? p[i] : p[np - 1 - i];
   return np;
 }
 
@@ -136,6 +138,22 @@ int ensure_device_init() {
   return OPTR_OK;
 }
 
+// After a launch: on failure report the kernel's resource limits.
+template <class K>
+int launch_check(K kernel, const char* name, int T, int CB, int gx, int gy, int threads, size_t smem) {
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) return OPTR_OK;
+  cudaFuncAttributes fa;
+  memset(&fa, 0, sizeof(fa));
+  cudaFuncGetAttributes(&fa, kernel);
+  fprintf(stderr,
+          "optr: %s<T=%d,CB=%d> launch grid=(%d,%d) block=%d smem=%zu failed: %s "
+          "(regs=%d maxThreads=%d maxDynSmem=%d)\n",
+          name, T, CB, gx, gy, threads, smem, cudaGetErrorString(e), fa.numRegs, fa.maxThreadsPerBlock,
+          fa.maxDynamicSharedSizeBytes);
+  return OPTR_ECUDA;
+}
+
 template <class K>
 int set_smem_attr(K kernel, size_t smem) {
   if (smem <= 48 * 1024) return OPTR_OK;
@@ -145,18 +163,17 @@ int set_smem_attr(K kernel, size_t smem) {
 
 constexpr int64_t kMaxGrid = 148 * 16;
 
-template <int T, int CB, class Src, class Snk>
+template <int T, int CB, int LO, class Src, class Snk>
 int launch_rtile(int cls, const PassGeom& pg, int worker_base, int nworkers, const Src& src, const Snk& snk,
                  cudaStream_t st) {
-  const size_t smem = sizeof(float) << T;
-  int rc = set_smem_attr(rtile_kernel<T, CB, Src, Snk>, smem);
+  const size_t smem = sizeof(float) * (size_t)pad(1 << T);
+  int rc = set_smem_attr(rtile_kernel<T, CB, LO, Src, Snk>, smem);
   if (rc) return rc;
   const int64_t gx = pg.ntiles < kMaxGrid ? pg.ntiles : kMaxGrid;
   KScope ks(cls, st);
-  rtile_kernel<T, CB, Src, Snk><<<dim3((unsigned)gx, (unsigned)nworkers), 1 << (T - 5), smem, st>>>(
+  rtile_kernel<T, CB, LO, Src, Snk><<<dim3((unsigned)gx, (unsigned)nworkers), 1 << (T - 5), smem, st>>>(
       pg, worker_base, src, snk);
-  CK(cudaGetLastError());
-  return OPTR_OK;
+  return launch_check(rtile_kernel<T, CB, LO, Src, Snk>, "rtile", T, CB, (int)gx, nworkers, 1 << (T - 5), smem);
 }
 
 template <class Src, class Snk>
@@ -173,8 +190,8 @@ int launch_smem(int cls, const PassGeom& pg, int worker_base, int nworkers, cons
   KScope ks(cls, st);
   smem_tile_kernel<Src, Snk><<<dim3((unsigned)gx, (unsigned)nworkers), threads, smem, st>>>(pg, worker_base, src,
                                                                                             snk);
-  CK(cudaGetLastError());
-  return OPTR_OK;
+  return launch_check(smem_tile_kernel<Src, Snk>, "smem_tile", pg.cb + pg.ks, pg.cb, (int)gx, nworkers, threads,
+                      smem);
 }
 
 template <class S>
@@ -185,15 +202,22 @@ int launch_pass(int cls, const PassGeom& pg, int nlog, int worker_base, int nwor
                 const Snk& snk, cudaStream_t st) {
   (void)nlog;
   const int T = pg.cb + pg.ks;
-  if (pg.cb == 0 && T == 13) return launch_rtile<13, 0>(cls, pg, worker_base, nworkers, src, snk, st);
+  if (pg.cb == 0 && pg.lo == 0 && T == 13) return launch_rtile<13, 0, 0>(cls, pg, worker_base, nworkers, src, snk, st);
+  if (pg.cb == 0 && pg.lo == 0 && T == 14) return launch_rtile<14, 0, 0>(cls, pg, worker_base, nworkers, src, snk, st);
   if constexpr (kStridedSrc<Src>) {
-    if (pg.cb == 3) {
+    if (pg.cb == 3 && pg.lo == 13) {
       switch (T) {
-        case 11: return launch_rtile<11, 3>(cls, pg, worker_base, nworkers, src, snk, st);
-        case 12: return launch_rtile<12, 3>(cls, pg, worker_base, nworkers, src, snk, st);
-        case 13: return launch_rtile<13, 3>(cls, pg, worker_base, nworkers, src, snk, st);
-        case 14: return launch_rtile<14, 3>(cls, pg, worker_base, nworkers, src, snk, st);
-        case 15: return launch_rtile<15, 3>(cls, pg, worker_base, nworkers, src, snk, st);
+        case 11: return launch_rtile<11, 3, 13>(cls, pg, worker_base, nworkers, src, snk, st);
+        case 12: return launch_rtile<12, 3, 13>(cls, pg, worker_base, nworkers, src, snk, st);
+        case 13: return launch_rtile<13, 3, 13>(cls, pg, worker_base, nworkers, src, snk, st);
+        case 14: return launch_rtile<14, 3, 13>(cls, pg, worker_base, nworkers, src, snk, st);
+        default: break;
+      }
+    }
+    if (pg.cb == 3 && pg.lo == 14) {
+      switch (T) {
+        case 13: return launch_rtile<13, 3, 14>(cls, pg, worker_base, nworkers, src, snk, st);
+        case 14: return launch_rtile<14, 3, 14>(cls, pg, worker_base, nworkers, src, snk, st);
         default: break;
       }
     }

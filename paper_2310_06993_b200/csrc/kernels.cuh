@@ -507,9 +507,9 @@ __device__ __forceinline__ int64_t tile_remap(const PassGeom& pg, int i) {
   return ((int64_t)(i >> pg.cb) << pg.lo) | (int64_t)(i & ((1 << pg.cb) - 1));
 }
 
-// Shared-memory bank swizzle: XOR index bits 0-4 with bits 5-9.  Every
-// layout below maps warp lanes onto five tile bits < 10 that are distinct
-// mod 5, which this swizzle makes conflict-free.
+// Shared-memory bank swizzle of the small-tile kernel: XOR index bits 0-4
+// with bits 5-9 (conflict-free when warp lanes sit on five tile bits < 10
+// that are distinct mod 5).
 __device__ __forceinline__ int swz(int i) { return i ^ ((i >> 5) & 31); }
 
 // ---------------------------------------------- register-layout tile FWHT
@@ -618,11 +618,25 @@ __device__ __forceinline__ void bfly32(float (&v)[32]) {
   }
 }
 
-template <int T, int CB, class Src, class Snk>
-__global__ void __launch_bounds__(1 << (T - 5)) rtile_kernel(PassGeom pg, int worker_base, const __grid_constant__ Src src,
+// Padded shared-memory index: one spare word per 32.  It is additive over
+// disjoint bit sets (pad(b|c) = pad(b) + pad(c)), so every access is a
+// per-thread base plus a compile-time immediate, and it is conflict-free for
+// every layout here (warp lanes sit on five tile bits < 10, distinct mod 5).
+__host__ __device__ constexpr int pad(int i) { return i + (i >> 5); }
+
+// global offset of tile element i (tile bits >= CB move up to LO)
+template <int CB, int LO>
+__host__ __device__ constexpr int64_t remap_c(int i) {
+  return ((int64_t)(i >> CB) << LO) | (int64_t)(i & ((1 << CB) - 1));
+}
+
+template <int T, int CB, int LO, class Src, class Snk>
+__global__ void __launch_bounds__(1 << (T - 5)) rtile_kernel(PassGeom pg, int worker_base,
+                                                          const __grid_constant__ Src src,
                                                           const __grid_constant__ Snk snk) {
   constexpr RPlan P = make_rplan(T, CB);
   constexpr int NR = P.nr;
+  constexpr int KS = T - CB;
   extern __shared__ float sm[];
   const int tid = threadIdx.x;
   const int w = worker_base + blockIdx.y;
@@ -632,13 +646,21 @@ __global__ void __launch_bounds__(1 << (T - 5)) rtile_kernel(PassGeom pg, int wo
   const int b1 = NR > 1 ? thread_base<T>(P, 1, tid) : 0;
   const int b2 = NR > 2 ? thread_base<T>(P, 2, tid) : 0;
   const int b3 = NR > 3 ? thread_base<T>(P, 3, tid) : 0;
+  constexpr int LR = NR - 1;
+  const int bl = LR == 0 ? b0 : (LR == 1 ? b1 : (LR == 2 ? b2 : b3));
+  const int64_t r0 = remap_c<CB, LO>(b0), rl = remap_c<CB, LO>(bl);
+  float* const s0 = sm + pad(b0);
+  float* const s1 = sm + pad(b1);
+  float* const s2 = sm + pad(b2);
+  float* const s3 = sm + pad(b3);
   for (int64_t t = blockIdx.x; t < pg.ntiles; t += gridDim.x) {
-    const int64_t g0 = tile_origin(pg, t);
-    s.begin_tile(g0, g0 + tile_remap(pg, (1 << T) - 1));
+    constexpr int CGB = LO - CB;
+    const int64_t g0 = ((t >> CGB) << (LO + KS)) + ((t & ((1LL << CGB) - 1)) << CB);
+    s.begin_tile(g0, g0 + remap_c<CB, LO>((1 << T) - 1));
     float v[32];
 #pragma unroll
     for (int m = 0; m < 8; ++m) {
-      const float4 q = s.load4(g0 + tile_remap(pg, b0 + roff(P, 0, 4 * m)));
+      const float4 q = s.load4(g0 + r0 + remap_c<CB, LO>(roff(P, 0, 4 * m)));
       v[4 * m] = q.x;
       v[4 * m + 1] = q.y;
       v[4 * m + 2] = q.z;
@@ -648,41 +670,40 @@ __global__ void __launch_bounds__(1 << (T - 5)) rtile_kernel(PassGeom pg, int wo
     if constexpr (NR > 1) {
       __syncthreads();
 #pragma unroll
-      for (int j = 0; j < 32; ++j) sm[swz(b0 + roff(P, 0, j))] = v[j];
+      for (int j = 0; j < 32; ++j) s0[pad(roff(P, 0, j))] = v[j];
       __syncthreads();
 #pragma unroll
-      for (int j = 0; j < 32; ++j) v[j] = sm[swz(b1 + roff(P, 1, j))];
+      for (int j = 0; j < 32; ++j) v[j] = s1[pad(roff(P, 1, j))];
       bfly32<P.xm[1]>(v);
     }
     if constexpr (NR > 2) {
 #pragma unroll
-      for (int j = 0; j < 32; ++j) sm[swz(b1 + roff(P, 1, j))] = v[j];
+      for (int j = 0; j < 32; ++j) s1[pad(roff(P, 1, j))] = v[j];
       __syncthreads();
 #pragma unroll
-      for (int j = 0; j < 32; ++j) v[j] = sm[swz(b2 + roff(P, 2, j))];
+      for (int j = 0; j < 32; ++j) v[j] = s2[pad(roff(P, 2, j))];
       bfly32<P.xm[2]>(v);
     }
     if constexpr (NR > 3) {
 #pragma unroll
-      for (int j = 0; j < 32; ++j) sm[swz(b2 + roff(P, 2, j))] = v[j];
+      for (int j = 0; j < 32; ++j) s2[pad(roff(P, 2, j))] = v[j];
       __syncthreads();
 #pragma unroll
-      for (int j = 0; j < 32; ++j) v[j] = sm[swz(b3 + roff(P, 3, j))];
+      for (int j = 0; j < 32; ++j) v[j] = s3[pad(roff(P, 3, j))];
       bfly32<P.xm[3]>(v);
     }
-    constexpr int LR = NR - 1;
-    const int bl = LR == 0 ? b0 : (LR == 1 ? b1 : (LR == 2 ? b2 : b3));
     if constexpr (P.pos[LR][0] == 0 && P.pos[LR][1] == 1) {
 #pragma unroll
       for (int m = 0; m < 8; ++m)
-        d.store4(g0 + tile_remap(pg, bl + roff(P, LR, 4 * m)),
+        d.store4(g0 + rl + remap_c<CB, LO>(roff(P, LR, 4 * m)),
                  make_float4(v[4 * m], v[4 * m + 1], v[4 * m + 2], v[4 * m + 3]));
     } else if constexpr (P.pos[LR][0] == 0) {
 #pragma unroll
-      for (int m = 0; m < 16; ++m) d.store2(g0 + tile_remap(pg, bl + roff(P, LR, 2 * m)), v[2 * m], v[2 * m + 1]);
+      for (int m = 0; m < 16; ++m)
+        d.store2(g0 + rl + remap_c<CB, LO>(roff(P, LR, 2 * m)), v[2 * m], v[2 * m + 1]);
     } else {
 #pragma unroll
-      for (int j = 0; j < 32; ++j) d.store1(g0 + tile_remap(pg, bl + roff(P, LR, j)), v[j]);
+      for (int j = 0; j < 32; ++j) d.store1(g0 + rl + remap_c<CB, LO>(roff(P, LR, j)), v[j]);
     }
   }
 }
