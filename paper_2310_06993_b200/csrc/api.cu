@@ -12,6 +12,9 @@
 
 #include "../../include/optr.h"
 #include "kernels.cuh"
+#include "tma.cuh"
+
+#include <cudaTypedefs.h>
 
 using namespace optr;
 
@@ -98,24 +101,27 @@ constexpr int kContigBits = 13;
 constexpr int kColBits = 3;
 
 int plan_passes(int n, PassGeom* out, bool encode_order) {
-  // contiguous pass on 2^c-entry tiles, strided passes of <= 11 row bits on
-  // 2^ks x 8 tiles (T = ks + 3 <= 14, so every tile fits one CTA's registers)
+  // A contiguous pass on 2^c-entry tiles plus strided passes of <= 11 row
+  // bits on 2^ks x 8 tiles (T = ks + 3 <= 14: one CTA's registers).  Encode
+  // runs the contiguous pass first (x streams from HBM) and decode runs it
+  // last (out streams to HBM), so the strided passes, whose 32-byte row
+  // segments are poor DRAM bursts, work on an L2-resident vector.
   PassGeom p[3];
   int np = 0;
   if (n <= kContigBits) {
     p[np++] = PassGeom{0, n, 0, 1};
   } else if (n <= kContigBits + 11) {
-    p[np++] = PassGeom{kContigBits, n - kContigBits, kColBits, 0};
     p[np++] = PassGeom{0, kContigBits, 0, 0};
+    p[np++] = PassGeom{kContigBits, n - kContigBits, kColBits, 0};
   } else if (n == kContigBits + 12) {
-    p[np++] = PassGeom{kContigBits + 1, n - kContigBits - 1, kColBits, 0};
     p[np++] = PassGeom{0, kContigBits + 1, 0, 0};
+    p[np++] = PassGeom{kContigBits + 1, n - kContigBits - 1, kColBits, 0};
   } else {
     int rest = n - kContigBits;
     int k1 = rest / 2;
-    p[np++] = PassGeom{kContigBits + k1, rest - k1, kColBits, 0};
-    p[np++] = PassGeom{kContigBits, k1, kColBits, 0};
     p[np++] = PassGeom{0, kContigBits, 0, 0};
+    p[np++] = PassGeom{kContigBits, k1, kColBits, 0};
+    p[np++] = PassGeom{kContigBits + k1, rest - k1, kColBits, 0};
   }
   for (int i = 0; i < np; ++i) p[i].ntiles = (1LL << n) >> (p[i].cb + p[i].ks);
   for (int i = 0; i < np; ++i) out[i] = encode_order ? p[i] : p[np - 1 - i];
@@ -194,17 +200,125 @@ int launch_smem(int cls, const PassGeom& pg, int worker_base, int nworkers, cons
                       smem);
 }
 
+
+// ------------------------------------------------------------ TMA strided
+PFN_cuTensorMapEncodeTiled_v12000 g_encode_tiled = nullptr;
+int g_tma_mode = -1;  // -1 unknown, 0 off, 1 on
+
+bool tma_enabled() {
+  if (g_tma_mode < 0) {
+    const char* e = getenv("OPTR_TMA");
+    g_tma_mode = (e && e[0] == '0') ? 0 : 1;
+    if (g_tma_mode) {
+      cudaDriverEntryPointQueryResult q;
+      if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void**)&g_encode_tiled, cudaEnableDefault, &q) !=
+              cudaSuccess ||
+          q != cudaDriverEntryPointSuccess || !g_encode_tiled)
+        g_tma_mode = 0;
+    }
+  }
+  return g_tma_mode == 1;
+}
+
+// fp32 tensor [d2][d1][d0] (d0 contiguous), boxes of 8 x box1 x 1
+bool make_map3(CUtensorMap* m, const void* base, uint64_t d0, uint64_t d1, uint64_t d2, uint32_t box1) {
+  cuuint64_t dims[3] = {d0, d1, d2};
+  cuuint64_t strides[2] = {d0 * 4, d0 * d1 * 4};
+  cuuint32_t box[3] = {8, box1, 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = g_encode_tiled(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(base), dims, strides, box,
+                              es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) fprintf(stderr, "optr: cuTensorMapEncodeTiled failed (%d)\n", (int)r);
+  return r == CUDA_SUCCESS;
+}
+
+template <int T, bool GATHER>
+int launch_tma_kernel(int cls, const TmaMaps& src, const CUtensorMap& dst, const TmaStridedArgs& a,
+                      cudaStream_t st) {
+  const size_t smem = tma_smem_bytes<T>();
+  int rc = set_smem_attr(tma_strided_kernel<T, GATHER>, smem);
+  if (rc) return rc;
+  static int nsm = 0;
+  if (!nsm) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    if (nsm <= 0) nsm = 148;
+  }
+  const int per_sm = (int)((227 * 1024) / smem) > 0 ? (int)((227 * 1024) / smem) : 1;
+  int64_t gx = (int64_t)nsm * per_sm;
+  if (gx > a.ntiles) gx = a.ntiles;
+  KScope ks(cls, st);
+  tma_strided_kernel<T, GATHER><<<(unsigned)gx, 1 << (T - 5), smem, st>>>(src, dst, a);
+  return launch_check(tma_strided_kernel<T, GATHER>, GATHER ? "tma_gather" : "tma_strided", T, 3, (int)gx, 1,
+                      1 << (T - 5), smem);
+}
+
+// Strided pass through TMA when the shapes allow it; returns -1 when the
+// caller should use the LSU kernel instead.
+template <class Src, class Snk>
+int try_tma_strided(int cls, const PassGeom& pg, int nlog, int worker, int nworkers, const Src& src, const Snk& snk,
+                    cudaStream_t st) {
+  constexpr bool kBuf = std::is_same<Src, SrcBuf>::value;
+  constexpr bool kGather = std::is_same<Src, SrcGather>::value;
+  if constexpr (!(kBuf || kGather) || !std::is_same<Snk, SnkBuf>::value) {
+    return -1;
+  } else {
+    const int T = pg.cb + pg.ks;
+    if (pg.cb != 3 || nworkers != 1 || T < 12 || T > 14 || !tma_enabled()) return -1;
+    const uint64_t d0 = 1ULL << pg.lo, d1 = 1ULL << pg.ks, d2 = 1ULL << (nlog - pg.lo - pg.ks);
+    TmaStridedArgs a;
+    memset(&a, 0, sizeof(a));
+    a.ntiles = pg.ntiles;
+    a.lo = pg.lo;
+    a.scale = snk.scale;
+    int box = (int)(d1 < 256 ? d1 : 256);
+    TmaMaps maps;
+    memset(&maps, 0, sizeof(maps));
+    if constexpr (kGather) {
+      if (src.pow2_shift < pg.lo || d2 != 1) return -1;
+      const int64_t srows = 1LL << (src.pow2_shift - pg.lo);
+      if (srows < box) box = (int)srows;
+      for (int o = 0; o < src.n; ++o)
+        if (!make_map3(&maps.m[o], src.A[o], d0, (uint64_t)srows, 1, (uint32_t)box)) return -1;
+      a.q = worker;
+      a.n = src.n;
+      a.r = src.r;
+      a.shard_shift = src.pow2_shift;
+      a.m = src.m;
+      a.got = src.got ? src.got + (int64_t)worker * src.dim : nullptr;
+      a.dim = src.dim;
+    } else {
+      if (!make_map3(&maps.m[0], src.y[worker], d0, d1, d2, (uint32_t)box)) return -1;
+    }
+    a.box_rows = box;
+    CUtensorMap dmap;
+    if (!make_map3(&dmap, snk.y[worker], d0, d1, d2, (uint32_t)box)) return -1;
+    switch (T) {
+      case 12: return launch_tma_kernel<12, kGather>(cls, maps, dmap, a, st);
+      case 13: return launch_tma_kernel<13, kGather>(cls, maps, dmap, a, st);
+      default: return launch_tma_kernel<14, kGather>(cls, maps, dmap, a, st);
+    }
+  }
+}
+
 template <class S>
-constexpr bool kStridedSrc = std::is_same<S, SrcEncode>::value || std::is_same<S, SrcBuf>::value;
+constexpr bool kStridedSrc = !std::is_same<S, SrcEncode>::value;
+template <class S>
+constexpr bool kStridedSnk = !std::is_same<S, SnkDecode>::value;
 
 template <class Src, class Snk>
 int launch_pass(int cls, const PassGeom& pg, int nlog, int worker_base, int nworkers, const Src& src,
                 const Snk& snk, cudaStream_t st) {
-  (void)nlog;
   const int T = pg.cb + pg.ks;
+  {
+    int rc = try_tma_strided(cls, pg, nlog, worker_base, nworkers, src, snk, st);
+    if (rc >= 0) return rc;
+  }
   if (pg.cb == 0 && pg.lo == 0 && T == 13) return launch_rtile<13, 0, 0>(cls, pg, worker_base, nworkers, src, snk, st);
   if (pg.cb == 0 && pg.lo == 0 && T == 14) return launch_rtile<14, 0, 0>(cls, pg, worker_base, nworkers, src, snk, st);
-  if constexpr (kStridedSrc<Src>) {
+  if constexpr (kStridedSrc<Src> && kStridedSnk<Snk>) {
     if (pg.cb == 3 && pg.lo == 13) {
       switch (T) {
         case 11: return launch_rtile<11, 3, 13>(cls, pg, worker_base, nworkers, src, snk, st);
@@ -269,6 +383,23 @@ int launch_aggregate(const AggArgs& ag, int nowners, int64_t smax, cudaStream_t 
 }
 
 Pcg sign_pcg(uint64_t seed) { return pcg_from_u64s(&seed, 1); }
+
+// Workers per transform launch: batch them while their vectors fit in about
+// half of L2 together, otherwise one worker at a time so each worker's
+// vector stays L2-resident between its contiguous and strided passes.
+int workers_per_launch(int64_t dim, int n) {
+  static int l2 = 0;
+  if (!l2) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev) != cudaSuccess || l2 <= 0) l2 = 50 << 20;
+  }
+  int64_t bytes = dim * 4;
+  int k = (int)((int64_t)l2 / 2 / (bytes > 0 ? bytes : 1));
+  if (k < 1) k = 1;
+  if (k > n) k = n;
+  return k;
+}
 
 void fill_sign_args(PrepArgs& a, uint32_t* signs, int64_t dim, uint64_t seed) {
   Pcg p = sign_pcg(seed);
@@ -586,7 +717,11 @@ int optr_tar_local(const void* const* x, void* const* out, int n, int64_t L, int
       Yw[w] = Y + (size_t)w * dim;
     }
     snk.scale = (float)(1.0 / sqrt((double)dim));
-    if ((rc = run_transform(log2_exact(dim), true, 0, n, src, buf, snk, st, OPTR_K_ENC_FIRST))) return rc;
+    const int k = workers_per_launch(dim, n);
+    for (int w0 = 0; w0 < n; w0 += k)
+      if ((rc = run_transform(log2_exact(dim), true, w0, (n - w0 < k ? n - w0 : k), src, buf, snk, st,
+                              OPTR_K_ENC_FIRST)))
+        return rc;
   } else {
     for (int w = 0; w < n; ++w) {
       if (dtype_in == OPTR_F32) {
@@ -625,6 +760,7 @@ int optr_tar_local(const void* const* x, void* const* out, int n, int64_t L, int
   ga.m = mv;
   ga.got = got_out;
   ga.dim = dim;
+  ga.pow2_shift = (sh.extra == 0 && is_pow2(sh.base)) ? log2_exact(sh.base) : -1;
   if (ht) {
     SrcBuf buf;
     memset(&buf, 0, sizeof(buf));
@@ -641,7 +777,11 @@ int optr_tar_local(const void* const* x, void* const* out, int n, int64_t L, int
     snk.count_extra = counts + n;  // stage-2 row
     snk.count_stride = 1;
     snk.dim = (double)dim;
-    if ((rc = run_transform(log2_exact(dim), false, 0, n, ga, buf, snk, st, OPTR_K_DEC_FIRST))) return rc;
+    const int k = workers_per_launch(dim, n);
+    for (int w0 = 0; w0 < n; w0 += k)
+      if ((rc = run_transform(log2_exact(dim), false, w0, (n - w0 < k ? n - w0 : k), ga, buf, snk, st,
+                              OPTR_K_DEC_FIRST)))
+        return rc;
   } else {
     AsmArgs as;
     memset(&as, 0, sizeof(as));
@@ -875,6 +1015,7 @@ int optr_tar(optr_comm c, const void* x, void* out, int64_t L, int dtype_in, int
   ga.m = mv;
   ga.got = nullptr;
   ga.dim = dim;
+  ga.pow2_shift = (sh.extra == 0 && is_pow2(sh.base)) ? log2_exact(sh.base) : -1;
   if (ht) {
     SrcBuf buf;
     memset(&buf, 0, sizeof(buf));

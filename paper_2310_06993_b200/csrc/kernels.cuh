@@ -340,6 +340,7 @@ struct SrcGather {
   MaskView m;
   uint8_t* got;  // optional [n][dim]
   int64_t dim;
+  int pow2_shift;  // log2(shard length) when all shards are one power of two, else -1
   struct B {
     const SrcGather* p;  // param space
     int q;
@@ -366,25 +367,32 @@ struct SrcGather {
       if (p->got) p->got[(int64_t)q * p->dim + g] = ok ? 1 : 0;
       return ok ? p->A[owner][e] : 0.f;
     }
+    // 4 consecutive entries inside one shard, e = offset of the first
+    __device__ __forceinline__ float4 load4_in(const float* a, const uint32_t* row, uint32_t e, int64_t g) const {
+      float4 v = ldg4(a + e);
+      if (row) {
+        Pkt4 pk = pkt4(e, (uint32_t)p->m.epp);
+        bool k0 = row_bit(row, pk.p[0]), k1 = row_bit(row, pk.p[1]);
+        bool k2 = row_bit(row, pk.p[2]), k3 = row_bit(row, pk.p[3]);
+        v.x = k0 ? v.x : 0.f;
+        v.y = k1 ? v.y : 0.f;
+        v.z = k2 ? v.z : 0.f;
+        v.w = k3 ? v.w : 0.f;
+        if (p->got) *reinterpret_cast<uchar4*>(p->got + (int64_t)q * p->dim + g) = make_uchar4(k0, k1, k2, k3);
+      } else if (p->got) {
+        *reinterpret_cast<uchar4*>(p->got + (int64_t)q * p->dim + g) = make_uchar4(1, 1, 1, 1);
+      }
+      return v;
+    }
     __device__ __forceinline__ float4 load4(int64_t g) const {
-      if (uj >= 0 && ((g - uoff) & 3) == 0) {
-        float4 v = ldg4(ua + g);
-        if (urow) {
-          Pkt4 pk = pkt4((uint32_t)(g - uoff), (uint32_t)p->m.epp);
-          bool k0 = row_bit(urow, pk.p[0]), k1 = row_bit(urow, pk.p[1]);
-          bool k2 = row_bit(urow, pk.p[2]), k3 = row_bit(urow, pk.p[3]);
-          v.x = k0 ? v.x : 0.f;
-          v.y = k1 ? v.y : 0.f;
-          v.z = k2 ? v.z : 0.f;
-          v.w = k3 ? v.w : 0.f;
-          if (p->got) {
-            uchar4 gb = make_uchar4(k0, k1, k2, k3);
-            *reinterpret_cast<uchar4*>(p->got + (int64_t)q * p->dim + g) = gb;
-          }
-        } else if (p->got) {
-          *reinterpret_cast<uchar4*>(p->got + (int64_t)q * p->dim + g) = make_uchar4(1, 1, 1, 1);
+      if (uj >= 0 && ((g - uoff) & 3) == 0) return load4_in(ua + uoff, urow, (uint32_t)(g - uoff), g);
+      if (p->pow2_shift >= 0) {  // equal power-of-two shards (pow2 dim, pow2 n)
+        const int j = (int)(g >> p->pow2_shift);
+        const uint32_t e = (uint32_t)(g & ((1LL << p->pow2_shift) - 1));
+        if ((e & 3) == 0 && (int64_t)e + 4 <= (1LL << p->pow2_shift)) {
+          const int owner = shard_owner(j, p->r, p->n);
+          return load4_in(p->A[owner], owner == q ? nullptr : p->m.row(1, q, owner), e, g);
         }
-        return v;
       }
       return make_float4(load1(g), load1(g + 1), load1(g + 2), load1(g + 3));
     }
