@@ -303,6 +303,67 @@ int try_tma_strided(int cls, const PassGeom& pg, int nlog, int worker, int nwork
   }
 }
 
+
+template <int T, int SK, class Snk>
+int launch_tma_contig_kernel(int cls, const TmaContigArgs& a, const Snk& snk, int worker, cudaStream_t st) {
+  const size_t smem = tma_contig_smem_bytes<T>();
+  int rc = set_smem_attr(tma_contig_kernel<T, SK, Snk>, smem);
+  if (rc) return rc;
+  static int nsm = 0;
+  if (!nsm) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    if (nsm <= 0) nsm = 148;
+  }
+  const int per_sm = (int)((227 * 1024) / smem) > 0 ? (int)((227 * 1024) / smem) : 1;
+  int64_t gx = (int64_t)nsm * per_sm;
+  if (gx > a.ntiles) gx = a.ntiles;
+  KScope ks(cls, st);
+  tma_contig_kernel<T, SK, Snk><<<(unsigned)gx, 1 << (T - 5), smem, st>>>(a, snk, worker);
+  return launch_check(tma_contig_kernel<T, SK, Snk>, "tma_contig", T, 0, (int)gx, 1, 1 << (T - 5), smem);
+}
+
+// Contiguous pass through bulk copies when the shapes allow; -1 otherwise.
+template <class Src, class Snk>
+int try_tma_contig(int cls, const PassGeom& pg, int nlog, int worker, int nworkers, const Src& src, const Snk& snk,
+                   cudaStream_t st) {
+  constexpr bool kBuf = std::is_same<Src, SrcBuf>::value;
+  constexpr bool kEnc = std::is_same<Src, SrcEncode>::value;
+  constexpr bool kGather = std::is_same<Src, SrcGather>::value;
+  if constexpr (!(kBuf || kEnc || kGather)) {
+    return -1;
+  } else {
+    const int T = pg.cb + pg.ks;
+    if (pg.cb != 0 || pg.lo != 0 || nworkers != 1 || (T != 13 && T != 14) || !tma_enabled()) return -1;
+    (void)nlog;
+    TmaContigArgs a;
+    memset(&a, 0, sizeof(a));
+    a.ntiles = pg.ntiles;
+    if constexpr (kBuf) {
+      a.x = src.y[worker];
+    } else if constexpr (kEnc) {
+      a.x = src.x[worker];
+      a.dtype = src.dtype;
+      a.L = src.L;
+      a.signs = src.signs;
+      if (((uintptr_t)a.x & 15) || ((uintptr_t)a.signs & 15)) return -1;
+    } else {
+      if (src.pow2_shift < T) return -1;
+      for (int o = 0; o < src.n; ++o) a.A[o] = src.A[o];
+      a.q = worker;
+      a.n = src.n;
+      a.r = src.r;
+      a.shard_shift = src.pow2_shift;
+      a.m = src.m;
+      a.got = src.got ? src.got + (int64_t)worker * src.dim : nullptr;
+    }
+    constexpr int SK = kBuf ? CS_BUF : (kEnc ? CS_ENC : CS_GATHER);
+    if (T == 13) return launch_tma_contig_kernel<13, SK>(cls, a, snk, worker, st);
+    return launch_tma_contig_kernel<14, SK>(cls, a, snk, worker, st);
+  }
+}
+
 template <class S>
 constexpr bool kStridedSrc = !std::is_same<S, SrcEncode>::value;
 template <class S>
@@ -314,6 +375,8 @@ int launch_pass(int cls, const PassGeom& pg, int nlog, int worker_base, int nwor
   const int T = pg.cb + pg.ks;
   {
     int rc = try_tma_strided(cls, pg, nlog, worker_base, nworkers, src, snk, st);
+    if (rc >= 0) return rc;
+    rc = try_tma_contig(cls, pg, nlog, worker_base, nworkers, src, snk, st);
     if (rc >= 0) return rc;
   }
   if (pg.cb == 0 && pg.lo == 0 && T == 13) return launch_rtile<13, 0, 0>(cls, pg, worker_base, nworkers, src, snk, st);

@@ -229,3 +229,197 @@ __global__ void __launch_bounds__(1 << (T - 5)) tma_strided_kernel(const __grid_
 }
 
 }  // namespace optr
+
+namespace optr {
+
+// ------------------------------------------------ TMA contiguous pass
+// Tiles are 2^T contiguous entries.  Loads are 1D bulk copies
+// (cp.async.bulk) into a two-stage shared-memory ring; the source transform
+// (encode: pad + signs + bf16 upcast; gather: owner shard + stage-2 mask) is
+// applied when the tile is read out of shared memory; results are stored
+// with vector STG (each warp writes 512 contiguous bytes).
+enum ContigSrc { CS_BUF = 0, CS_ENC = 1, CS_GATHER = 2 };
+
+struct TmaContigArgs {
+  int64_t ntiles;
+  // CS_BUF / CS_ENC: source vector (fp32, or x of dtype_in for CS_ENC)
+  const void* x;
+  int dtype;
+  int64_t L;              // CS_ENC: entries of x (the rest of the tile is padding)
+  const uint32_t* signs;  // CS_ENC
+  // CS_GATHER (collectives.py:140-150)
+  const float* A[kMaxW];
+  int q, n, r;
+  int shard_shift;  // equal power-of-two shards of 2^shard_shift >= 2^T entries
+  MaskView m;
+  uint8_t* got;  // optional, already offset to worker q
+};
+
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
+template <int T, int SK>
+__device__ __forceinline__ void contig_issue(const TmaContigArgs& a, int64_t t, unsigned char* stage, uint32_t* sgn,
+                                             uint64_t* bar) {
+  const int64_t g0 = t << T;
+  if (SK == CS_GATHER) {
+    const int j = (int)(g0 >> a.shard_shift);
+    const int owner = shard_owner(j, a.r, a.n);
+    const int64_t e0 = g0 - ((int64_t)j << a.shard_shift);
+    mbar_expect_tx(bar, (uint32_t)(sizeof(float) << T));
+    bulk_load(stage, a.A[owner] + e0, (uint32_t)(sizeof(float) << T), bar);
+    return;
+  }
+  if (SK == CS_BUF) {
+    mbar_expect_tx(bar, (uint32_t)(sizeof(float) << T));
+    bulk_load(stage, (const float*)a.x + g0, (uint32_t)(sizeof(float) << T), bar);
+    return;
+  }
+  // CS_ENC: the valid part of x (16-byte multiple) and the tile's sign words
+  const int esz = a.dtype == OPTR_BF16 ? 2 : 4;
+  int64_t valid = a.L - g0;
+  if (valid > (1 << T)) valid = 1 << T;
+  if (valid < 0) valid = 0;
+  uint32_t bytes = (uint32_t)((valid * esz) & ~15LL);
+  const uint32_t sbytes = (uint32_t)(sizeof(uint32_t) << (T - 5));
+  mbar_expect_tx(bar, bytes + sbytes);
+  if (bytes) bulk_load(stage, (const unsigned char*)a.x + g0 * esz, bytes, bar);
+  bulk_load(sgn, a.signs + (g0 >> 5), sbytes, bar);
+}
+
+template <int T>
+constexpr size_t tma_contig_smem_bytes() {
+  return (size_t)2 * (sizeof(float) << T) + (size_t)2 * (sizeof(uint32_t) << (T - 5)) +
+         sizeof(float) * ((size_t)pad(1 << T) + 8) + 64 + 1024;
+}
+
+template <int T, int SK, class Snk>
+__global__ void __launch_bounds__(1 << (T - 5)) tma_contig_kernel(const __grid_constant__ TmaContigArgs a,
+                                                                const __grid_constant__ Snk snk, int worker) {
+  constexpr RPlan P = make_rplan(T, 0);
+  constexpr int NR = P.nr;
+  static_assert(NR == 3, "contiguous TMA kernel expects three register rounds");
+  extern __shared__ unsigned char smraw[];
+  unsigned char* base = (unsigned char*)(((uintptr_t)smraw + 1023) & ~(uintptr_t)1023);
+  unsigned char* stage[2] = {base, base + (sizeof(float) << T)};
+  uint32_t* sgw[2] = {(uint32_t*)(base + 2 * (sizeof(float) << T)),
+                      (uint32_t*)(base + 2 * (sizeof(float) << T)) + (1 << (T - 5))};
+  float* work = (float*)(base + 2 * (sizeof(float) << T) + 2 * (sizeof(uint32_t) << (T - 5)));
+  uint64_t* full = (uint64_t*)(work + pad(1 << T) + 8);
+
+  const int tid = threadIdx.x;
+  const int b0 = thread_base<T>(P, 0, tid);
+  const int b1 = thread_base<T>(P, 1, tid);
+  const int b2 = thread_base<T>(P, 2, tid);
+  float* const w0 = work + pad(b0);
+  float* const w1 = work + pad(b1);
+  float* const w2 = work + pad(b2);
+  const auto d = snk.bind(worker);
+
+  if (tid == 0) {
+    mbar_init(&full[0], 1);
+    mbar_init(&full[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int64_t stride = gridDim.x;
+  int64_t t = blockIdx.x;
+  if (tid == 0) {
+    if (t < a.ntiles) contig_issue<T, SK>(a, t, stage[0], sgw[0], &full[0]);
+    if (t + stride < a.ntiles) contig_issue<T, SK>(a, t + stride, stage[1], sgw[1], &full[1]);
+  }
+  for (int k = 0; t < a.ntiles; ++k, t += stride) {
+    const int buf = k & 1;
+    mbar_wait(&full[buf], (uint32_t)((k >> 1) & 1));
+    const int64_t g0 = t << T;
+    float v[32];
+#pragma unroll
+    for (int m = 0; m < 8; ++m) {
+      const int i = b0 + roff(P, 0, 4 * m);
+      float4 q4;
+      if (SK == CS_ENC) {
+        const int64_t g = g0 + i;
+        if (a.dtype == OPTR_BF16) {
+          const uint2 u = *reinterpret_cast<const uint2*>(stage[buf] + (size_t)i * 2);
+          const float2 fa = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.x));
+          const float2 fb = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.y));
+          q4 = make_float4(fa.x, fa.y, fb.x, fb.y);
+        } else {
+          q4 = *reinterpret_cast<const float4*>(stage[buf] + (size_t)i * 4);
+        }
+        const int esz = a.dtype == OPTR_BF16 ? 2 : 4;
+        const int64_t bulk_end = g0 + ((((a.L - g0) * esz) & ~15LL) / esz);
+        if (g + 4 > bulk_end) {  // past the bulk copy: unaligned tail of x, then padding
+          float e[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+            if (g + c < a.L) e[c] = load_elem(a.x, a.dtype, g + c);
+          q4 = make_float4(e[0], e[1], e[2], e[3]);
+        }
+        const uint32_t sw = sgw[buf][i >> 5];
+        const int bb = i & 31;
+        q4.x = sgn(sw, bb, q4.x);
+        q4.y = sgn(sw, bb + 1, q4.y);
+        q4.z = sgn(sw, bb + 2, q4.z);
+        q4.w = sgn(sw, bb + 3, q4.w);
+      } else {
+        q4 = *reinterpret_cast<const float4*>(stage[buf] + (size_t)i * 4);
+        if (SK == CS_GATHER) {
+          const int64_t g = g0 + i;
+          const int j = (int)(g >> a.shard_shift);
+          const int owner = shard_owner(j, a.r, a.n);
+          const uint32_t e = (uint32_t)(g - ((int64_t)j << a.shard_shift));
+          if (owner != a.q) {
+            const uint32_t* row = a.m.row(1, a.q, owner);
+            const Pkt4 pk = pkt4(e, (uint32_t)a.m.epp);
+            const bool k0 = row_bit(row, pk.p[0]), k1 = row_bit(row, pk.p[1]);
+            const bool k2 = row_bit(row, pk.p[2]), k3 = row_bit(row, pk.p[3]);
+            q4.x = k0 ? q4.x : 0.f;
+            q4.y = k1 ? q4.y : 0.f;
+            q4.z = k2 ? q4.z : 0.f;
+            q4.w = k3 ? q4.w : 0.f;
+            if (a.got) *reinterpret_cast<uchar4*>(a.got + g) = make_uchar4(k0, k1, k2, k3);
+          } else if (a.got) {
+            *reinterpret_cast<uchar4*>(a.got + g) = make_uchar4(1, 1, 1, 1);
+          }
+        }
+      }
+      v[4 * m] = q4.x;
+      v[4 * m + 1] = q4.y;
+      v[4 * m + 2] = q4.z;
+      v[4 * m + 3] = q4.w;
+    }
+    bfly32<P.xm[0]>(v);
+#pragma unroll
+    for (int j = 0; j < 32; ++j) w0[pad(roff(P, 0, j))] = v[j];
+    __syncthreads();  // everyone has read stage[buf]; work holds round A
+    if (tid == 0 && t + 2 * stride < a.ntiles) contig_issue<T, SK>(a, t + 2 * stride, stage[buf], sgw[buf], &full[buf]);
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] = w1[pad(roff(P, 1, j))];
+    bfly32<P.xm[1]>(v);
+#pragma unroll
+    for (int j = 0; j < 32; ++j) w1[pad(roff(P, 1, j))] = v[j];
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] = w2[pad(roff(P, 2, j))];
+    bfly32<P.xm[2]>(v);
+    if constexpr (P.pos[2][0] == 0 && P.pos[2][1] == 1) {
+#pragma unroll
+      for (int m = 0; m < 8; ++m)
+        d.store4(g0 + b2 + roff(P, 2, 4 * m), make_float4(v[4 * m], v[4 * m + 1], v[4 * m + 2], v[4 * m + 3]));
+    } else if constexpr (P.pos[2][0] == 0) {
+#pragma unroll
+      for (int m = 0; m < 16; ++m) d.store2(g0 + b2 + roff(P, 2, 2 * m), v[2 * m], v[2 * m + 1]);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) d.store1(g0 + b2 + roff(P, 2, j), v[j]);
+    }
+    __syncthreads();  // work is free for the next tile
+  }
+}
+
+}  // namespace optr

@@ -10,5 +10,5 @@ timeout 600 python bench.py --steps 10 --warmup 3 "$@" > $OUT/bench.log 2>&1; ec
 CMD="python bench.py --steps 1 --warmup 3 --no-cpu-baseline $*"
 timeout 600 $CMD > $OUT/plain.log 2>&1 && \
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches.csv $CMD > $OUT/ncu_launch.log 2>&1
-timeout 900 ncu --set full --import-source on --clock-control none -k regex:"rtile|aggregate|prep" -s 12 -c 6 -o $OUT/prof $CMD > $OUT/ncu_full.log 2>&1
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:"tma|rtile|aggregate|prep" -s 24 -c 8 -o $OUT/prof $CMD > $OUT/ncu_full.log 2>&1
 echo done
