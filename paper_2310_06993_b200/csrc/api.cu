@@ -697,6 +697,83 @@ int optr_rht_decode(const float* y, const uint8_t* mask, int64_t dim, int64_t L,
   return rc;
 }
 
+
+}  // extern "C"
+
+namespace {
+// ------------------------------------------------------- helper streams
+// Per-worker pass chains run on two helper streams forked from (and joined
+// back into) the caller's stream, so one worker's passes fill the ramp and
+// tail of the other's while both vectors stay L2-resident.
+constexpr int kHelpers = 2;
+struct Helpers {
+  bool init = false;
+  cudaStream_t s[kHelpers];
+  cudaEvent_t fork;
+  cudaEvent_t join[kHelpers];
+  std::mutex mu;
+};
+Helpers g_help[64];
+
+Helpers* helpers() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  Helpers* h = &g_help[dev & 63];
+  std::lock_guard<std::mutex> lk(g_attr_mu);
+  if (!h->init) {
+    for (int i = 0; i < kHelpers; ++i) {
+      if (cudaStreamCreateWithFlags(&h->s[i], cudaStreamNonBlocking) != cudaSuccess) return nullptr;
+      if (cudaEventCreateWithFlags(&h->join[i], cudaEventDisableTiming) != cudaSuccess) return nullptr;
+    }
+    if (cudaEventCreateWithFlags(&h->fork, cudaEventDisableTiming) != cudaSuccess) return nullptr;
+    h->init = true;
+  }
+  return h;
+}
+
+int fork_helpers(Helpers* h, cudaStream_t st) {
+  CK(cudaEventRecord(h->fork, st));
+  for (int i = 0; i < kHelpers; ++i) CK(cudaStreamWaitEvent(h->s[i], h->fork, 0));
+  return OPTR_OK;
+}
+
+int join_helpers(Helpers* h, cudaStream_t st) {
+  for (int i = 0; i < kHelpers; ++i) {
+    CK(cudaEventRecord(h->join[i], h->s[i]));
+    CK(cudaStreamWaitEvent(st, h->join[i], 0));
+  }
+  return OPTR_OK;
+}
+
+// Run `fn(worker_base, nworkers, stream)` over all n workers: batched while
+// they fit in L2 together, else one worker per launch on the helper streams.
+template <class F>
+int for_workers(int64_t dim, int n, cudaStream_t st, F fn) {
+  const int k = workers_per_launch(dim, n);
+  if (k >= n) return fn(0, n, st);
+  Helpers* h = helpers();
+  if (!h) {
+    for (int w0 = 0; w0 < n; w0 += k) {
+      int rc = fn(w0, (n - w0 < k ? n - w0 : k), st);
+      if (rc) return rc;
+    }
+    return OPTR_OK;
+  }
+  std::lock_guard<std::mutex> lk(h->mu);
+  int rc = fork_helpers(h, st);
+  if (rc) return rc;
+  int i = 0;
+  for (int w0 = 0; w0 < n; w0 += k, ++i) {
+    rc = fn(w0, (n - w0 < k ? n - w0 : k), h->s[i % kHelpers]);
+    if (rc) break;
+  }
+  int rc2 = join_helpers(h, st);
+  return rc ? rc : rc2;
+}
+}  // namespace
+
+extern "C" {
+
 // -------------------------------------------------- TAR, n workers, one GPU
 struct LocalLayout {
   size_t y, a, signs, bitmap, counts, total;
@@ -780,11 +857,10 @@ int optr_tar_local(const void* const* x, void* const* out, int n, int64_t L, int
       Yw[w] = Y + (size_t)w * dim;
     }
     snk.scale = (float)(1.0 / sqrt((double)dim));
-    const int k = workers_per_launch(dim, n);
-    for (int w0 = 0; w0 < n; w0 += k)
-      if ((rc = run_transform(log2_exact(dim), true, w0, (n - w0 < k ? n - w0 : k), src, buf, snk, st,
-                              OPTR_K_ENC_FIRST)))
-        return rc;
+    rc = for_workers(dim, n, st, [&](int w0, int nw, cudaStream_t s2) {
+      return run_transform(log2_exact(dim), true, w0, nw, src, buf, snk, s2, OPTR_K_ENC_FIRST);
+    });
+    if (rc) return rc;
   } else {
     for (int w = 0; w < n; ++w) {
       if (dtype_in == OPTR_F32) {
@@ -840,11 +916,10 @@ int optr_tar_local(const void* const* x, void* const* out, int n, int64_t L, int
     snk.count_extra = counts + n;  // stage-2 row
     snk.count_stride = 1;
     snk.dim = (double)dim;
-    const int k = workers_per_launch(dim, n);
-    for (int w0 = 0; w0 < n; w0 += k)
-      if ((rc = run_transform(log2_exact(dim), false, w0, (n - w0 < k ? n - w0 : k), ga, buf, snk, st,
-                              OPTR_K_DEC_FIRST)))
-        return rc;
+    rc = for_workers(dim, n, st, [&](int w0, int nw, cudaStream_t s2) {
+      return run_transform(log2_exact(dim), false, w0, nw, ga, buf, snk, s2, OPTR_K_DEC_FIRST);
+    });
+    if (rc) return rc;
   } else {
     AsmArgs as;
     memset(&as, 0, sizeof(as));

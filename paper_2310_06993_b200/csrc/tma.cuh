@@ -121,7 +121,7 @@ __global__ void __launch_bounds__(1 << (T - 5)) tma_strided_kernel(const __grid_
   extern __shared__ unsigned char smraw[];
   // 1024-byte aligned base for the TMA buffers
   unsigned char* base = (unsigned char*)(((uintptr_t)smraw + 1023) & ~(uintptr_t)1023);
-  float* stage[2] = {(float*)base, (float*)base + (1 << T)};
+  float* const stage0 = (float*)base;
   float* work = (float*)base + 2 * (1 << T);
   uint64_t* full = (uint64_t*)(work + pad(1 << T) + 8);
 
@@ -142,18 +142,18 @@ __global__ void __launch_bounds__(1 << (T - 5)) tma_strided_kernel(const __grid_
   const int64_t stride = gridDim.x;
   int64_t t = blockIdx.x;
   if (tid == 0) {
-    if (t < a.ntiles) tma_issue_load<T, GATHER>(src, a, t, stage[0], &full[0]);
-    if (t + stride < a.ntiles) tma_issue_load<T, GATHER>(src, a, t + stride, stage[1], &full[1]);
+    if (t < a.ntiles) tma_issue_load<T, GATHER>(src, a, t, stage0, &full[0]);
+    if (t + stride < a.ntiles) tma_issue_load<T, GATHER>(src, a, t + stride, stage0 + (1 << T), &full[1]);
   }
   const int cgb = a.lo - 3;
   for (int k = 0; t < a.ntiles; ++k, t += stride) {
     const int buf = k & 1;
     if (tid == 0 && k >= 1 && t + stride < a.ntiles) {
       bulk_wait_read0();  // the store of tile k-1 has read stage[buf^1]
-      tma_issue_load<T, GATHER>(src, a, t + stride, stage[buf ^ 1], &full[buf ^ 1]);
+      tma_issue_load<T, GATHER>(src, a, t + stride, stage0 + ((buf ^ 1) << T), &full[buf ^ 1]);
     }
     mbar_wait(&full[buf], (uint32_t)((k >> 1) & 1));
-    float* sb = stage[buf];
+    float* sb = stage0 + (buf << T);
     float v[32];
     // round A: dense tile, float4 per (row, 4 columns)
 #pragma unroll
@@ -305,9 +305,8 @@ __global__ void __launch_bounds__(1 << (T - 5)) tma_contig_kernel(const __grid_c
   static_assert(NR == 3, "contiguous TMA kernel expects three register rounds");
   extern __shared__ unsigned char smraw[];
   unsigned char* base = (unsigned char*)(((uintptr_t)smraw + 1023) & ~(uintptr_t)1023);
-  unsigned char* stage[2] = {base, base + (sizeof(float) << T)};
-  uint32_t* sgw[2] = {(uint32_t*)(base + 2 * (sizeof(float) << T)),
-                      (uint32_t*)(base + 2 * (sizeof(float) << T)) + (1 << (T - 5))};
+  unsigned char* const stage0 = base;
+  uint32_t* const sgw0 = (uint32_t*)(base + 2 * (sizeof(float) << T));
   float* work = (float*)(base + 2 * (sizeof(float) << T) + 2 * (sizeof(uint32_t) << (T - 5)));
   uint64_t* full = (uint64_t*)(work + pad(1 << T) + 8);
 
@@ -329,13 +328,21 @@ __global__ void __launch_bounds__(1 << (T - 5)) tma_contig_kernel(const __grid_c
   const int64_t stride = gridDim.x;
   int64_t t = blockIdx.x;
   if (tid == 0) {
-    if (t < a.ntiles) contig_issue<T, SK>(a, t, stage[0], sgw[0], &full[0]);
-    if (t + stride < a.ntiles) contig_issue<T, SK>(a, t + stride, stage[1], sgw[1], &full[1]);
+    if (t < a.ntiles) contig_issue<T, SK>(a, t, stage0, sgw0, &full[0]);
+    if (t + stride < a.ntiles)
+      contig_issue<T, SK>(a, t + stride, stage0 + (sizeof(float) << T), sgw0 + (1 << (T - 5)), &full[1]);
   }
   for (int k = 0; t < a.ntiles; ++k, t += stride) {
     const int buf = k & 1;
     mbar_wait(&full[buf], (uint32_t)((k >> 1) & 1));
     const int64_t g0 = t << T;
+    unsigned char* const sb = stage0 + ((size_t)buf * (sizeof(float) << T));
+    const uint32_t* const sw0 = sgw0 + (buf << (T - 5));
+    int64_t bulk_end = 0;
+    if (SK == CS_ENC) {
+      const int lsh = a.dtype == OPTR_BF16 ? 1 : 2;
+      bulk_end = g0 + ((((a.L - g0) << lsh) & ~15LL) >> lsh);
+    }
     float v[32];
 #pragma unroll
     for (int m = 0; m < 8; ++m) {
@@ -344,15 +351,13 @@ __global__ void __launch_bounds__(1 << (T - 5)) tma_contig_kernel(const __grid_c
       if (SK == CS_ENC) {
         const int64_t g = g0 + i;
         if (a.dtype == OPTR_BF16) {
-          const uint2 u = *reinterpret_cast<const uint2*>(stage[buf] + (size_t)i * 2);
+          const uint2 u = *reinterpret_cast<const uint2*>(sb + (size_t)i * 2);
           const float2 fa = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.x));
           const float2 fb = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.y));
           q4 = make_float4(fa.x, fa.y, fb.x, fb.y);
         } else {
-          q4 = *reinterpret_cast<const float4*>(stage[buf] + (size_t)i * 4);
+          q4 = *reinterpret_cast<const float4*>(sb + (size_t)i * 4);
         }
-        const int esz = a.dtype == OPTR_BF16 ? 2 : 4;
-        const int64_t bulk_end = g0 + ((((a.L - g0) * esz) & ~15LL) / esz);
         if (g + 4 > bulk_end) {  // past the bulk copy: unaligned tail of x, then padding
           float e[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
@@ -360,14 +365,14 @@ __global__ void __launch_bounds__(1 << (T - 5)) tma_contig_kernel(const __grid_c
             if (g + c < a.L) e[c] = load_elem(a.x, a.dtype, g + c);
           q4 = make_float4(e[0], e[1], e[2], e[3]);
         }
-        const uint32_t sw = sgw[buf][i >> 5];
+        const uint32_t sw = sw0[i >> 5];
         const int bb = i & 31;
         q4.x = sgn(sw, bb, q4.x);
         q4.y = sgn(sw, bb + 1, q4.y);
         q4.z = sgn(sw, bb + 2, q4.z);
         q4.w = sgn(sw, bb + 3, q4.w);
       } else {
-        q4 = *reinterpret_cast<const float4*>(stage[buf] + (size_t)i * 4);
+        q4 = *reinterpret_cast<const float4*>(sb + (size_t)i * 4);
         if (SK == CS_GATHER) {
           const int64_t g = g0 + i;
           const int j = (int)(g >> a.shard_shift);
@@ -397,7 +402,8 @@ __global__ void __launch_bounds__(1 << (T - 5)) tma_contig_kernel(const __grid_c
 #pragma unroll
     for (int j = 0; j < 32; ++j) w0[pad(roff(P, 0, j))] = v[j];
     __syncthreads();  // everyone has read stage[buf]; work holds round A
-    if (tid == 0 && t + 2 * stride < a.ntiles) contig_issue<T, SK>(a, t + 2 * stride, stage[buf], sgw[buf], &full[buf]);
+    if (tid == 0 && t + 2 * stride < a.ntiles)
+      contig_issue<T, SK>(a, t + 2 * stride, sb, sgw0 + (buf << (T - 5)), &full[buf]);
 #pragma unroll
     for (int j = 0; j < 32; ++j) v[j] = w1[pad(roff(P, 1, j))];
     bfly32<P.xm[1]>(v);
