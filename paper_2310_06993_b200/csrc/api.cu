@@ -233,11 +233,12 @@ bool make_map3(CUtensorMap* m, const void* base, uint64_t d0, uint64_t d1, uint6
   return r == CUDA_SUCCESS;
 }
 
-template <int T, bool GATHER>
-int launch_tma_kernel(int cls, const TmaMaps& src, const CUtensorMap& dst, const TmaStridedArgs& a,
-                      cudaStream_t st) {
+template <int T, bool STRIDED, int SK, class Snk>
+int launch_tma_pass(int cls, const TmaMaps& maps, const CUtensorMap& dmap, const TmaArgs& a, const Snk& snk,
+                    int worker, cudaStream_t st) {
   const size_t smem = tma_smem_bytes<T>();
-  int rc = set_smem_attr(tma_strided_kernel<T, GATHER>, smem);
+  auto kern = tma_pass_kernel<T, STRIDED, SK, Snk>;
+  int rc = set_smem_attr(kern, smem);
   if (rc) return rc;
   static int nsm = 0;
   if (!nsm) {
@@ -246,100 +247,75 @@ int launch_tma_kernel(int cls, const TmaMaps& src, const CUtensorMap& dst, const
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     if (nsm <= 0) nsm = 148;
   }
-  const int per_sm = (int)((227 * 1024) / smem) > 0 ? (int)((227 * 1024) / smem) : 1;
+  int per_sm = (int)((227 * 1024) / (smem + 1024));
+  if (per_sm < 1) per_sm = 1;
   int64_t gx = (int64_t)nsm * per_sm;
   if (gx > a.ntiles) gx = a.ntiles;
   KScope ks(cls, st);
-  tma_strided_kernel<T, GATHER><<<(unsigned)gx, 1 << (T - 5), smem, st>>>(src, dst, a);
-  return launch_check(tma_strided_kernel<T, GATHER>, GATHER ? "tma_gather" : "tma_strided", T, 3, (int)gx, 1,
-                      1 << (T - 5), smem);
+  kern<<<(unsigned)gx, 1 << (T - 5), smem, st>>>(maps, dmap, a, snk, worker);
+  return launch_check(kern, STRIDED ? "tma_strided" : "tma_contig", T, STRIDED ? 3 : 0, (int)gx, 1, 1 << (T - 5),
+                      smem);
 }
 
-// Strided pass through TMA when the shapes allow it; returns -1 when the
-// caller should use the LSU kernel instead.
+// A pass through the TMA ring kernel when the shapes allow it; -1 when the
+// caller should use the LSU kernels instead.
 template <class Src, class Snk>
-int try_tma_strided(int cls, const PassGeom& pg, int nlog, int worker, int nworkers, const Src& src, const Snk& snk,
-                    cudaStream_t st) {
+int try_tma(int cls, const PassGeom& pg, int nlog, int worker, int nworkers, const Src& src, const Snk& snk,
+            cudaStream_t st) {
   constexpr bool kBuf = std::is_same<Src, SrcBuf>::value;
+  constexpr bool kEnc = std::is_same<Src, SrcEncode>::value;
   constexpr bool kGather = std::is_same<Src, SrcGather>::value;
-  if constexpr (!(kBuf || kGather) || !std::is_same<Snk, SnkBuf>::value) {
+  constexpr bool kSnkBuf = std::is_same<Snk, SnkBuf>::value;
+  constexpr int SK = kBuf ? TS_BUF : (kEnc ? TS_ENC : TS_GATHER);
+  if constexpr (!(kBuf || kEnc || kGather)) {
     return -1;
   } else {
     const int T = pg.cb + pg.ks;
-    if (pg.cb != 3 || nworkers != 1 || T < 12 || T > 14 || !tma_enabled()) return -1;
-    const uint64_t d0 = 1ULL << pg.lo, d1 = 1ULL << pg.ks, d2 = 1ULL << (nlog - pg.lo - pg.ks);
-    TmaStridedArgs a;
+    if (nworkers != 1 || !tma_enabled()) return -1;
+    TmaArgs a;
     memset(&a, 0, sizeof(a));
     a.ntiles = pg.ntiles;
     a.lo = pg.lo;
-    a.scale = snk.scale;
-    int box = (int)(d1 < 256 ? d1 : 256);
     TmaMaps maps;
     memset(&maps, 0, sizeof(maps));
+    CUtensorMap dmap;
+    memset(&dmap, 0, sizeof(dmap));
     if constexpr (kGather) {
-      if (src.pow2_shift < pg.lo || d2 != 1) return -1;
-      const int64_t srows = 1LL << (src.pow2_shift - pg.lo);
-      if (srows < box) box = (int)srows;
-      for (int o = 0; o < src.n; ++o)
-        if (!make_map3(&maps.m[o], src.A[o], d0, (uint64_t)srows, 1, (uint32_t)box)) return -1;
+      for (int o = 0; o < src.n; ++o) a.A[o] = src.A[o];
       a.q = worker;
       a.n = src.n;
       a.r = src.r;
       a.shard_shift = src.pow2_shift;
       a.m = src.m;
       a.got = src.got ? src.got + (int64_t)worker * src.dim : nullptr;
-      a.dim = src.dim;
-    } else {
-      if (!make_map3(&maps.m[0], src.y[worker], d0, d1, d2, (uint32_t)box)) return -1;
     }
-    a.box_rows = box;
-    CUtensorMap dmap;
-    if (!make_map3(&dmap, snk.y[worker], d0, d1, d2, (uint32_t)box)) return -1;
-    switch (T) {
-      case 12: return launch_tma_kernel<12, kGather>(cls, maps, dmap, a, st);
-      case 13: return launch_tma_kernel<13, kGather>(cls, maps, dmap, a, st);
-      default: return launch_tma_kernel<14, kGather>(cls, maps, dmap, a, st);
+    if (pg.cb == 3) {  // strided: tensor boxes in, tensor boxes out
+      if constexpr (kEnc || !kSnkBuf) {
+        return -1;
+      } else {
+        if (T < 12 || T > 14) return -1;
+        const uint64_t d0 = 1ULL << pg.lo, d1 = 1ULL << pg.ks, d2 = 1ULL << (nlog - pg.lo - pg.ks);
+        int box = (int)(d1 < 256 ? d1 : 256);
+        if constexpr (kGather) {
+          if (src.pow2_shift < pg.lo || d2 != 1) return -1;
+          const int64_t srows = 1LL << (src.pow2_shift - pg.lo);
+          if (srows < box) box = (int)srows;
+          for (int o = 0; o < src.n; ++o)
+            if (!make_map3(&maps.m[o], src.A[o], d0, (uint64_t)srows, 1, (uint32_t)box)) return -1;
+        } else {
+          if (!make_map3(&maps.m[0], src.y[worker], d0, d1, d2, (uint32_t)box)) return -1;
+        }
+        if (!make_map3(&dmap, snk.y[worker], d0, d1, d2, (uint32_t)box)) return -1;
+        a.box_rows = box;
+        a.scale = snk.scale;
+        switch (T) {
+          case 12: return launch_tma_pass<12, true, SK>(cls, maps, dmap, a, snk, worker, st);
+          case 13: return launch_tma_pass<13, true, SK>(cls, maps, dmap, a, snk, worker, st);
+          default: return launch_tma_pass<14, true, SK>(cls, maps, dmap, a, snk, worker, st);
+        }
+      }
     }
-  }
-}
-
-
-template <int T, int SK, class Snk>
-int launch_tma_contig_kernel(int cls, const TmaContigArgs& a, const Snk& snk, int worker, cudaStream_t st) {
-  const size_t smem = tma_contig_smem_bytes<T>();
-  int rc = set_smem_attr(tma_contig_kernel<T, SK, Snk>, smem);
-  if (rc) return rc;
-  static int nsm = 0;
-  if (!nsm) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    if (nsm <= 0) nsm = 148;
-  }
-  const int per_sm = (int)((227 * 1024) / smem) > 0 ? (int)((227 * 1024) / smem) : 1;
-  int64_t gx = (int64_t)nsm * per_sm;
-  if (gx > a.ntiles) gx = a.ntiles;
-  KScope ks(cls, st);
-  tma_contig_kernel<T, SK, Snk><<<(unsigned)gx, 1 << (T - 5), smem, st>>>(a, snk, worker);
-  return launch_check(tma_contig_kernel<T, SK, Snk>, "tma_contig", T, 0, (int)gx, 1, 1 << (T - 5), smem);
-}
-
-// Contiguous pass through bulk copies when the shapes allow; -1 otherwise.
-template <class Src, class Snk>
-int try_tma_contig(int cls, const PassGeom& pg, int nlog, int worker, int nworkers, const Src& src, const Snk& snk,
-                   cudaStream_t st) {
-  constexpr bool kBuf = std::is_same<Src, SrcBuf>::value;
-  constexpr bool kEnc = std::is_same<Src, SrcEncode>::value;
-  constexpr bool kGather = std::is_same<Src, SrcGather>::value;
-  if constexpr (!(kBuf || kEnc || kGather)) {
-    return -1;
-  } else {
-    const int T = pg.cb + pg.ks;
-    if (pg.cb != 0 || pg.lo != 0 || nworkers != 1 || (T != 13 && T != 14) || !tma_enabled()) return -1;
-    (void)nlog;
-    TmaContigArgs a;
-    memset(&a, 0, sizeof(a));
-    a.ntiles = pg.ntiles;
+    if (pg.cb != 0 || pg.lo != 0 || (T != 13 && T != 14)) return -1;
     if constexpr (kBuf) {
       a.x = src.y[worker];
     } else if constexpr (kEnc) {
@@ -350,17 +326,9 @@ int try_tma_contig(int cls, const PassGeom& pg, int nlog, int worker, int nworke
       if (((uintptr_t)a.x & 15) || ((uintptr_t)a.signs & 15)) return -1;
     } else {
       if (src.pow2_shift < T) return -1;
-      for (int o = 0; o < src.n; ++o) a.A[o] = src.A[o];
-      a.q = worker;
-      a.n = src.n;
-      a.r = src.r;
-      a.shard_shift = src.pow2_shift;
-      a.m = src.m;
-      a.got = src.got ? src.got + (int64_t)worker * src.dim : nullptr;
     }
-    constexpr int SK = kBuf ? CS_BUF : (kEnc ? CS_ENC : CS_GATHER);
-    if (T == 13) return launch_tma_contig_kernel<13, SK>(cls, a, snk, worker, st);
-    return launch_tma_contig_kernel<14, SK>(cls, a, snk, worker, st);
+    if (T == 13) return launch_tma_pass<13, false, SK>(cls, maps, dmap, a, snk, worker, st);
+    return launch_tma_pass<14, false, SK>(cls, maps, dmap, a, snk, worker, st);
   }
 }
 
@@ -374,9 +342,7 @@ int launch_pass(int cls, const PassGeom& pg, int nlog, int worker_base, int nwor
                 const Snk& snk, cudaStream_t st) {
   const int T = pg.cb + pg.ks;
   {
-    int rc = try_tma_strided(cls, pg, nlog, worker_base, nworkers, src, snk, st);
-    if (rc >= 0) return rc;
-    rc = try_tma_contig(cls, pg, nlog, worker_base, nworkers, src, snk, st);
+    int rc = try_tma(cls, pg, nlog, worker_base, nworkers, src, snk, st);
     if (rc >= 0) return rc;
   }
   if (pg.cb == 0 && pg.lo == 0 && T == 13) return launch_rtile<13, 0, 0>(cls, pg, worker_base, nworkers, src, snk, st);
