@@ -162,9 +162,24 @@ __device__ __forceinline__ float4 gather_mask4(const TmaArgs& a, int64_t g, floa
   }
   const uint32_t e = (uint32_t)(g - ((int64_t)j << a.shard_shift));
   const uint32_t* row = a.m.row(1, a.q, owner);
-  const Pkt4 pk = pkt4(e, (uint32_t)a.m.epp);
-  const bool k0 = row_bit(row, pk.p[0]), k1 = row_bit(row, pk.p[1]);
-  const bool k2 = row_bit(row, pk.p[2]), k3 = row_bit(row, pk.p[3]);
+  const uint32_t epp = (uint32_t)a.m.epp;
+  bool k0, k1, k2, k3;
+  if (epp >= 4) {  // the 4 entries span packets p0 and at most p0+1
+    const uint32_t p0 = e / epp, rem = e - p0 * epp;
+    const uint32_t w = __ldg(row + (p0 >> 5));
+    const bool c0 = (w >> (p0 & 31)) & 1u;
+    const bool c1 = (p0 & 31) == 31 ? (__ldg(row + (p0 >> 5) + 1) & 1u) : ((w >> ((p0 & 31) + 1)) & 1u);
+    k0 = c0;
+    k1 = rem + 1 >= epp ? c1 : c0;
+    k2 = rem + 2 >= epp ? c1 : c0;
+    k3 = rem + 3 >= epp ? c1 : c0;
+  } else {
+    const Pkt4 pk = pkt4(e, epp);
+    k0 = row_bit(row, pk.p[0]);
+    k1 = row_bit(row, pk.p[1]);
+    k2 = row_bit(row, pk.p[2]);
+    k3 = row_bit(row, pk.p[3]);
+  }
   if (a.got) *reinterpret_cast<uchar4*>(a.got + g) = make_uchar4(k0, k1, k2, k3);
   return make_float4(k0 ? v.x : 0.f, k1 ? v.y : 0.f, k2 ? v.z : 0.f, k3 ? v.w : 0.f);
 }
@@ -178,16 +193,18 @@ __global__ void __launch_bounds__(1 << (T - 5)) tma_pass_kernel(const __grid_con
   constexpr RPlan P = make_rplan(T, CB);
   static_assert(P.nr == 3, "TMA pass expects three register rounds");
   static_assert(P.pos[0][0] == 0 && P.pos[0][1] == 1, "round A holds float4 groups");
+  static_assert(sizeof(float) * pad(1 << T) <= tma_stage_bytes<T>(), "padded tile fits the stage");
   constexpr size_t SB = tma_stage_bytes<T>();
-  extern __shared__ unsigned char smraw[];
-  unsigned char* const base = (unsigned char*)(((uintptr_t)smraw + 1023) & ~(uintptr_t)1023);
-  uint64_t* const full = (uint64_t*)(base + kStages * SB);
+  extern __shared__ __align__(16) unsigned char smraw[];
+  // 1024-byte aligned ring; indexing smraw keeps the shared address space
+  unsigned char* const base = smraw + ((1024u - (smem_u32(smraw) & 1023u)) & 1023u);
+  uint64_t* const full = reinterpret_cast<uint64_t*>(base + kStages * SB);
 
   const int tid = threadIdx.x;
   const int b0 = thread_base<T>(P, 0, tid);
   const int b1 = thread_base<T>(P, 1, tid);
   const int b2 = thread_base<T>(P, 2, tid);
-  const int z0 = swzc(b0), z1 = swzc(b1), z2 = swzc(b2);
+  const int p0 = pad(b0), p1 = pad(b1), p2 = pad(b2);
   const auto d = snk.bind(worker);
 
   if (tid == 0) {
@@ -214,9 +231,11 @@ __global__ void __launch_bounds__(1 << (T - 5)) tma_pass_kernel(const __grid_con
     float v[32];
     // ---- round A: dense tile, float4 groups, fused source transform
     int64_t bulk_end = 0;
+    bool enc_fast = true;
     if constexpr (SK == TS_ENC) {
       const int lsh = a.dtype == OPTR_BF16 ? 1 : 2;
       bulk_end = g0 + ((((a.L - g0) << lsh) & ~15LL) >> lsh);
+      enc_fast = g0 + (1 << T) <= bulk_end;
     }
 #pragma unroll
     for (int m = 0; m < 8; ++m) {
@@ -232,16 +251,18 @@ __global__ void __launch_bounds__(1 << (T - 5)) tma_pass_kernel(const __grid_con
         } else {
           q4 = *reinterpret_cast<const float4*>(tile + i);
         }
-        if (g + 4 > bulk_end) {  // past the bulk copy: unaligned tail of x, then padding
+        if (!enc_fast && g + 4 > bulk_end) {  // past the bulk copy: unaligned tail of x, then padding
           float e[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
           for (int c = 0; c < 4; ++c)
             if (g + c < a.L) e[c] = load_elem(a.x, a.dtype, g + c);
           q4 = make_float4(e[0], e[1], e[2], e[3]);
         }
-        const uint32_t sw = ((const uint32_t*)(sb + (sizeof(float) << T)))[i >> 5];
-        const int bb = i & 31;
-        q4 = make_float4(sgn(sw, bb, q4.x), sgn(sw, bb + 1, q4.y), sgn(sw, bb + 2, q4.z), sgn(sw, bb + 3, q4.w));
+        const uint32_t sw = reinterpret_cast<const uint32_t*>(sb + (sizeof(float) << T))[i >> 5] >> (i & 31);
+        q4 = make_float4(__int_as_float(__float_as_int(q4.x) ^ ((~sw & 1u) << 31)),
+                         __int_as_float(__float_as_int(q4.y) ^ ((~sw & 2u) << 30)),
+                         __int_as_float(__float_as_int(q4.z) ^ ((~sw & 4u) << 29)),
+                         __int_as_float(__float_as_int(q4.w) ^ ((~sw & 8u) << 28)));
       } else {
         q4 = *reinterpret_cast<const float4*>(tile + i);
         if constexpr (SK == TS_GATHER) q4 = gather_mask4(a, g, q4);
@@ -253,17 +274,19 @@ __global__ void __launch_bounds__(1 << (T - 5)) tma_pass_kernel(const __grid_con
     }
     bfly32<P.xm[0]>(v);
     __syncthreads();  // the dense tile has been read
+    // rounds B, C in the padded layout (it ends exactly where the stage's
+    // sign words end; those were consumed in round A)
 #pragma unroll
-    for (int j = 0; j < 32; ++j) tile[z0 ^ swzc(roff(P, 0, j))] = v[j];
+    for (int j = 0; j < 32; ++j) tile[p0 + pad(roff(P, 0, j))] = v[j];
     __syncthreads();
 #pragma unroll
-    for (int j = 0; j < 32; ++j) v[j] = tile[z1 ^ swzc(roff(P, 1, j))];
+    for (int j = 0; j < 32; ++j) v[j] = tile[p1 + pad(roff(P, 1, j))];
     bfly32<P.xm[1]>(v);
 #pragma unroll
-    for (int j = 0; j < 32; ++j) tile[z1 ^ swzc(roff(P, 1, j))] = v[j];
+    for (int j = 0; j < 32; ++j) tile[p1 + pad(roff(P, 1, j))] = v[j];
     __syncthreads();
 #pragma unroll
-    for (int j = 0; j < 32; ++j) v[j] = tile[z2 ^ swzc(roff(P, 2, j))];
+    for (int j = 0; j < 32; ++j) v[j] = tile[p2 + pad(roff(P, 2, j))];
     bfly32<P.xm[2]>(v);
     __syncthreads();  // the swizzled tile has been read: the stage is free
     if constexpr (!STRIDED) {
