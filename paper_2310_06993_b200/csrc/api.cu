@@ -233,11 +233,11 @@ bool make_map3(CUtensorMap* m, const void* base, uint64_t d0, uint64_t d1, uint6
   return r == CUDA_SUCCESS;
 }
 
-template <int T, bool STRIDED, int SK, class Snk>
-int launch_tma_pass(int cls, const TmaMaps& maps, const CUtensorMap& dmap, const TmaArgs& a, const Snk& snk,
-                    int worker, cudaStream_t st) {
-  const size_t smem = tma_smem_bytes<T>();
-  auto kern = tma_pass_kernel<T, STRIDED, SK, Snk>;
+template <int T, int S, bool STRIDED, int SK, class Snk>
+int launch_tma_pass_s(int cls, const TmaMaps& maps, const CUtensorMap& dmap, const TmaArgs& a, const Snk& snk,
+                      int worker, cudaStream_t st) {
+  const size_t smem = tma_smem_bytes<T, S>();
+  auto kern = tma_pass_kernel<T, S, STRIDED, SK, Snk>;
   int rc = set_smem_attr(kern, smem);
   if (rc) return rc;
   static int nsm = 0;
@@ -255,6 +255,23 @@ int launch_tma_pass(int cls, const TmaMaps& maps, const CUtensorMap& dmap, const
   kern<<<(unsigned)gx, 1 << (T - 5), smem, st>>>(maps, dmap, a, snk, worker);
   return launch_check(kern, STRIDED ? "tma_strided" : "tma_contig", T, STRIDED ? 3 : 0, (int)gx, 1, 1 << (T - 5),
                       smem);
+}
+
+// ring depth of the TMA pass kernels (OPTR_TMA_STAGES=3 for three)
+int tma_stages() {
+  static int s = 0;
+  if (!s) {
+    const char* e = getenv("OPTR_TMA_STAGES");
+    s = (e && e[0] == '3') ? 3 : 2;
+  }
+  return s;
+}
+
+template <int T, bool STRIDED, int SK, class Snk>
+int launch_tma_pass(int cls, const TmaMaps& maps, const CUtensorMap& dmap, const TmaArgs& a, const Snk& snk,
+                    int worker, cudaStream_t st) {
+  if (tma_stages() == 3) return launch_tma_pass_s<T, 3, STRIDED, SK>(cls, maps, dmap, a, snk, worker, st);
+  return launch_tma_pass_s<T, 2, STRIDED, SK>(cls, maps, dmap, a, snk, worker, st);
 }
 
 // A pass through the TMA ring kernel when the shapes allow it; -1 when the

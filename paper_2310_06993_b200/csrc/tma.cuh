@@ -23,7 +23,6 @@
 
 namespace optr {
 
-constexpr int kStages = 3;
 
 struct TmaMaps {
   CUtensorMap m[kMaxW];
@@ -100,9 +99,9 @@ template <int T>
 __host__ __device__ constexpr size_t tma_stage_bytes() {
   return (sizeof(float) << T) + (sizeof(uint32_t) << (T - 5));  // tile + its sign words
 }
-template <int T>
+template <int T, int S>
 __host__ __device__ constexpr size_t tma_smem_bytes() {
-  return kStages * tma_stage_bytes<T>() + 64 + 1024;
+  return S * tma_stage_bytes<T>() + 64 + 1024;
 }
 
 // Issue the loads of tile t into stage buffer `st` (sign words after the tile).
@@ -184,7 +183,7 @@ __device__ __forceinline__ float4 gather_mask4(const TmaArgs& a, int64_t g, floa
   return make_float4(k0 ? v.x : 0.f, k1 ? v.y : 0.f, k2 ? v.z : 0.f, k3 ? v.w : 0.f);
 }
 
-template <int T, bool STRIDED, int SK, class Snk>
+template <int T, int kStages, bool STRIDED, int SK, class Snk>
 __global__ void __launch_bounds__(1 << (T - 5)) tma_pass_kernel(const __grid_constant__ TmaMaps maps,
                                                               const __grid_constant__ CUtensorMap dst,
                                                               const __grid_constant__ TmaArgs a,
