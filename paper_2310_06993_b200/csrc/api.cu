@@ -220,13 +220,16 @@ bool tma_enabled() {
   return g_tma_mode == 1;
 }
 
-// fp32 tensor [d2][d1][d0] (d0 contiguous), boxes of 8 x box1 x 1
-bool make_map3(CUtensorMap* m, const void* base, uint64_t d0, uint64_t d1, uint64_t d2, uint32_t box1) {
+// tensor [d2][d1][d0] (d0 contiguous) of fp32 / bf16, boxes of 8 x box1 x 1
+bool make_map3(CUtensorMap* m, const void* base, uint64_t d0, uint64_t d1, uint64_t d2, uint32_t box1,
+               int dtype = OPTR_F32) {
+  const uint64_t esz = dtype == OPTR_BF16 ? 2 : 4;
   cuuint64_t dims[3] = {d0, d1, d2};
-  cuuint64_t strides[2] = {d0 * 4, d0 * d1 * 4};
+  cuuint64_t strides[2] = {d0 * esz, d0 * d1 * esz};
   cuuint32_t box[3] = {8, box1, 1};
   cuuint32_t es[3] = {1, 1, 1};
-  CUresult r = g_encode_tiled(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(base), dims, strides, box,
+  CUresult r = g_encode_tiled(m, dtype == OPTR_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                              3, const_cast<void*>(base), dims, strides, box,
                               es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                               CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) fprintf(stderr, "optr: cuTensorMapEncodeTiled failed (%d)\n", (int)r);
@@ -307,7 +310,7 @@ int try_tma(int cls, const PassGeom& pg, int nlog, int worker, int nworkers, con
       a.got = src.got ? src.got + (int64_t)worker * src.dim : nullptr;
     }
     if (pg.cb == 3) {  // strided: tensor boxes in, tensor boxes out
-      if constexpr (kEnc || !kSnkBuf) {
+      if constexpr (kEnc) {
         return -1;
       } else {
         if (T < 12 || T > 14) return -1;
@@ -322,9 +325,18 @@ int try_tma(int cls, const PassGeom& pg, int nlog, int worker, int nworkers, con
         } else {
           if (!make_map3(&maps.m[0], src.y[worker], d0, d1, d2, (uint32_t)box)) return -1;
         }
-        if (!make_map3(&dmap, snk.y[worker], d0, d1, d2, (uint32_t)box)) return -1;
+        if constexpr (kSnkBuf) {
+          if (!make_map3(&dmap, snk.y[worker], d0, d1, d2, (uint32_t)box)) return -1;
+          a.scale = snk.scale;
+        } else {  // decode epilogue: map over the full rows of `out`
+          if (d2 != 1) return -1;
+          const int64_t rows_full = snk.L >> pg.lo;
+          if (rows_full > 0 &&
+              !make_map3(&dmap, snk.out[worker], d0, (uint64_t)rows_full, 1, (uint32_t)box, snk.dtype))
+            return -1;
+          if (((uintptr_t)snk.out[worker] & 15) || ((uintptr_t)snk.signs & 15)) return -1;
+        }
         a.box_rows = box;
-        a.scale = snk.scale;
         switch (T) {
           case 12: return launch_tma_pass<12, true, SK>(cls, maps, dmap, a, snk, worker, st);
           case 13: return launch_tma_pass<13, true, SK>(cls, maps, dmap, a, snk, worker, st);
@@ -347,6 +359,42 @@ int try_tma(int cls, const PassGeom& pg, int nlog, int worker, int nworkers, con
     if (T == 13) return launch_tma_pass<13, false, SK>(cls, maps, dmap, a, snk, worker, st);
     return launch_tma_pass<14, false, SK>(cls, maps, dmap, a, snk, worker, st);
   }
+}
+
+constexpr int kAggChunk = 1024;
+
+int launch_tma_aggregate(const AggArgs& ag, int nowners, int64_t smax, cudaStream_t st) {
+  TmaAggArgs a;
+  memset(&a, 0, sizeof(a));
+  for (int i = 0; i < ag.n; ++i) {
+    a.Y[i] = ag.Y[i];
+    a.A[i] = ag.A[i];
+  }
+  a.sh = ag.sh;
+  a.n = ag.n;
+  a.r = ag.r;
+  a.owner_base = ag.owner_base;
+  a.m = ag.m;
+  const size_t smem = tma_agg_smem_bytes<kAggChunk>(ag.n);
+  int rc = set_smem_attr(tma_agg_kernel<kAggChunk>, smem);
+  if (rc) return rc;
+  static int nsm = 0;
+  if (!nsm) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    if (nsm <= 0) nsm = 148;
+  }
+  int per_sm = (int)((227 * 1024) / (smem + 1024));
+  if (per_sm < 1) per_sm = 1;
+  if (per_sm > 8) per_sm = 8;
+  const int64_t nchunks = (smax + kAggChunk - 1) / kAggChunk;
+  int64_t gx = (int64_t)nsm * per_sm / nowners;
+  if (gx < 1) gx = 1;
+  if (gx > nchunks) gx = nchunks;
+  KScope ks(OPTR_K_AGG, st);
+  tma_agg_kernel<kAggChunk><<<dim3((unsigned)gx, (unsigned)nowners), kAggChunk / 4, smem, st>>>(a);
+  return launch_check(tma_agg_kernel<kAggChunk>, "tma_aggregate", 0, 0, (int)gx, nowners, kAggChunk / 4, smem);
 }
 
 template <class S>
@@ -414,8 +462,11 @@ bool agg_vec_ok(const AggArgs& a) {
   return true;
 }
 
+int launch_tma_aggregate(const AggArgs& ag, int nowners, int64_t smax, cudaStream_t st);
+
 int launch_aggregate(const AggArgs& ag, int nowners, int64_t smax, cudaStream_t st) {
   if (smax <= 0) return OPTR_OK;
+  if (agg_vec_ok(ag) && tma_enabled()) return launch_tma_aggregate(ag, nowners, smax, st);
   int64_t blocks = (smax / 4 + 255) / 256;
   if (blocks < 1) blocks = 1;
   if (blocks > kMaxGrid) blocks = kMaxGrid;
@@ -429,6 +480,19 @@ int launch_aggregate(const AggArgs& ag, int nowners, int64_t smax, cudaStream_t 
 }
 
 Pcg sign_pcg(uint64_t seed) { return pcg_from_u64s(&seed, 1); }
+
+// Decode pass order.  Contiguous first (default): the stage-2 receive pulls
+// whole owner chunks (bulk copies; large NVLink requests) and the strided
+// pass finishes into `out` with the decode epilogue.  OPTR_DEC_ORDER=strided
+// gathers in the strided pass instead.
+bool decode_contig_first() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("OPTR_DEC_ORDER");
+    v = (e && e[0] == 's') ? 0 : 1;
+  }
+  return v == 1;
+}
 
 // Workers per transform launch: batch them while their vectors fit in about
 // half of L2 together, otherwise one worker at a time so each worker's
@@ -900,7 +964,7 @@ int optr_tar_local(const void* const* x, void* const* out, int n, int64_t L, int
     snk.count_stride = 1;
     snk.dim = (double)dim;
     rc = for_workers(dim, n, st, [&](int w0, int nw, cudaStream_t s2) {
-      return run_transform(log2_exact(dim), false, w0, nw, ga, buf, snk, s2, OPTR_K_DEC_FIRST);
+      return run_transform(log2_exact(dim), decode_contig_first(), w0, nw, ga, buf, snk, s2, OPTR_K_DEC_FIRST);
     });
     if (rc) return rc;
   } else {
@@ -1151,7 +1215,7 @@ int optr_tar(optr_comm c, const void* x, void* out, int64_t L, int dtype_in, int
     snk.count_extra = counts + n;
     snk.count_stride = 1;
     snk.dim = (double)dim;
-    if ((rc = run_transform(log2_exact(dim), false, me, 1, ga, buf, snk, st, OPTR_K_DEC_FIRST))) return rc;
+    if ((rc = run_transform(log2_exact(dim), decode_contig_first(), me, 1, ga, buf, snk, st, OPTR_K_DEC_FIRST))) return rc;
   } else {
     AsmArgs as;
     memset(&as, 0, sizeof(as));

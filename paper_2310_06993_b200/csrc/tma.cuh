@@ -19,6 +19,8 @@
 #pragma once
 #include <cuda.h>
 
+#include <type_traits>
+
 #include "kernels.cuh"
 
 namespace optr {
@@ -192,6 +194,8 @@ __global__ void __launch_bounds__(1 << (T - 5)) tma_pass_kernel(const __grid_con
   constexpr RPlan P = make_rplan(T, CB);
   static_assert(P.nr == 3, "TMA pass expects three register rounds");
   static_assert(P.pos[0][0] == 0 && P.pos[0][1] == 1, "round A holds float4 groups");
+  static_assert(!STRIDED || !std::is_same<Snk, SnkDecode>::value || (P.pos[2][0] == 0 && P.pos[2][1] == 1),
+                "decode epilogue stores float4 groups");
   static_assert(sizeof(float) * pad(1 << T) <= tma_stage_bytes<T>(), "padded tile fits the stage");
   constexpr size_t SB = tma_stage_bytes<T>();
   extern __shared__ __align__(16) unsigned char smraw[];
@@ -302,6 +306,54 @@ __global__ void __launch_bounds__(1 << (T - 5)) tma_pass_kernel(const __grid_con
 #pragma unroll
         for (int j = 0; j < 32; ++j) d.store1(g0 + b2 + roff(P, 2, j), v[j]);
       }
+    } else if constexpr (std::is_same<Snk, SnkDecode>::value) {
+      // decode epilogue (hadamard.py:119-123, runner.py:253-256): scale,
+      // signs, cast, then TMA store into `out` for the rows inside [0, L)
+      // (the map stops at the last full row; the partial row goes by STG)
+      const int64_t rows_full = d.L >> a.lo;
+#pragma unroll
+      for (int m = 0; m < 8; ++m) {
+        const int i = b2 + roff(P, 2, 4 * m);
+        const int64_t g = g0 + ((int64_t)(i >> 3) << a.lo) + (i & 7);
+        const uint32_t w = __ldg(d.signs + (g >> 5)) >> (g & 31);
+        float4 o4 = make_float4(v[4 * m] * d.scale, v[4 * m + 1] * d.scale, v[4 * m + 2] * d.scale,
+                                v[4 * m + 3] * d.scale);
+        o4 = make_float4(__int_as_float(__float_as_int(o4.x) ^ ((~w & 1u) << 31)),
+                         __int_as_float(__float_as_int(o4.y) ^ ((~w & 2u) << 30)),
+                         __int_as_float(__float_as_int(o4.z) ^ ((~w & 4u) << 29)),
+                         __int_as_float(__float_as_int(o4.w) ^ ((~w & 8u) << 28)));
+        if ((i >> 3) >= rows_full) {  // partial last row / padding rows
+          const float r4[4] = {o4.x, o4.y, o4.z, o4.w};
+          for (int c = 0; c < 4; ++c)
+            if (g + c < d.L) store_elem(d.out, d.dtype, g + c, r4[c]);
+        }
+        if (d.dtype == OPTR_BF16) {
+          const __nv_bfloat162 lo2 = __floats2bfloat162_rn(o4.x, o4.y), hi2 = __floats2bfloat162_rn(o4.z, o4.w);
+          uint2 u;
+          u.x = *reinterpret_cast<const uint32_t*>(&lo2);
+          u.y = *reinterpret_cast<const uint32_t*>(&hi2);
+          *reinterpret_cast<uint2*>(sb + (size_t)i * 2) = u;
+        } else {
+          *reinterpret_cast<float4*>(tile + i) = o4;
+        }
+      }
+      fence_async_smem();
+      __syncthreads();
+      if (tid == 0) {
+        const int c0 = (int)((t & ((1LL << cgb) - 1)) << 3);
+        const int nbox = (1 << (T - 3)) / a.box_rows;
+        const int esz = d.dtype == OPTR_BF16 ? 2 : 4;
+        for (int b = 0; b < nbox; ++b)
+          if ((int64_t)b * a.box_rows < rows_full)
+            tma_store_3d(&dst, sb + (size_t)b * a.box_rows * 8 * esz, c0, b * a.box_rows, 0);
+        bulk_commit();
+        if (k >= 1) {
+          bulk_wait_read1();
+          const int64_t tn = t + (kStages - 1) * stride;
+          const int sp = (k - 1) % kStages;
+          if (tn < a.ntiles) tile_issue<T, STRIDED, SK>(maps, a, tn, base + sp * SB, &full[sp]);
+        }
+      }
     } else {
       // dense result -> TMA tensor store; the previous stage is refilled once
       // its own store has finished reading shared memory
@@ -339,6 +391,100 @@ __global__ void __launch_bounds__(1 << (T - 5)) tma_pass_kernel(const __grid_con
   }
   if constexpr (STRIDED) {
     if (tid == 0) bulk_wait0();
+  }
+}
+
+}  // namespace optr
+
+namespace optr {
+
+// ------------------------------------------------ TMA stage-1 aggregate
+// TAR stage 1 at owner o (collectives.py:113-125, _mean_received :77-94):
+// the owner's shard of every worker's wire vector streams into shared
+// memory in CH-entry chunks by 1D bulk copies (peer-mapped buffers in the
+// multi-GPU path, so the NVLink requests are whole chunks), two chunks in
+// flight per CTA; each thread then takes the fp64 mean of 4 entries in
+// ascending node order under the stage-1 masks.
+struct TmaAggArgs {
+  const float* Y[kMaxW];  // wire vector of each worker
+  float* A[kMaxW];        // aggregate shard of each owner
+  Shards sh;
+  int n, r, owner_base;
+  MaskView m;
+};
+
+template <int CH>
+__host__ __device__ constexpr size_t tma_agg_smem_bytes(int n) {
+  return (size_t)2 * n * CH * sizeof(float) + 64 + 1024;
+}
+
+template <int CH>
+__global__ void __launch_bounds__(CH / 4) tma_agg_kernel(const __grid_constant__ TmaAggArgs a) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  unsigned char* const base = smraw + ((1024u - (smem_u32(smraw) & 1023u)) & 1023u);
+  float* const buf = reinterpret_cast<float*>(base);  // [2][n][CH]
+  uint64_t* const full = reinterpret_cast<uint64_t*>(base + (size_t)2 * a.n * CH * sizeof(float));
+  const int tid = threadIdx.x;
+  const int n = a.n;
+  const int o = a.owner_base + blockIdx.y;
+  const int j = owned_shard(o, a.r, n);
+  const int64_t off = a.sh.off(j), len = a.sh.len(j);
+  const int64_t nchunks = (len + CH - 1) / CH;
+  float* const A = a.A[o];
+  if (tid == 0) {
+    mbar_init(&full[0], 1);
+    mbar_init(&full[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  auto issue = [&](int64_t c, int s) {
+    const int64_t e0 = c * CH;
+    int64_t cnt = len - e0;
+    if (cnt > CH) cnt = CH;
+    const uint32_t bytes = (uint32_t)(cnt * sizeof(float));
+    mbar_expect_tx(&full[s], bytes * (uint32_t)n);
+    for (int i = 0; i < n; ++i) bulk_load(buf + ((size_t)s * n + i) * CH, a.Y[i] + off + e0, bytes, &full[s]);
+  };
+  const int64_t stride = gridDim.x;
+  int64_t c = blockIdx.x;
+  if (tid == 0) {
+    if (c < nchunks) issue(c, 0);
+    if (c + stride < nchunks) issue(c + stride, 1);
+  }
+  const uint32_t epp = (uint32_t)a.m.epp;
+  for (int k = 0; c < nchunks; ++k, c += stride) {
+    const int s = k & 1;
+    mbar_wait(&full[s], (uint32_t)((k >> 1) & 1));
+    const int64_t e = c * CH + tid * 4;
+    float4 res = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (e < len) {
+      const Pkt4 pk = pkt4((uint32_t)e, epp);
+      double acc[4] = {0.0, 0.0, 0.0, 0.0}, cnt[4] = {0.0, 0.0, 0.0, 0.0};
+      for (int i = 0; i < n; ++i) {
+        const float4 v = *reinterpret_cast<const float4*>(buf + ((size_t)s * n + i) * CH + tid * 4);
+        bool k0 = true, k1 = true, k2 = true, k3 = true;
+        if (i != o) {
+          const uint32_t* row = a.m.row(0, o, i);
+          k0 = row_bit(row, pk.p[0]);
+          k1 = row_bit(row, pk.p[1]);
+          k2 = row_bit(row, pk.p[2]);
+          k3 = row_bit(row, pk.p[3]);
+        }
+        acc[0] += k0 ? (double)v.x : 0.0;
+        acc[1] += k1 ? (double)v.y : 0.0;
+        acc[2] += k2 ? (double)v.z : 0.0;
+        acc[3] += k3 ? (double)v.w : 0.0;
+        cnt[0] += k0 ? 1.0 : 0.0;
+        cnt[1] += k1 ? 1.0 : 0.0;
+        cnt[2] += k2 ? 1.0 : 0.0;
+        cnt[3] += k3 ? 1.0 : 0.0;
+      }
+      res = make_float4(mean_of(acc[0], cnt[0]), mean_of(acc[1], cnt[1]), mean_of(acc[2], cnt[2]),
+                        mean_of(acc[3], cnt[3]));
+    }
+    __syncthreads();  // stage s has been read
+    if (tid == 0 && c + 2 * stride < nchunks) issue(c + 2 * stride, s);
+    if (e + 4 <= len) st4(A + e, res);
   }
 }
 
