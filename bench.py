@@ -320,34 +320,39 @@ def run_ours(args):
     e2e = {"value": round(n_workers * grad_bytes / (e2e_ms * 1e-3) / 1e9, 3), "unit": "GB/s",
            "ms_per_step": round(e2e_ms, 3), "h2d_bytes_per_step": io_bytes, "d2h_bytes_per_step": io_bytes}
 
-    # ---- roofline of the dominant kernel class
+    # ---- roofline of the dominant kernel class (live CUDA-event durations)
     peaks = load_peaks()
-    dom = max((k for k in per_kernel if per_kernel[k][1] > 0), key=lambda k: per_kernel[k][0])
-    dom_ms, dom_n = per_kernel[dom]
-    # per launch: every launch covers one bucket x (local: all workers, multi: one)
-    alg = 0
-    for L in buckets:
-        dim = next_pow2(L) if ht else L
-        alg += kernel_bytes(dom, dim, L, n_workers, s_in, s_out) * per_rank_workers
-    alg_per_launch = alg / len(buckets)
-    avg_launch_s = dom_ms / dom_n * 1e-3
-    achieved = alg_per_launch / avg_launch_s / 1e9
-    if multi and dom in ("aggregate", "dec_first"):
-        # NVLink-bound: bytes pulled from peers per launch
-        nv = 0
+    live = {k: v for k, v in per_kernel.items() if v[1] > 0}
+    dom = max(live, key=lambda k: live[k][0])
+    dom_ms, dom_n, dom_units = live[dom]
+
+    def class_bytes(cls, nvlink=False):
+        """Algorithmic bytes the timed launches of `cls` moved: per-worker
+        bytes of each bucket x worker-passes (units spread evenly over buckets)."""
+        units = live[cls][2]
+        per_b = 0
         for L in buckets:
             dim = next_pow2(L) if ht else L
-            nv += 4 * dim * (n_workers - 1) // n_workers
-        nv_ach = nv / len(buckets) / avg_launch_s / 1e9
+            if nvlink:
+                per_b += 4 * dim * (n_workers - 1) // n_workers
+            else:
+                per_b += kernel_bytes(cls, dim, L, n_workers, s_in, s_out)
+        return units * per_b / len(buckets)
+
+    achieved = class_bytes(dom) / (dom_ms * 1e-3) / 1e9
+    if multi and dom in ("aggregate", "dec_first"):
+        nv_ach = class_bytes(dom, nvlink=True) / (dom_ms * 1e-3) / 1e9
         roof = {"bound": "nvlink", "achieved": round(nv_ach, 1), "peak": NVLINK_GBS, "unit": "GB/s",
-                "frac": round(nv_ach / NVLINK_GBS, 4), "kernel": dom,
+                "frac": round(nv_ach / NVLINK_GBS, 4), "kernel": dom, "peak_src": "measured peer copy",
                 "hbm_achieved": round(achieved, 1), "traffic": None}
     else:
         roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
                 "frac": round(achieved / peaks["hbm_gbs"], 4), "kernel": dom, "peak_src": peaks["src"],
                 "traffic": None}
-    kernels = {k: {"ms_per_step": round(v[0] / args.steps, 4), "launches_per_step": v[1] / args.steps}
-               for k, v in per_kernel.items() if v[1] > 0}
+    kernels = {k: {"ms_per_step": round(v[0] / args.steps, 4), "launches_per_step": v[1] / args.steps,
+                   "avg_launch_us": round(v[0] / v[1] * 1e3, 2),
+                   "hbm_gbs": round(class_bytes(k) / (v[0] * 1e-3) / 1e9, 1)}
+               for k, v in live.items()}
 
     # whole-step roofline (SURVEY §8(d)): max(HBM_alg/HBM, NVL/NVLink)
     hbm_alg, nvl = step_alg_bytes(buckets, n_workers, s_in, s_out, ht)

@@ -166,8 +166,10 @@ int optr_comm_barrier(optr_comm c, void* stream);
 /* Enable (1) / disable (0) CUDA-event timing of every kernel launch. */
 int optr_timing_enable(int on);
 /* Synchronise recorded events and return, per class, the summed device
- * milliseconds and the launch count since the last reset; then reset. */
-int optr_timing_collect(double* ms_out, int64_t* launches_out);
+ * milliseconds, the launch count and the worker-passes those launches
+ * covered (a launch over k co-resident workers counts k) since the last
+ * reset; then reset.  Any pointer may be NULL. */
+int optr_timing_collect(double* ms_out, int64_t* launches_out, int64_t* units_out);
 /* Kernels this library launched since load (all classes, any device). */
 int64_t optr_launch_count(void);
 

@@ -72,7 +72,7 @@ SIGNATURES = {
                         ctypes.POINTER(optr_mask_spec), _vp, _vp]),
     "optr_comm_barrier": (_int, [_vp, _vp]),
     "optr_timing_enable": (_int, [_int]),
-    "optr_timing_collect": (_int, [ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_i64)]),
+    "optr_timing_collect": (_int, [ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_i64), ctypes.POINTER(_i64)]),
     "optr_launch_count": (_i64, []),
 }
 
@@ -121,11 +121,12 @@ def timing_enable(on: bool) -> None:
 
 
 def timing_collect() -> dict:
-    """{class name: (total_ms, launches)} since the last collect."""
+    """{class name: (total_ms, launches, worker_passes)} since the last collect."""
     ms = (ctypes.c_double * len(K_NAMES))()
     cnt = (ctypes.c_int64 * len(K_NAMES))()
-    check(lib().optr_timing_collect(ms, cnt), "timing_collect")
-    return {k: (ms[i], cnt[i]) for i, k in enumerate(K_NAMES)}
+    units = (ctypes.c_int64 * len(K_NAMES))()
+    check(lib().optr_timing_collect(ms, cnt, units), "timing_collect")
+    return {k: (ms[i], cnt[i], units[i]) for i, k in enumerate(K_NAMES)}
 
 
 def launch_count() -> int:

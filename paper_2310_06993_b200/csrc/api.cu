@@ -52,6 +52,7 @@ std::mutex g_tmu;
 bool g_timing = false;
 struct TRec {
   int cls;
+  int units;
   cudaEvent_t a, b;
 };
 std::vector<TRec> g_trecs;
@@ -61,9 +62,10 @@ std::vector<TRec> g_trecs;
 struct KScope {
   cudaStream_t st;
   int cls;
+  int units;
   cudaEvent_t a = nullptr, b = nullptr;
-  KScope(int c, cudaStream_t s, int nlaunch = 1) : st(s), cls(c) {
-    g_launches += nlaunch;
+  KScope(int c, cudaStream_t s, int u = 1) : st(s), cls(c), units(u) {
+    g_launches += 1;
     if (g_timing) {
       cudaEventCreate(&a);
       cudaEventCreate(&b);
@@ -74,7 +76,7 @@ struct KScope {
     if (a) {
       cudaEventRecord(b, st);
       std::lock_guard<std::mutex> lk(g_tmu);
-      g_trecs.push_back(TRec{cls, a, b});
+      g_trecs.push_back(TRec{cls, units, a, b});
     }
   }
 };
@@ -176,7 +178,7 @@ int launch_rtile(int cls, const PassGeom& pg, int worker_base, int nworkers, con
   int rc = set_smem_attr(rtile_kernel<T, CB, LO, Src, Snk>, smem);
   if (rc) return rc;
   const int64_t gx = pg.ntiles < kMaxGrid ? pg.ntiles : kMaxGrid;
-  KScope ks(cls, st);
+  KScope ks(cls, st, nworkers);
   rtile_kernel<T, CB, LO, Src, Snk><<<dim3((unsigned)gx, (unsigned)nworkers), 1 << (T - 5), smem, st>>>(
       pg, worker_base, src, snk);
   return launch_check(rtile_kernel<T, CB, LO, Src, Snk>, "rtile", T, CB, (int)gx, nworkers, 1 << (T - 5), smem);
@@ -193,7 +195,7 @@ int launch_smem(int cls, const PassGeom& pg, int worker_base, int nworkers, cons
   int threads = nelem / 32;
   if (threads < 32) threads = 32;
   if (threads > 256) threads = 256;
-  KScope ks(cls, st);
+  KScope ks(cls, st, nworkers);
   smem_tile_kernel<Src, Snk><<<dim3((unsigned)gx, (unsigned)nworkers), threads, smem, st>>>(pg, worker_base, src,
                                                                                             snk);
   return launch_check(smem_tile_kernel<Src, Snk>, "smem_tile", pg.cb + pg.ks, pg.cb, (int)gx, nworkers, threads,
@@ -392,7 +394,7 @@ int launch_tma_aggregate(const AggArgs& ag, int nowners, int64_t smax, cudaStrea
   int64_t gx = (int64_t)nsm * per_sm / nowners;
   if (gx < 1) gx = 1;
   if (gx > nchunks) gx = nchunks;
-  KScope ks(OPTR_K_AGG, st);
+  KScope ks(OPTR_K_AGG, st, nowners);
   tma_agg_kernel<kAggChunk><<<dim3((unsigned)gx, (unsigned)nowners), kAggChunk / 4, smem, st>>>(a);
   return launch_check(tma_agg_kernel<kAggChunk>, "tma_aggregate", 0, 0, (int)gx, nowners, kAggChunk / 4, smem);
 }
@@ -470,7 +472,7 @@ int launch_aggregate(const AggArgs& ag, int nowners, int64_t smax, cudaStream_t 
   int64_t blocks = (smax / 4 + 255) / 256;
   if (blocks < 1) blocks = 1;
   if (blocks > kMaxGrid) blocks = kMaxGrid;
-  KScope ks(OPTR_K_AGG, st);
+  KScope ks(OPTR_K_AGG, st, nowners);
   if (agg_vec_ok(ag))
     aggregate_kernel<true><<<dim3((unsigned)blocks, nowners), 256, 0, st>>>(ag);
   else
@@ -481,17 +483,18 @@ int launch_aggregate(const AggArgs& ag, int nowners, int64_t smax, cudaStream_t 
 
 Pcg sign_pcg(uint64_t seed) { return pcg_from_u64s(&seed, 1); }
 
-// Decode pass order.  Contiguous first (default): the stage-2 receive pulls
-// whole owner chunks (bulk copies; large NVLink requests) and the strided
-// pass finishes into `out` with the decode epilogue.  OPTR_DEC_ORDER=strided
-// gathers in the strided pass instead.
-bool decode_contig_first() {
-  static int v = -1;
-  if (v < 0) {
+// Decode pass order.  Multi-GPU: contiguous first, so the stage-2 receive
+// pulls whole owner chunks over NVLink (bulk copies) and the strided pass
+// finishes into `out` with the decode epilogue.  One GPU: strided first,
+// gathering from the L2-resident aggregates, contiguous last into `out`.
+// OPTR_DEC_ORDER=strided|contig overrides.
+bool decode_contig_first(bool multi_gpu) {
+  static int v = -2;
+  if (v == -2) {
     const char* e = getenv("OPTR_DEC_ORDER");
-    v = (e && e[0] == 's') ? 0 : 1;
+    v = !e ? -1 : (e[0] == 's' ? 0 : 1);
   }
-  return v == 1;
+  return v < 0 ? multi_gpu : v == 1;
 }
 
 // Workers per transform launch: batch them while their vectors fit in about
@@ -964,7 +967,7 @@ int optr_tar_local(const void* const* x, void* const* out, int n, int64_t L, int
     snk.count_stride = 1;
     snk.dim = (double)dim;
     rc = for_workers(dim, n, st, [&](int w0, int nw, cudaStream_t s2) {
-      return run_transform(log2_exact(dim), decode_contig_first(), w0, nw, ga, buf, snk, s2, OPTR_K_DEC_FIRST);
+      return run_transform(log2_exact(dim), decode_contig_first(false), w0, nw, ga, buf, snk, s2, OPTR_K_DEC_FIRST);
     });
     if (rc) return rc;
   } else {
@@ -976,7 +979,7 @@ int optr_tar_local(const void* const* x, void* const* out, int n, int64_t L, int
     as.L = L;
     int64_t blocks = (L + 255) / 256;
     if (blocks > 4736) blocks = 4736;
-    KScope ks(OPTR_K_ASSEMBLE, st);
+    KScope ks(OPTR_K_ASSEMBLE, st, n);
     assemble_kernel<<<dim3((unsigned)blocks, n), 256, 0, st>>>(as);
     CK(cudaGetLastError());
   }
@@ -992,9 +995,16 @@ struct optr_comm_s {
   char* sym;
   char* peer[OPTR_MAX_WORKERS];
   bool opened[OPTR_MAX_WORKERS];
-  char* local;  // signs | bitmap | counts
-  size_t off_signs, off_bitmap, off_counts, local_bytes;
+  char* local;  // two parities of signs | bitmap | counts
+  size_t off_signs, off_bitmap, off_counts, local_bytes;  // within one parity
   unsigned long long epoch;
+  // prep (signs + masks + counts) runs on its own stream into the buffers of
+  // call parity p as soon as call c-2 (the last user of p) is done, so it
+  // overlaps the previous call's kernels
+  cudaStream_t pstream;
+  cudaEvent_t prep_ready[2], done[2];
+  bool done_recorded[2];
+  uint64_t calls;
 };
 
 size_t optr_comm_handle_bytes(void) { return sizeof(cudaIpcMemHandle_t); }
@@ -1031,12 +1041,17 @@ int optr_comm_create(optr_comm* out, int device, int rank, int n, int64_t max_le
   off = align_up(off + (size_t)2 * n * 8, 256);
   c->local_bytes = off;
   if (cudaMalloc((void**)&c->sym, c->sym_bytes) != cudaSuccess ||
-      cudaMalloc((void**)&c->local, c->local_bytes) != cudaSuccess) {
+      cudaMalloc((void**)&c->local, 2 * c->local_bytes) != cudaSuccess) {
     cudaFree(c->sym);
     free(c);
     return OPTR_ENOMEM;
   }
   CK(cudaMemset(c->sym, 0, c->sym_bytes));
+  CK(cudaStreamCreateWithFlags(&c->pstream, cudaStreamNonBlocking));
+  for (int p = 0; p < 2; ++p) {
+    CK(cudaEventCreateWithFlags(&c->prep_ready[p], cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&c->done[p], cudaEventDisableTiming));
+  }
   CK(cudaDeviceSynchronize());
   c->peer[rank] = c->sym;
   *out = c;
@@ -1075,6 +1090,11 @@ int optr_comm_destroy(optr_comm c) {
     if (c->opened[i]) cudaIpcCloseMemHandle(c->peer[i]);
   cudaFree(c->sym);
   cudaFree(c->local);
+  cudaStreamDestroy(c->pstream);
+  for (int p = 0; p < 2; ++p) {
+    cudaEventDestroy(c->prep_ready[p]);
+    cudaEventDestroy(c->done[p]);
+  }
   free(c);
   return OPTR_OK;
 }
@@ -1131,9 +1151,11 @@ int optr_tar(optr_comm c, const void* x, void* out, int64_t L, int dtype_in, int
   cudaStream_t st = (cudaStream_t)stream;
   const int me = c->rank;
   const int r = ((rotation % n) + n) % n;
-  uint32_t* signs = (uint32_t*)(c->local + c->off_signs);
-  uint32_t* bitmap = (uint32_t*)(c->local + c->off_bitmap);
-  unsigned long long* counts = (unsigned long long*)(c->local + c->off_counts);
+  const int par = (int)(c->calls++ & 1);
+  char* const loc = c->local + (size_t)par * c->local_bytes;
+  uint32_t* signs = (uint32_t*)(loc + c->off_signs);
+  uint32_t* bitmap = (uint32_t*)(loc + c->off_bitmap);
+  unsigned long long* counts = (unsigned long long*)(loc + c->off_counts);
   float* Yp[kMaxW];
   float* Ap[kMaxW];
   for (int i = 0; i < n; ++i) {
@@ -1142,13 +1164,17 @@ int optr_tar(optr_comm c, const void* x, void* out, int64_t L, int dtype_in, int
   }
   Shards sh = make_shards(dim, n);
 
-  CK(cudaMemsetAsync(counts, 0, (size_t)2 * n * 8, st));
+  const cudaStream_t ps = c->pstream;
+  if (c->done_recorded[par]) CK(cudaStreamWaitEvent(ps, c->done[par], 0));
+  CK(cudaMemsetAsync(counts, 0, (size_t)2 * n * 8, ps));
   PrepArgs pa;
   memset(&pa, 0, sizeof(pa));
   if (ht) fill_sign_args(pa, signs, dim, derive_seed(job_seed, bucket_id, generation));
   const uint32_t* cbits = nullptr;
   if ((rc = setup_masks(pa, masks, dim, n, r, epp, bitmap, counts, me, me + 1, &cbits))) return rc;
-  if ((rc = launch_prep(pa, st))) return rc;
+  if ((rc = launch_prep(pa, ps))) return rc;
+  CK(cudaEventRecord(c->prep_ready[par], ps));
+  CK(cudaStreamWaitEvent(st, c->prep_ready[par], 0));
   MaskView mv{cbits, pa.pw, n, epp};
 
   // encode into my symmetric wire buffer
@@ -1215,7 +1241,7 @@ int optr_tar(optr_comm c, const void* x, void* out, int64_t L, int dtype_in, int
     snk.count_extra = counts + n;
     snk.count_stride = 1;
     snk.dim = (double)dim;
-    if ((rc = run_transform(log2_exact(dim), decode_contig_first(), me, 1, ga, buf, snk, st, OPTR_K_DEC_FIRST))) return rc;
+    if ((rc = run_transform(log2_exact(dim), decode_contig_first(true), me, 1, ga, buf, snk, st, OPTR_K_DEC_FIRST))) return rc;
   } else {
     AsmArgs as;
     memset(&as, 0, sizeof(as));
@@ -1234,6 +1260,8 @@ int optr_tar(optr_comm c, const void* x, void* out, int64_t L, int dtype_in, int
     CK(cudaMemcpyAsync(received_out, counts + me, 8, cudaMemcpyDeviceToDevice, st));
     CK(cudaMemcpyAsync(received_out + 1, counts + n + me, 8, cudaMemcpyDeviceToDevice, st));
   }
+  CK(cudaEventRecord(c->done[par], st));
+  c->done_recorded[par] = true;
   return OPTR_OK;
 }
 
@@ -1244,7 +1272,7 @@ int optr_timing_enable(int on) {
   return OPTR_OK;
 }
 
-int optr_timing_collect(double* ms_out, int64_t* launches_out) {
+int optr_timing_collect(double* ms_out, int64_t* launches_out, int64_t* units_out) {
   std::vector<TRec> recs;
   {
     std::lock_guard<std::mutex> lk(g_tmu);
@@ -1254,6 +1282,8 @@ int optr_timing_collect(double* ms_out, int64_t* launches_out) {
     for (int i = 0; i < OPTR_K_CLASSES; ++i) ms_out[i] = 0.0;
   if (launches_out)
     for (int i = 0; i < OPTR_K_CLASSES; ++i) launches_out[i] = 0;
+  if (units_out)
+    for (int i = 0; i < OPTR_K_CLASSES; ++i) units_out[i] = 0;
   int rc = OPTR_OK;
   for (auto& r : recs) {
     float ms = 0.f;
@@ -1262,6 +1292,7 @@ int optr_timing_collect(double* ms_out, int64_t* launches_out) {
     if (r.cls >= 0 && r.cls < OPTR_K_CLASSES) {
       if (ms_out) ms_out[r.cls] += ms;
       if (launches_out) launches_out[r.cls] += 1;
+      if (units_out) units_out[r.cls] += r.units;
     }
     cudaEventDestroy(r.a);
     cudaEventDestroy(r.b);
