@@ -173,6 +173,13 @@ int optr_timing_collect(double* ms_out, int64_t* launches_out, int64_t* units_ou
 /* Kernels this library launched since load (all classes, any device). */
 int64_t optr_launch_count(void);
 
+/* --------------------------------------------------------------- probes */
+/* Measurement helpers for the NVLink / HBM peaks (tools/nvlink_probe.py). */
+int optr_probe_enable_peer(int device, int peer);
+/* float4 grid-stride copy of `bytes` (multiple of 16) on `device`; either
+ * pointer may be a peer allocation (SM pull / push over NVLink). */
+int optr_probe_copy(void* dst, const void* src, int64_t bytes, int blocks, int device, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -74,6 +74,8 @@ SIGNATURES = {
     "optr_timing_enable": (_int, [_int]),
     "optr_timing_collect": (_int, [ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_i64), ctypes.POINTER(_i64)]),
     "optr_launch_count": (_i64, []),
+    "optr_probe_enable_peer": (_int, [_int, _int]),
+    "optr_probe_copy": (_int, [_vp, _vp, _i64, _int, _int, _vp]),
 }
 
 _lib = None
