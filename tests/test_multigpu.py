@@ -127,3 +127,56 @@ def test_tar_rht_multi_gpu_vs_oracle():
                     assert rel < 1e-5, (ci, rank, rel)
                 else:
                     np.testing.assert_array_equal(out, want[rank])
+
+
+# ------------------------------------------------------------ DDP hook
+def _ddp_worker(rank, world, port, outdir):
+    import torch.distributed as dist
+    import torch.nn as nn
+    from torch.nn.parallel import DistributedDataParallel as DDP
+
+    from paper_2310_06993_b200.ddp_hook import OptiReduceState, max_bucket_len_for, optireduce_hook
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(rank)
+    dev = torch.device("cuda", rank)
+    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=dev)
+    grads = {}
+    for mode in ("nccl", "optireduce"):
+        torch.manual_seed(0)
+        model = nn.Sequential(nn.Linear(512, 1024), nn.ReLU(), nn.Linear(1024, 700), nn.ReLU(),
+                              nn.Linear(700, 10)).to(dev)
+        ddp = DDP(model, device_ids=[rank], bucket_cap_mb=1)
+        if mode == "optireduce":
+            state = OptiReduceState(max_bucket_len=max_bucket_len_for(model, 1), ht=True, seed=3)
+            ddp.register_comm_hook(state, optireduce_hook)
+        g = torch.Generator(device=dev).manual_seed(100 + rank)
+        x = torch.randn(64, 512, device=dev, generator=g)
+        loss = ddp(x).square().mean()
+        loss.backward()
+        torch.cuda.synchronize()
+        grads[mode] = torch.cat([p.grad.flatten() for p in model.parameters()]).cpu().numpy()
+        if mode == "optireduce":
+            assert state.generation == 1
+            state.comm.close()
+    np.save(os.path.join(outdir, f"ddp_r{rank}.npy"), np.stack([grads["nccl"], grads["optireduce"]]))
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.multigpu
+def test_ddp_comm_hook_lossless_matches_mean():
+    """Lossless TAR+RHT through the DDP hook == DDP's own mean all-reduce
+    within the float32 codec error."""
+    import torch.multiprocessing as mp
+
+    if not torch.cuda.is_available() or torch.cuda.device_count() < 2:
+        pytest.skip("needs >= 2 GPUs")
+    world = min(torch.cuda.device_count(), 8)
+    with tempfile.TemporaryDirectory() as d:
+        mp.spawn(_ddp_worker, args=(world, _free_port(), d), nprocs=world, join=True)
+        for r in range(world):
+            ref, got = np.load(os.path.join(d, f"ddp_r{r}.npy"))
+            rel = np.linalg.norm(got.astype(np.float64) - ref) / np.linalg.norm(ref)
+            assert rel < 1e-5, rel
