@@ -58,11 +58,11 @@ class OptiReduceState:
 
 
 def max_bucket_len_for(model, bucket_cap_mb: float = 25.0, dtype_bytes: int = 4) -> int:
-    """Upper bound on DDP bucket lengths: the cap, or the largest parameter
-    when one parameter alone exceeds it."""
+    """Upper bound on DDP bucket lengths: the reducer closes a bucket once it
+    reaches the cap, so a bucket holds less than cap + its last parameter."""
     cap = int(bucket_cap_mb * 1024 * 1024 // dtype_bytes)
     biggest = max((p.numel() for p in model.parameters() if p.requires_grad), default=1)
-    return max(cap, biggest) + 1024
+    return cap + biggest + 1024
 
 
 def optireduce_hook(state: OptiReduceState, bucket):
