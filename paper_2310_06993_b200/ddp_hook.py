@@ -42,12 +42,19 @@ class OptiReduceState:
     comm: object = field(default=None, repr=False)
     received: list = field(default_factory=list, repr=False)  # per-bucket [2] counts of the last pass
 
-    def communicator(self, device):
+    def communicator(self, device, needed_len: int = 0):
+        """The NVLink communicator, (re)created collectively when a bucket is
+        longer than its buffers: every rank sees the same bucket sequence, so
+        every rank grows at the same call."""
+        if self.comm is not None and needed_len > self.comm.max_len:
+            self.comm.close()
+            self.comm = None
+            self.max_bucket_len = max(needed_len, 2 * self.max_bucket_len)
         if self.comm is None:
             from .dist import TarCommunicator
 
-            self.comm = TarCommunicator(max_len=self.max_bucket_len, epp=self.max_payload // 4,
-                                        group=self.process_group, device=device)
+            self.comm = TarCommunicator(max_len=max(self.max_bucket_len, needed_len),
+                                        epp=self.max_payload // 4, group=self.process_group, device=device)
         return self.comm
 
     def masks(self, bucket_index: int) -> MaskSpec:
@@ -71,7 +78,7 @@ def optireduce_hook(state: OptiReduceState, bucket):
     buf = bucket.buffer()
     if not buf.is_contiguous():
         buf = buf.contiguous()
-    comm = state.communicator(buf.device)
+    comm = state.communicator(buf.device, buf.numel())
     out = torch.empty_like(buf)
     rec = torch.zeros(2, dtype=torch.int64, device=buf.device)
     world = comm.world
