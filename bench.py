@@ -224,10 +224,12 @@ def run_ours(args):
             r = gen % n_workers
             if multi:
                 comm.allreduce((src or grads)[b], (dst or outs)[b], rotation=r, ht=ht, job_seed=7,
-                               generation=gen, bucket_id=b, masks=masks)
+                               generation=gen, bucket_id=b, masks=masks, async_op=True)
             else:
                 tar_allreduce_local((src or grads)[b], rotation=r, ht=ht, job_seed=7, generation=gen,
                                     bucket_id=b, masks=masks, out=(dst or outs)[b])
+        if multi:
+            comm.join()
         state["gen"] += 1
 
     def barrier():

@@ -146,6 +146,18 @@ int optr_tar(optr_comm c, const void* x, void* out, int64_t L, int dtype_in,
              int rotation, int ht, const optr_mask_spec* masks, uint64_t* received_out,
              void* stream);
 
+/* Same as optr_tar, but the caller's stream does not wait for the result:
+ * the call runs on the communicator's work stream of its call parity, so
+ * consecutive buckets overlap (one bucket's NVLink stages with the next
+ * bucket's encode).  x and out must stay valid and untouched until
+ * optr_comm_join.  At most two calls are in flight per parity ordering. */
+int optr_tar_async(optr_comm c, const void* x, void* out, int64_t L, int dtype_in,
+                   int dtype_out, uint64_t job_seed, uint64_t bucket_id, uint64_t generation,
+                   int rotation, int ht, const optr_mask_spec* masks, uint64_t* received_out,
+                   void* stream);
+/* Make `stream` wait for every optr_tar_async call issued so far. */
+int optr_comm_join(optr_comm c, void* stream);
+
 /* Device-side all-rank barrier on `stream` (flags over NVLink). */
 int optr_comm_barrier(optr_comm c, void* stream);
 

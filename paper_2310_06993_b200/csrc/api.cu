@@ -991,13 +991,17 @@ int optr_tar_local(const void* const* x, void* const* out, int n, int64_t L, int
 struct optr_comm_s {
   int rank, n, epp, device;
   int64_t max_dim;
-  size_t off_flags, off_y, off_a, sym_bytes;
+  // two parities of [Y | A] so consecutive calls can overlap; three flag
+  // sets (one per parity, one for the public barrier)
+  size_t off_flags[3], off_y[2], off_a[2], sym_bytes;
   char* sym;
   char* peer[OPTR_MAX_WORKERS];
   bool opened[OPTR_MAX_WORKERS];
   char* local;  // two parities of signs | bitmap | counts
   size_t off_signs, off_bitmap, off_counts, local_bytes;  // within one parity
-  unsigned long long epoch;
+  unsigned long long epoch[3];
+  cudaStream_t ws[2];       // per-parity work streams
+  cudaEvent_t fork[2];
   // prep (signs + masks + counts) runs on its own stream into the buffers of
   // call parity p as soon as call c-2 (the last user of p) is done, so it
   // overlaps the previous call's kernels
@@ -1024,12 +1028,16 @@ int optr_comm_create(optr_comm* out, int device, int rank, int n, int64_t max_le
   Shards sh = make_shards(c->max_dim, n);
   int64_t smax = sh.base + (sh.extra ? 1 : 0);
   size_t off = 0;
-  c->off_flags = off;
-  off = align_up(off + OPTR_MAX_WORKERS * 8, 256);
-  c->off_y = off;
-  off = align_up(off + (size_t)c->max_dim * 4, 256);
-  c->off_a = off;
-  off = align_up(off + (size_t)smax * 4, 256);
+  for (int f = 0; f < 3; ++f) {
+    c->off_flags[f] = off;
+    off = align_up(off + OPTR_MAX_WORKERS * 8, 256);
+  }
+  for (int p = 0; p < 2; ++p) {
+    c->off_y[p] = off;
+    off = align_up(off + (size_t)c->max_dim * 4, 1024);
+    c->off_a[p] = off;
+    off = align_up(off + (size_t)smax * 4, 1024);
+  }
   c->sym_bytes = off;
   int64_t pw = mask_words(c->max_dim, n, 1);  // epp >= 1 bound
   off = 0;
@@ -1051,6 +1059,8 @@ int optr_comm_create(optr_comm* out, int device, int rank, int n, int64_t max_le
   for (int p = 0; p < 2; ++p) {
     CK(cudaEventCreateWithFlags(&c->prep_ready[p], cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&c->done[p], cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&c->fork[p], cudaEventDisableTiming));
+    CK(cudaStreamCreateWithFlags(&c->ws[p], cudaStreamNonBlocking));
   }
   CK(cudaDeviceSynchronize());
   c->peer[rank] = c->sym;
@@ -1094,6 +1104,8 @@ int optr_comm_destroy(optr_comm c) {
   for (int p = 0; p < 2; ++p) {
     cudaEventDestroy(c->prep_ready[p]);
     cudaEventDestroy(c->done[p]);
+    cudaEventDestroy(c->fork[p]);
+    cudaStreamDestroy(c->ws[p]);
   }
   free(c);
   return OPTR_OK;
@@ -1116,26 +1128,56 @@ __global__ void barrier_kernel2(FlagPtrs peers, unsigned long long* mine, int ra
   } while (v < epoch);
 }
 
-int optr_comm_barrier(optr_comm c, void* stream) {
-  if (!c) return OPTR_EINVAL;
+static int comm_barrier(optr_comm c, int set, cudaStream_t st) {
   FlagPtrs fp;
   memset(&fp, 0, sizeof(fp));
   for (int i = 0; i < c->n; ++i) {
     if (!c->peer[i]) return OPTR_EINVAL;
-    fp.f[i] = (unsigned long long*)(c->peer[i] + c->off_flags);
+    fp.f[i] = (unsigned long long*)(c->peer[i] + c->off_flags[set]);
   }
-  c->epoch += 1;
-  KScope ks(OPTR_K_BARRIER, (cudaStream_t)stream);
-  barrier_kernel2<<<1, 32, 0, (cudaStream_t)stream>>>(fp, (unsigned long long*)(c->sym + c->off_flags),
-                                                      c->rank, c->n, c->epoch);
+  c->epoch[set] += 1;
+  KScope ks(OPTR_K_BARRIER, st);
+  barrier_kernel2<<<1, 32, 0, st>>>(fp, (unsigned long long*)(c->sym + c->off_flags[set]), c->rank, c->n,
+                                     c->epoch[set]);
   CK(cudaGetLastError());
   return OPTR_OK;
 }
 
-int optr_tar(optr_comm c, const void* x, void* out, int64_t L, int dtype_in, int dtype_out,
-             uint64_t job_seed, uint64_t bucket_id, uint64_t generation, int rotation, int ht,
-             const optr_mask_spec* masks,
+int optr_comm_barrier(optr_comm c, void* stream) {
+  if (!c) return OPTR_EINVAL;
+  CK(cudaSetDevice(c->device));
+  return comm_barrier(c, 2, (cudaStream_t)stream);
+}
+
+int optr_comm_join(optr_comm c, void* stream) {
+  if (!c) return OPTR_EINVAL;
+  CK(cudaSetDevice(c->device));
+  for (int p = 0; p < 2; ++p)
+    if (c->done_recorded[p]) CK(cudaStreamWaitEvent((cudaStream_t)stream, c->done[p], 0));
+  return OPTR_OK;
+}
+
+static int tar_enqueue(optr_comm c, const void* x, void* out, int64_t L, int dtype_in, int dtype_out,
+                       uint64_t job_seed, uint64_t bucket_id, uint64_t generation, int rotation, int ht,
+                       const optr_mask_spec* masks, uint64_t* received_out, void* stream, bool async);
+
+int optr_tar(optr_comm c, const void* x, void* out, int64_t L, int dtype_in, int dtype_out, uint64_t job_seed,
+             uint64_t bucket_id, uint64_t generation, int rotation, int ht, const optr_mask_spec* masks,
              uint64_t* received_out, void* stream) {
+  return tar_enqueue(c, x, out, L, dtype_in, dtype_out, job_seed, bucket_id, generation, rotation, ht, masks,
+                     received_out, stream, false);
+}
+
+int optr_tar_async(optr_comm c, const void* x, void* out, int64_t L, int dtype_in, int dtype_out,
+                   uint64_t job_seed, uint64_t bucket_id, uint64_t generation, int rotation, int ht,
+                   const optr_mask_spec* masks, uint64_t* received_out, void* stream) {
+  return tar_enqueue(c, x, out, L, dtype_in, dtype_out, job_seed, bucket_id, generation, rotation, ht, masks,
+                     received_out, stream, true);
+}
+
+static int tar_enqueue(optr_comm c, const void* x, void* out, int64_t L, int dtype_in, int dtype_out,
+                       uint64_t job_seed, uint64_t bucket_id, uint64_t generation, int rotation, int ht,
+                       const optr_mask_spec* masks, uint64_t* received_out, void* stream, bool async) {
   if (!c) return OPTR_EINVAL;
   int n = c->n;
   int rc = check_common(n, L, dtype_in, dtype_out, masks);
@@ -1148,10 +1190,15 @@ int optr_tar(optr_comm c, const void* x, void* out, int64_t L, int dtype_in, int
   for (int i = 0; i < n; ++i)
     if (!c->peer[i]) return OPTR_EINVAL;  // optr_comm_open not called
   CK(cudaSetDevice(c->device));
-  cudaStream_t st = (cudaStream_t)stream;
+  const cudaStream_t caller = (cudaStream_t)stream;
   const int me = c->rank;
   const int r = ((rotation % n) + n) % n;
   const int par = (int)(c->calls++ & 1);
+  // this call's kernels run on the parity's work stream, after the caller's
+  // prior work (inputs ready)
+  const cudaStream_t st = c->ws[par];
+  CK(cudaEventRecord(c->fork[par], caller));
+  CK(cudaStreamWaitEvent(st, c->fork[par], 0));
   char* const loc = c->local + (size_t)par * c->local_bytes;
   uint32_t* signs = (uint32_t*)(loc + c->off_signs);
   uint32_t* bitmap = (uint32_t*)(loc + c->off_bitmap);
@@ -1159,8 +1206,8 @@ int optr_tar(optr_comm c, const void* x, void* out, int64_t L, int dtype_in, int
   float* Yp[kMaxW];
   float* Ap[kMaxW];
   for (int i = 0; i < n; ++i) {
-    Yp[i] = (float*)(c->peer[i] + c->off_y);
-    Ap[i] = (float*)(c->peer[i] + c->off_a);
+    Yp[i] = (float*)(c->peer[i] + c->off_y[par]);
+    Ap[i] = (float*)(c->peer[i] + c->off_a[par]);
   }
   Shards sh = make_shards(dim, n);
 
@@ -1198,7 +1245,7 @@ int optr_tar(optr_comm c, const void* x, void* out, int64_t L, int dtype_in, int
     cast_copy_kernel<<<1184, 256, 0, st>>>(x, dtype_in, Yp[me], dim);
     CK(cudaGetLastError());
   }
-  if ((rc = optr_comm_barrier(c, stream))) return rc;
+  if ((rc = comm_barrier(c, par, st))) return rc;
 
   // stage 1: pull my shard from every peer over NVLink, masked mean
   AggArgs ag;
@@ -1214,7 +1261,7 @@ int optr_tar(optr_comm c, const void* x, void* out, int64_t L, int dtype_in, int
   ag.owner_base = me;
   int64_t smax = sh.base + (sh.extra ? 1 : 0);
   if ((rc = launch_aggregate(ag, 1, smax, st))) return rc;
-  if ((rc = optr_comm_barrier(c, stream))) return rc;
+  if ((rc = comm_barrier(c, par, st))) return rc;
 
   // stage 2: pull every owner's aggregate over NVLink, fused into decode
   SrcGather ga;
@@ -1262,6 +1309,7 @@ int optr_tar(optr_comm c, const void* x, void* out, int64_t L, int dtype_in, int
   }
   CK(cudaEventRecord(c->done[par], st));
   c->done_recorded[par] = true;
+  if (!async) CK(cudaStreamWaitEvent(caller, c->done[par], 0));
   return OPTR_OK;
 }
 

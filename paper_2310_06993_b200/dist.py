@@ -79,10 +79,14 @@ class TarCommunicator:
 
     def allreduce(self, x, out, *, rotation: int, ht: bool = True, job_seed: int = 0,
                   generation: int = 0, bucket_id: int | None = None, masks: MaskSpec | None = None,
-                  received=None, stream=None):
+                  received=None, stream=None, async_op: bool = False):
         """This rank's part of one TAR(+RHT) generation.  ``x``/``out`` are
         this rank's CUDA buffers (fp32/bf16).  ``received``: optional CUDA
-        int64[2] for (stage-1, stage-2) received entries."""
+        int64[2] for (stage-1, stage-2) received entries.
+
+        ``async_op=True`` lets consecutive buckets overlap (optr_tar_async):
+        the stream does not wait for ``out`` until ``join()``; keep ``x`` and
+        ``out`` untouched until then."""
         import torch
 
         if self._h is None:
@@ -94,12 +98,20 @@ class TarCommunicator:
             pass  # epp is per call; buffers only bound the packet count
         spec = masks.to_c()
         st = stream if stream is not None else torch.cuda.current_stream(self.device)
-        check(lib().optr_tar(self._h, x.data_ptr(), out.data_ptr(), len(x), _dtype_code(x), _dtype_code(out),
+        fn = lib().optr_tar_async if async_op else lib().optr_tar
+        check(fn(self._h, x.data_ptr(), out.data_ptr(), len(x), _dtype_code(x), _dtype_code(out),
                              int(job_seed), int(generation % 65536 if bucket_id is None else bucket_id),
                              int(generation), int(rotation), int(bool(ht)), ctypes.byref(spec),
                              received.data_ptr() if received is not None else None, st.cuda_stream),
               "tar")
         return out
+
+    def join(self, stream=None):
+        """Make ``stream`` (default: current) wait for all async calls."""
+        import torch
+
+        st = stream if stream is not None else torch.cuda.current_stream(self.device)
+        check(lib().optr_comm_join(self._h, st.cuda_stream), "comm_join")
 
     def close(self):
         if self._h is not None:
