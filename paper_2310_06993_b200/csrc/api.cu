@@ -886,7 +886,7 @@ int optr_tar_local(const void* const* x, void* const* out, int n, int64_t L, int
   const uint32_t* cbits = nullptr;
   if ((rc = setup_masks(pa, masks, dim, n, r, epp, bitmap, counts, 0, n, &cbits))) return rc;
   if ((rc = launch_prep(pa, st))) return rc;
-  MaskView mv{cbits, pa.pw, n, epp};
+  MaskView mv{cbits, pa.pw, n, epp, make_divider((uint32_t)epp)};
   Shards sh = make_shards(dim, n);
 
   // 2. wire vectors
@@ -1222,7 +1222,7 @@ static int tar_enqueue(optr_comm c, const void* x, void* out, int64_t L, int dty
   if ((rc = launch_prep(pa, ps))) return rc;
   CK(cudaEventRecord(c->prep_ready[par], ps));
   CK(cudaStreamWaitEvent(st, c->prep_ready[par], 0));
-  MaskView mv{cbits, pa.pw, n, epp};
+  MaskView mv{cbits, pa.pw, n, epp, make_divider((uint32_t)epp)};
 
   // encode into my symmetric wire buffer
   if (ht) {

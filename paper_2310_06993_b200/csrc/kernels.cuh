@@ -64,12 +64,32 @@ __host__ __device__ __forceinline__ int64_t n_packets(int64_t len, int epp) {
   return len > 0 ? (len + epp - 1) / epp : 0;
 }
 
+// Exact e / d for 32-bit e via a 64-bit multiply-high: q = umulhi64(e, M),
+// M = ceil(2^64 / d); the error e(Md - 2^64)/(d 2^64) < e/2^64 < 1/d.
+struct Divider {
+  uint64_t m;  // 0 when d == 1
+  __device__ __forceinline__ uint32_t div(uint32_t e) const {
+    return m ? (uint32_t)__umul64hi((unsigned long long)e, (unsigned long long)m) : e;
+  }
+};
+inline Divider make_divider(uint32_t d) {
+  Divider v;
+  if (d <= 1) {
+    v.m = 0;
+  } else {
+    unsigned __int128 one = (unsigned __int128)1 << 64;
+    v.m = (uint64_t)((one + d - 1) / d);
+  }
+  return v;
+}
+
 // Packet-bitmap addressing (optr.h): stage 0/1, receiver dst, sender src.
 struct MaskView {
   const uint32_t* bits;
   int64_t pw;  // u32 words per pair
   int n;
   int epp;
+  Divider dv;  // division by epp
   __device__ __forceinline__ const uint32_t* row(int stage, int dst, int src) const {
     return bits + ((int64_t)(stage * n + dst) * n + src) * pw;
   }
@@ -77,6 +97,27 @@ struct MaskView {
 
 __device__ __forceinline__ bool row_bit(const uint32_t* row, uint32_t pkt) {
   return (__ldg(row + (pkt >> 5)) >> (pkt & 31)) & 1u;
+}
+
+// Keep-flags (bit c = entry e+c delivered) of 4 consecutive shard entries
+// e..e+3 from a packet bitmap row: one word load, one packet boundary at most
+// when epp >= 4.
+__device__ __forceinline__ uint32_t keep4(const uint32_t* row, uint32_t e, const MaskView& m) {
+  const uint32_t epp = (uint32_t)m.epp;
+  if (epp >= 4) {
+    const uint32_t p0 = m.dv.div(e), rem = e - p0 * epp;
+    const uint32_t w = __ldg(row + (p0 >> 5)) >> (p0 & 31);
+    const uint32_t b0 = w & 1u;
+    if (rem + 3 < epp) return b0 ? 0xFu : 0u;
+    const uint32_t b1 = (p0 & 31) == 31 ? (__ldg(row + (p0 >> 5) + 1) & 1u) : ((w >> 1) & 1u);
+    const uint32_t split = epp - rem;  // entries 0..split-1 in p0, the rest in p0+1
+    const uint32_t lo = (1u << split) - 1u;
+    return (b0 ? lo : 0u) | (b1 ? (0xFu & ~lo) : 0u);
+  }
+  uint32_t k = 0;
+#pragma unroll
+  for (int c = 0; c < 4; ++c) k |= (row_bit(row, (e + c) / epp) ? 1u : 0u) << c;
+  return k;
 }
 
 // packet index of entries e..e+3 of a shard (epp = entries per packet)
@@ -371,9 +412,8 @@ struct SrcGather {
     __device__ __forceinline__ float4 load4_in(const float* a, const uint32_t* row, uint32_t e, int64_t g) const {
       float4 v = ldg4(a + e);
       if (row) {
-        Pkt4 pk = pkt4(e, (uint32_t)p->m.epp);
-        bool k0 = row_bit(row, pk.p[0]), k1 = row_bit(row, pk.p[1]);
-        bool k2 = row_bit(row, pk.p[2]), k3 = row_bit(row, pk.p[3]);
+        const uint32_t kk = keep4(row, e, p->m);
+        const bool k0 = kk & 1u, k1 = kk & 2u, k2 = kk & 4u, k3 = kk & 8u;
         v.x = k0 ? v.x : 0.f;
         v.y = k1 ? v.y : 0.f;
         v.z = k2 ? v.z : 0.f;
@@ -815,7 +855,6 @@ __global__ void __launch_bounds__(256) aggregate_kernel(const __grid_constant__ 
     for (int64_t e4 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e4 < n4;
          e4 += (int64_t)gridDim.x * blockDim.x) {
       const int64_t e = e4 * 4;
-      const Pkt4 pk = pkt4((uint32_t)e, epp);
       double acc[4] = {0.0, 0.0, 0.0, 0.0}, cnt[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
       for (int i = 0; i < kMaxW; ++i) {
@@ -831,9 +870,8 @@ __global__ void __launch_bounds__(256) aggregate_kernel(const __grid_constant__ 
             cnt[2] += 1.0;
             cnt[3] += 1.0;
           } else {
-            const uint32_t* row = a.m.row(0, o, i);
-            const bool k0 = row_bit(row, pk.p[0]), k1 = row_bit(row, pk.p[1]);
-            const bool k2 = row_bit(row, pk.p[2]), k3 = row_bit(row, pk.p[3]);
+            const uint32_t kk = keep4(a.m.row(0, o, i), (uint32_t)e, a.m);
+            const bool k0 = kk & 1u, k1 = kk & 2u, k2 = kk & 4u, k3 = kk & 8u;
             acc[0] += k0 ? (double)v.x : 0.0;
             acc[1] += k1 ? (double)v.y : 0.0;
             acc[2] += k2 ? (double)v.z : 0.0;

@@ -162,25 +162,12 @@ __device__ __forceinline__ float4 gather_mask4(const TmaArgs& a, int64_t g, floa
     return v;
   }
   const uint32_t e = (uint32_t)(g - ((int64_t)j << a.shard_shift));
-  const uint32_t* row = a.m.row(1, a.q, owner);
-  const uint32_t epp = (uint32_t)a.m.epp;
-  bool k0, k1, k2, k3;
-  if (epp >= 4) {  // the 4 entries span packets p0 and at most p0+1
-    const uint32_t p0 = e / epp, rem = e - p0 * epp;
-    const uint32_t w = __ldg(row + (p0 >> 5));
-    const bool c0 = (w >> (p0 & 31)) & 1u;
-    const bool c1 = (p0 & 31) == 31 ? (__ldg(row + (p0 >> 5) + 1) & 1u) : ((w >> ((p0 & 31) + 1)) & 1u);
-    k0 = c0;
-    k1 = rem + 1 >= epp ? c1 : c0;
-    k2 = rem + 2 >= epp ? c1 : c0;
-    k3 = rem + 3 >= epp ? c1 : c0;
-  } else {
-    const Pkt4 pk = pkt4(e, epp);
-    k0 = row_bit(row, pk.p[0]);
-    k1 = row_bit(row, pk.p[1]);
-    k2 = row_bit(row, pk.p[2]);
-    k3 = row_bit(row, pk.p[3]);
+  const uint32_t kk = keep4(a.m.row(1, a.q, owner), e, a.m);
+  if (kk == 0xFu) {
+    if (a.got) *reinterpret_cast<uchar4*>(a.got + g) = make_uchar4(1, 1, 1, 1);
+    return v;
   }
+  const bool k0 = kk & 1u, k1 = kk & 2u, k2 = kk & 4u, k3 = kk & 8u;
   if (a.got) *reinterpret_cast<uchar4*>(a.got + g) = make_uchar4(k0, k1, k2, k3);
   return make_float4(k0 ? v.x : 0.f, k1 ? v.y : 0.f, k2 ? v.z : 0.f, k3 ? v.w : 0.f);
 }
@@ -451,36 +438,30 @@ __global__ void __launch_bounds__(CH / 4) tma_agg_kernel(const __grid_constant__
     if (c < nchunks) issue(c, 0);
     if (c + stride < nchunks) issue(c + stride, 1);
   }
-  const uint32_t epp = (uint32_t)a.m.epp;
   for (int k = 0; c < nchunks; ++k, c += stride) {
     const int s = k & 1;
     mbar_wait(&full[s], (uint32_t)((k >> 1) & 1));
     const int64_t e = c * CH + tid * 4;
     float4 res = make_float4(0.f, 0.f, 0.f, 0.f);
     if (e < len) {
-      const Pkt4 pk = pkt4((uint32_t)e, epp);
-      double acc[4] = {0.0, 0.0, 0.0, 0.0}, cnt[4] = {0.0, 0.0, 0.0, 0.0};
+      double acc[4] = {0.0, 0.0, 0.0, 0.0};
+      uint32_t c4[4] = {0u, 0u, 0u, 0u};
+      const float* src = buf + (size_t)s * n * CH + tid * 4;
       for (int i = 0; i < n; ++i) {
-        const float4 v = *reinterpret_cast<const float4*>(buf + ((size_t)s * n + i) * CH + tid * 4);
-        bool k0 = true, k1 = true, k2 = true, k3 = true;
-        if (i != o) {
-          const uint32_t* row = a.m.row(0, o, i);
-          k0 = row_bit(row, pk.p[0]);
-          k1 = row_bit(row, pk.p[1]);
-          k2 = row_bit(row, pk.p[2]);
-          k3 = row_bit(row, pk.p[3]);
-        }
-        acc[0] += k0 ? (double)v.x : 0.0;
-        acc[1] += k1 ? (double)v.y : 0.0;
-        acc[2] += k2 ? (double)v.z : 0.0;
-        acc[3] += k3 ? (double)v.w : 0.0;
-        cnt[0] += k0 ? 1.0 : 0.0;
-        cnt[1] += k1 ? 1.0 : 0.0;
-        cnt[2] += k2 ? 1.0 : 0.0;
-        cnt[3] += k3 ? 1.0 : 0.0;
+        const float4 v = *reinterpret_cast<const float4*>(src + (size_t)i * CH);
+        const uint32_t kk = i == o ? 0xFu : keep4(a.m.row(0, o, i), (uint32_t)e, a.m);
+        // misses add +0.0 (the reference adds its zero-filled buffer)
+        acc[0] += (kk & 1u) ? (double)v.x : 0.0;
+        acc[1] += (kk & 2u) ? (double)v.y : 0.0;
+        acc[2] += (kk & 4u) ? (double)v.z : 0.0;
+        acc[3] += (kk & 8u) ? (double)v.w : 0.0;
+        c4[0] += kk & 1u;
+        c4[1] += (kk >> 1) & 1u;
+        c4[2] += (kk >> 2) & 1u;
+        c4[3] += (kk >> 3) & 1u;
       }
-      res = make_float4(mean_of(acc[0], cnt[0]), mean_of(acc[1], cnt[1]), mean_of(acc[2], cnt[2]),
-                        mean_of(acc[3], cnt[3]));
+      res = make_float4(mean_of(acc[0], (double)c4[0]), mean_of(acc[1], (double)c4[1]),
+                        mean_of(acc[2], (double)c4[2]), mean_of(acc[3], (double)c4[3]));
     }
     __syncthreads();  // stage s has been read
     if (tid == 0 && c + 2 * stride < nchunks) issue(c + 2 * stride, s);
