@@ -378,7 +378,11 @@ int launch_tma_aggregate(const AggArgs& ag, int nowners, int64_t smax, cudaStrea
   a.owner_base = ag.owner_base;
   a.m = ag.m;
   const size_t smem = tma_agg_smem_bytes<kAggChunk>(ag.n);
-  int rc = set_smem_attr(tma_agg_kernel<kAggChunk>, smem);
+  auto kern = ag.n == 2 ? tma_agg_kernel<kAggChunk, 2>
+            : ag.n == 4 ? tma_agg_kernel<kAggChunk, 4>
+            : ag.n == 8 ? tma_agg_kernel<kAggChunk, 8>
+                        : tma_agg_kernel<kAggChunk, 0>;
+  int rc = set_smem_attr(kern, smem);
   if (rc) return rc;
   static int nsm = 0;
   if (!nsm) {
@@ -395,8 +399,8 @@ int launch_tma_aggregate(const AggArgs& ag, int nowners, int64_t smax, cudaStrea
   if (gx < 1) gx = 1;
   if (gx > nchunks) gx = nchunks;
   KScope ks(OPTR_K_AGG, st, nowners);
-  tma_agg_kernel<kAggChunk><<<dim3((unsigned)gx, (unsigned)nowners), kAggChunk / 4, smem, st>>>(a);
-  return launch_check(tma_agg_kernel<kAggChunk>, "tma_aggregate", 0, 0, (int)gx, nowners, kAggChunk / 4, smem);
+  kern<<<dim3((unsigned)gx, (unsigned)nowners), kAggChunk / 4, smem, st>>>(a);
+  return launch_check(kern, "tma_aggregate", 0, 0, (int)gx, nowners, kAggChunk / 4, smem);
 }
 
 template <class S>

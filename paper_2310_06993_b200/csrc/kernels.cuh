@@ -835,9 +835,12 @@ struct AggArgs {
 // acc / cnt with cnt in 1..n: a power-of-two count divides exactly by
 // multiplying with its reciprocal; otherwise IEEE division (np.divide).
 __device__ __forceinline__ float mean_of(double acc, double cnt) {
-  unsigned c = (unsigned)cnt;
-  double q = (c & (c - 1)) == 0 ? acc * (1.0 / cnt) : acc / cnt;
-  return (float)q;
+  const unsigned c = (unsigned)cnt;
+  if ((c & (c - 1)) == 0) {  // exact: multiply by 2^-log2(c), built from its exponent bits
+    const long long e = 1023 - (long long)(__ffs(c) - 1);
+    return (float)(acc * __longlong_as_double(e << 52));
+  }
+  return (float)(acc / cnt);
 }
 
 // collectives.py:77-94 with the own shard at its rank position and

@@ -405,14 +405,14 @@ __host__ __device__ constexpr size_t tma_agg_smem_bytes(int n) {
   return (size_t)2 * n * CH * sizeof(float) + 64 + 1024;
 }
 
-template <int CH>
+template <int CH, int NW>
 __global__ void __launch_bounds__(CH / 4) tma_agg_kernel(const __grid_constant__ TmaAggArgs a) {
   extern __shared__ __align__(16) unsigned char smraw[];
   unsigned char* const base = smraw + ((1024u - (smem_u32(smraw) & 1023u)) & 1023u);
   float* const buf = reinterpret_cast<float*>(base);  // [2][n][CH]
   uint64_t* const full = reinterpret_cast<uint64_t*>(base + (size_t)2 * a.n * CH * sizeof(float));
   const int tid = threadIdx.x;
-  const int n = a.n;
+  const int n = NW > 0 ? NW : a.n;  // compile-time worker count for the common n
   const int o = a.owner_base + blockIdx.y;
   const int j = owned_shard(o, a.r, n);
   const int64_t off = a.sh.off(j), len = a.sh.len(j);
@@ -447,7 +447,9 @@ __global__ void __launch_bounds__(CH / 4) tma_agg_kernel(const __grid_constant__
       double acc[4] = {0.0, 0.0, 0.0, 0.0};
       uint32_t c4[4] = {0u, 0u, 0u, 0u};
       const float* src = buf + (size_t)s * n * CH + tid * 4;
-      for (int i = 0; i < n; ++i) {
+#pragma unroll
+      for (int i = 0; i < (NW > 0 ? NW : kMaxW); ++i) {
+        if (NW == 0 && i >= n) break;
         const float4 v = *reinterpret_cast<const float4*>(src + (size_t)i * CH);
         const uint32_t kk = i == o ? 0xFu : keep4(a.m.row(0, o, i), (uint32_t)e, a.m);
         // misses add +0.0 (the reference adds its zero-filled buffer)
