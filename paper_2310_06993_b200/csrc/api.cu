@@ -239,8 +239,8 @@ bool make_map3(CUtensorMap* m, const void* base, uint64_t d0, uint64_t d1, uint6
 }
 
 template <int T, int S, bool STRIDED, int SK, class Snk>
-int launch_tma_pass_s(int cls, const TmaMaps& maps, const CUtensorMap& dmap, const TmaArgs& a, const Snk& snk,
-                      int worker, cudaStream_t st) {
+int launch_tma_pass_s(int cls, const TmaMaps& maps, const TmaMaps& dmaps, const TmaArgs& a, const Snk& snk,
+                      int worker, int nworkers, cudaStream_t st) {
   const size_t smem = tma_smem_bytes<T, S>();
   auto kern = tma_pass_kernel<T, S, STRIDED, SK, Snk>;
   int rc = set_smem_attr(kern, smem);
@@ -254,12 +254,12 @@ int launch_tma_pass_s(int cls, const TmaMaps& maps, const CUtensorMap& dmap, con
   }
   int per_sm = (int)((227 * 1024) / (smem + 1024));
   if (per_sm < 1) per_sm = 1;
-  int64_t gx = (int64_t)nsm * per_sm;
+  int64_t gx = ((int64_t)nsm * per_sm + nworkers - 1) / nworkers;
   if (gx > a.ntiles) gx = a.ntiles;
-  KScope ks(cls, st);
-  kern<<<(unsigned)gx, 1 << (T - 5), smem, st>>>(maps, dmap, a, snk, worker);
-  return launch_check(kern, STRIDED ? "tma_strided" : "tma_contig", T, STRIDED ? 3 : 0, (int)gx, 1, 1 << (T - 5),
-                      smem);
+  KScope ks(cls, st, nworkers);
+  kern<<<dim3((unsigned)gx, (unsigned)nworkers), 1 << (T - 5), smem, st>>>(maps, dmaps, a, snk, worker);
+  return launch_check(kern, STRIDED ? "tma_strided" : "tma_contig", T, STRIDED ? 3 : 0, (int)gx, nworkers,
+                      1 << (T - 5), smem);
 }
 
 // ring depth of the TMA pass kernels (OPTR_TMA_STAGES=3 for three)
@@ -273,14 +273,16 @@ int tma_stages() {
 }
 
 template <int T, bool STRIDED, int SK, class Snk>
-int launch_tma_pass(int cls, const TmaMaps& maps, const CUtensorMap& dmap, const TmaArgs& a, const Snk& snk,
-                    int worker, cudaStream_t st) {
-  if (tma_stages() == 3) return launch_tma_pass_s<T, 3, STRIDED, SK>(cls, maps, dmap, a, snk, worker, st);
-  return launch_tma_pass_s<T, 2, STRIDED, SK>(cls, maps, dmap, a, snk, worker, st);
+int launch_tma_pass(int cls, const TmaMaps& maps, const TmaMaps& dmaps, const TmaArgs& a, const Snk& snk,
+                    int worker, int nworkers, cudaStream_t st) {
+  if (tma_stages() == 3)
+    return launch_tma_pass_s<T, 3, STRIDED, SK>(cls, maps, dmaps, a, snk, worker, nworkers, st);
+  return launch_tma_pass_s<T, 2, STRIDED, SK>(cls, maps, dmaps, a, snk, worker, nworkers, st);
 }
 
 // A pass through the TMA ring kernel when the shapes allow it; -1 when the
-// caller should use the LSU kernels instead.
+// caller should use the LSU kernels instead.  Workers [worker, worker+nworkers)
+// go in one launch (grid.y = worker).
 template <class Src, class Snk>
 int try_tma(int cls, const PassGeom& pg, int nlog, int worker, int nworkers, const Src& src, const Snk& snk,
             cudaStream_t st) {
@@ -293,23 +295,22 @@ int try_tma(int cls, const PassGeom& pg, int nlog, int worker, int nworkers, con
     return -1;
   } else {
     const int T = pg.cb + pg.ks;
-    if (nworkers != 1 || !tma_enabled()) return -1;
+    if (!tma_enabled()) return -1;
     TmaArgs a;
     memset(&a, 0, sizeof(a));
     a.ntiles = pg.ntiles;
     a.lo = pg.lo;
-    TmaMaps maps;
+    TmaMaps maps, dmaps;
     memset(&maps, 0, sizeof(maps));
-    CUtensorMap dmap;
-    memset(&dmap, 0, sizeof(dmap));
+    memset(&dmaps, 0, sizeof(dmaps));
     if constexpr (kGather) {
       for (int o = 0; o < src.n; ++o) a.A[o] = src.A[o];
-      a.q = worker;
       a.n = src.n;
       a.r = src.r;
       a.shard_shift = src.pow2_shift;
       a.m = src.m;
-      a.got = src.got ? src.got + (int64_t)worker * src.dim : nullptr;
+      a.got = src.got;
+      a.dim = src.dim;
     }
     if (pg.cb == 3) {  // strided: tensor boxes in, tensor boxes out
       if constexpr (kEnc) {
@@ -324,42 +325,50 @@ int try_tma(int cls, const PassGeom& pg, int nlog, int worker, int nworkers, con
           if (srows < box) box = (int)srows;
           for (int o = 0; o < src.n; ++o)
             if (!make_map3(&maps.m[o], src.A[o], d0, (uint64_t)srows, 1, (uint32_t)box)) return -1;
-        } else {
-          if (!make_map3(&maps.m[0], src.y[worker], d0, d1, d2, (uint32_t)box)) return -1;
         }
-        if constexpr (kSnkBuf) {
-          if (!make_map3(&dmap, snk.y[worker], d0, d1, d2, (uint32_t)box)) return -1;
-          a.scale = snk.scale;
-        } else {  // decode epilogue: map over the full rows of `out`
-          if (d2 != 1) return -1;
-          const int64_t rows_full = snk.L >> pg.lo;
-          if (rows_full > 0 &&
-              !make_map3(&dmap, snk.out[worker], d0, (uint64_t)rows_full, 1, (uint32_t)box, snk.dtype))
-            return -1;
-          if (((uintptr_t)snk.out[worker] & 15) || ((uintptr_t)snk.signs & 15)) return -1;
+        for (int w = worker; w < worker + nworkers; ++w) {
+          if constexpr (kBuf) {
+            if (!make_map3(&maps.m[w], src.y[w], d0, d1, d2, (uint32_t)box)) return -1;
+          }
+          if constexpr (kSnkBuf) {
+            if (!make_map3(&dmaps.m[w], snk.y[w], d0, d1, d2, (uint32_t)box)) return -1;
+          } else {  // decode epilogue: map over the full rows of `out`
+            if (d2 != 1) return -1;
+            const int64_t rows_full = snk.L >> pg.lo;
+            if (rows_full > 0 &&
+                !make_map3(&dmaps.m[w], snk.out[w], d0, (uint64_t)rows_full, 1, (uint32_t)box, snk.dtype))
+              return -1;
+            if (((uintptr_t)snk.out[w] & 15) || ((uintptr_t)snk.signs & 15)) return -1;
+          }
         }
+        if constexpr (kSnkBuf) a.scale = snk.scale;
         a.box_rows = box;
         switch (T) {
-          case 12: return launch_tma_pass<12, true, SK>(cls, maps, dmap, a, snk, worker, st);
-          case 13: return launch_tma_pass<13, true, SK>(cls, maps, dmap, a, snk, worker, st);
-          default: return launch_tma_pass<14, true, SK>(cls, maps, dmap, a, snk, worker, st);
+          case 12: return launch_tma_pass<12, true, SK>(cls, maps, dmaps, a, snk, worker, nworkers, st);
+          case 13: return launch_tma_pass<13, true, SK>(cls, maps, dmaps, a, snk, worker, nworkers, st);
+          default: return launch_tma_pass<14, true, SK>(cls, maps, dmaps, a, snk, worker, nworkers, st);
         }
       }
     }
     if (pg.cb != 0 || pg.lo != 0 || (T != 13 && T != 14)) return -1;
-    if constexpr (kBuf) {
-      a.x = src.y[worker];
-    } else if constexpr (kEnc) {
-      a.x = src.x[worker];
+    for (int w = worker; w < worker + nworkers; ++w) {
+      if constexpr (kBuf) {
+        a.xw[w] = src.y[w];
+      } else if constexpr (kEnc) {
+        a.xw[w] = src.x[w];
+        if (((uintptr_t)a.xw[w] & 15) || ((uintptr_t)src.signs & 15)) return -1;
+      }
+    }
+    if constexpr (kEnc) {
       a.dtype = src.dtype;
       a.L = src.L;
       a.signs = src.signs;
-      if (((uintptr_t)a.x & 15) || ((uintptr_t)a.signs & 15)) return -1;
-    } else {
+    }
+    if constexpr (kGather) {
       if (src.pow2_shift < T) return -1;
     }
-    if (T == 13) return launch_tma_pass<13, false, SK>(cls, maps, dmap, a, snk, worker, st);
-    return launch_tma_pass<14, false, SK>(cls, maps, dmap, a, snk, worker, st);
+    if (T == 13) return launch_tma_pass<13, false, SK>(cls, maps, dmaps, a, snk, worker, nworkers, st);
+    return launch_tma_pass<14, false, SK>(cls, maps, dmaps, a, snk, worker, nworkers, st);
   }
 }
 
@@ -511,6 +520,12 @@ int workers_per_launch(int64_t dim, int n) {
     cudaGetDevice(&dev);
     if (cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev) != cudaSuccess || l2 <= 0) l2 = 50 << 20;
   }
+  static int batch = -1;
+  if (batch < 0) {
+    const char* e = getenv("OPTR_BATCH_WORKERS");
+    batch = (e && e[0] == '1') ? 1 : 0;
+  }
+  if (batch) return n;
   int64_t bytes = dim * 4;
   int k = (int)((int64_t)l2 / 2 / (bytes > 0 ? bytes : 1));
   if (k < 1) k = 1;

@@ -37,17 +37,19 @@ struct TmaArgs {
   int lo;        // strided: first transformed bit (row stride 2^lo entries)
   int box_rows;  // strided: rows per TMA box (<= 256)
   float scale;   // strided sink: result scale
-  // TS_BUF / TS_ENC (contiguous): source vector; TS_ENC: x of `dtype`, L entries
-  const void* x;
+  // TS_BUF / TS_ENC (contiguous): source vector of each worker; TS_ENC: x of
+  // `dtype`, L entries
+  const void* xw[kMaxW];
   int dtype;
   int64_t L;
   const uint32_t* signs;
-  // TS_GATHER (collectives.py:140-150): owner shards, stage-2 masks of worker q
+  // TS_GATHER (collectives.py:140-150): owner shards, stage-2 masks
   const float* A[kMaxW];
-  int q, n, r;
+  int n, r;
   int shard_shift;  // equal power-of-two shards of 2^shard_shift entries
   MaskView m;
-  uint8_t* got;  // optional, offset to worker q
+  uint8_t* got;  // optional [worker][dim]
+  int64_t dim;
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -108,8 +110,8 @@ __host__ __device__ constexpr size_t tma_smem_bytes() {
 
 // Issue the loads of tile t into stage buffer `st` (sign words after the tile).
 template <int T, bool STRIDED, int SK>
-__device__ __forceinline__ void tile_issue(const TmaMaps& maps, const TmaArgs& a, int64_t t, unsigned char* st,
-                                           uint64_t* bar) {
+__device__ __forceinline__ void tile_issue(const TmaMaps& maps, const TmaArgs& a, int w, int64_t t,
+                                           unsigned char* st, uint64_t* bar) {
   if constexpr (STRIDED) {
     constexpr int KS = T - 3;
     const int cgb = a.lo - 3;
@@ -125,7 +127,7 @@ __device__ __forceinline__ void tile_issue(const TmaMaps& maps, const TmaArgs& a
         const int j = row >> rsh;
         tma_load_3d(dst, &maps.m[shard_owner(j, a.r, a.n)], bar, c0, row - (j << rsh), 0);
       } else {
-        tma_load_3d(dst, &maps.m[0], bar, c0, row, outer);
+        tma_load_3d(dst, &maps.m[w], bar, c0, row, outer);
       }
     }
   } else {
@@ -137,7 +139,7 @@ __device__ __forceinline__ void tile_issue(const TmaMaps& maps, const TmaArgs& a
       bulk_load(st, a.A[shard_owner(j, a.r, a.n)] + e0, (uint32_t)(sizeof(float) << T), bar);
     } else if (SK == TS_BUF) {
       mbar_expect_tx(bar, (uint32_t)(sizeof(float) << T));
-      bulk_load(st, (const float*)a.x + g0, (uint32_t)(sizeof(float) << T), bar);
+      bulk_load(st, (const float*)a.xw[w] + g0, (uint32_t)(sizeof(float) << T), bar);
     } else {
       const int lsh = a.dtype == OPTR_BF16 ? 1 : 2;
       int64_t valid = a.L - g0;
@@ -146,7 +148,7 @@ __device__ __forceinline__ void tile_issue(const TmaMaps& maps, const TmaArgs& a
       const uint32_t bytes = (uint32_t)((valid << lsh) & ~15LL);
       const uint32_t sbytes = (uint32_t)(sizeof(uint32_t) << (T - 5));
       mbar_expect_tx(bar, bytes + sbytes);
-      if (bytes) bulk_load(st, (const unsigned char*)a.x + (g0 << lsh), bytes, bar);
+      if (bytes) bulk_load(st, (const unsigned char*)a.xw[w] + (g0 << lsh), bytes, bar);
       bulk_load(st + (sizeof(float) << T), a.signs + (g0 >> 5), sbytes, bar);
     }
   }
@@ -154,29 +156,32 @@ __device__ __forceinline__ void tile_issue(const TmaMaps& maps, const TmaArgs& a
 
 // Masked float4 of worker q's stage-2 receive at global index g (4 entries
 // inside one shard).
-__device__ __forceinline__ float4 gather_mask4(const TmaArgs& a, int64_t g, float4 v) {
+__device__ __forceinline__ float4 gather_mask4(const TmaArgs& a, int q, uint8_t* got, int64_t g, float4 v) {
   const int j = (int)(g >> a.shard_shift);
   const int owner = shard_owner(j, a.r, a.n);
-  if (owner == a.q) {
-    if (a.got) *reinterpret_cast<uchar4*>(a.got + g) = make_uchar4(1, 1, 1, 1);
+  if (owner == q) {
+    if (got) *reinterpret_cast<uchar4*>(got + g) = make_uchar4(1, 1, 1, 1);
     return v;
   }
   const uint32_t e = (uint32_t)(g - ((int64_t)j << a.shard_shift));
-  const uint32_t kk = keep4(a.m.row(1, a.q, owner), e, a.m);
+  const uint32_t kk = keep4(a.m.row(1, q, owner), e, a.m);
   if (kk == 0xFu) {
-    if (a.got) *reinterpret_cast<uchar4*>(a.got + g) = make_uchar4(1, 1, 1, 1);
+    if (got) *reinterpret_cast<uchar4*>(got + g) = make_uchar4(1, 1, 1, 1);
     return v;
   }
   const bool k0 = kk & 1u, k1 = kk & 2u, k2 = kk & 4u, k3 = kk & 8u;
-  if (a.got) *reinterpret_cast<uchar4*>(a.got + g) = make_uchar4(k0, k1, k2, k3);
+  if (got) *reinterpret_cast<uchar4*>(got + g) = make_uchar4(k0, k1, k2, k3);
   return make_float4(k0 ? v.x : 0.f, k1 ? v.y : 0.f, k2 ? v.z : 0.f, k3 ? v.w : 0.f);
 }
 
 template <int T, int kStages, bool STRIDED, int SK, class Snk>
 __global__ void __launch_bounds__(1 << (T - 5)) tma_pass_kernel(const __grid_constant__ TmaMaps maps,
-                                                              const __grid_constant__ CUtensorMap dst,
+                                                              const __grid_constant__ TmaMaps dmaps,
                                                               const __grid_constant__ TmaArgs a,
-                                                              const __grid_constant__ Snk snk, int worker) {
+                                                              const __grid_constant__ Snk snk, int worker_base) {
+  const int worker = worker_base + blockIdx.y;
+  const CUtensorMap& dst = dmaps.m[worker];
+  uint8_t* const gotw = (SK == TS_GATHER && a.got) ? a.got + (int64_t)worker * a.dim : nullptr;
   constexpr int CB = STRIDED ? 3 : 0;
   constexpr RPlan P = make_rplan(T, CB);
   static_assert(P.nr == 3, "TMA pass expects three register rounds");
@@ -206,7 +211,7 @@ __global__ void __launch_bounds__(1 << (T - 5)) tma_pass_kernel(const __grid_con
   if (tid == 0) {
     for (int s = 0; s < kStages; ++s) {
       const int64_t ts = blockIdx.x + s * stride;
-      if (ts < a.ntiles) tile_issue<T, STRIDED, SK>(maps, a, ts, base + s * SB, &full[s]);
+      if (ts < a.ntiles) tile_issue<T, STRIDED, SK>(maps, a, worker, ts, base + s * SB, &full[s]);
     }
   }
   const int cgb = STRIDED ? a.lo - 3 : 0;
@@ -245,7 +250,7 @@ __global__ void __launch_bounds__(1 << (T - 5)) tma_pass_kernel(const __grid_con
           float e[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
           for (int c = 0; c < 4; ++c)
-            if (g + c < a.L) e[c] = load_elem(a.x, a.dtype, g + c);
+            if (g + c < a.L) e[c] = load_elem(a.xw[worker], a.dtype, g + c);
           q4 = make_float4(e[0], e[1], e[2], e[3]);
         }
         const uint32_t sw = reinterpret_cast<const uint32_t*>(sb + (sizeof(float) << T))[i >> 5] >> (i & 31);
@@ -255,7 +260,7 @@ __global__ void __launch_bounds__(1 << (T - 5)) tma_pass_kernel(const __grid_con
                          __int_as_float(__float_as_int(q4.w) ^ ((~sw & 8u) << 28)));
       } else {
         q4 = *reinterpret_cast<const float4*>(tile + i);
-        if constexpr (SK == TS_GATHER) q4 = gather_mask4(a, g, q4);
+        if constexpr (SK == TS_GATHER) q4 = gather_mask4(a, worker, gotw, g, q4);
       }
       v[4 * m] = q4.x;
       v[4 * m + 1] = q4.y;
@@ -281,7 +286,7 @@ __global__ void __launch_bounds__(1 << (T - 5)) tma_pass_kernel(const __grid_con
     __syncthreads();  // the swizzled tile has been read: the stage is free
     if constexpr (!STRIDED) {
       if (tid == 0 && t + kStages * stride < a.ntiles)
-        tile_issue<T, STRIDED, SK>(maps, a, t + kStages * stride, sb, &full[s]);
+        tile_issue<T, STRIDED, SK>(maps, a, worker, t + kStages * stride, sb, &full[s]);
       if constexpr (P.pos[2][0] == 0 && P.pos[2][1] == 1) {
 #pragma unroll
         for (int m = 0; m < 8; ++m)
@@ -338,7 +343,7 @@ __global__ void __launch_bounds__(1 << (T - 5)) tma_pass_kernel(const __grid_con
           bulk_wait_read1();
           const int64_t tn = t + (kStages - 1) * stride;
           const int sp = (k - 1) % kStages;
-          if (tn < a.ntiles) tile_issue<T, STRIDED, SK>(maps, a, tn, base + sp * SB, &full[sp]);
+          if (tn < a.ntiles) tile_issue<T, STRIDED, SK>(maps, a, worker, tn, base + sp * SB, &full[sp]);
         }
       }
     } else {
@@ -371,7 +376,7 @@ __global__ void __launch_bounds__(1 << (T - 5)) tma_pass_kernel(const __grid_con
           bulk_wait_read1();  // the store of tile k-1 has left its stage
           const int64_t tn = t + (kStages - 1) * stride;
           const int sp = (k - 1) % kStages;
-          if (tn < a.ntiles) tile_issue<T, STRIDED, SK>(maps, a, tn, base + sp * SB, &full[sp]);
+          if (tn < a.ntiles) tile_issue<T, STRIDED, SK>(maps, a, worker, tn, base + sp * SB, &full[sp]);
         }
       }
     }
