@@ -380,7 +380,9 @@ int launch_tma_aggregate(const AggArgs& ag, int nowners, int64_t smax, cudaStrea
   for (int i = 0; i < ag.n; ++i) {
     a.Y[i] = ag.Y[i];
     a.A[i] = ag.A[i];
+    a.G[i] = ag.G[i];
   }
+  a.push = ag.push;
   a.sh = ag.sh;
   a.n = ag.n;
   a.r = ag.r;
@@ -501,6 +503,16 @@ Pcg sign_pcg(uint64_t seed) { return pcg_from_u64s(&seed, 1); }
 // finishes into `out` with the decode epilogue.  One GPU: strided first,
 // gathering from the L2-resident aggregates, contiguous last into `out`.
 // OPTR_DEC_ORDER=strided|contig overrides.
+// OPTR_STAGE2=pull keeps the stage-2 pull inside the decode pass.
+bool stage2_push() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("OPTR_STAGE2");
+    v = (e && e[0] == 'p' && e[1] == 'u' && e[2] == 'l') ? 0 : 1;
+  }
+  return v == 1;
+}
+
 bool decode_contig_first(bool multi_gpu) {
   static int v = -2;
   if (v == -2) {
@@ -1012,7 +1024,7 @@ struct optr_comm_s {
   int64_t max_dim;
   // two parities of [Y | A] so consecutive calls can overlap; three flag
   // sets (one per parity, one for the public barrier)
-  size_t off_flags[3], off_y[2], off_a[2], sym_bytes;
+  size_t off_flags[3], off_y[2], off_a[2], off_g[2], sym_bytes;
   char* sym;
   char* peer[OPTR_MAX_WORKERS];
   bool opened[OPTR_MAX_WORKERS];
@@ -1056,6 +1068,8 @@ int optr_comm_create(optr_comm* out, int device, int rank, int n, int64_t max_le
     off = align_up(off + (size_t)c->max_dim * 4, 1024);
     c->off_a[p] = off;
     off = align_up(off + (size_t)smax * 4, 1024);
+    c->off_g[p] = off;  // stage-2 receive vector, written by every owner's push
+    off = align_up(off + (size_t)c->max_dim * 4, 1024);
   }
   c->sym_bytes = off;
   int64_t pw = mask_words(c->max_dim, n, 1);  // epp >= 1 bound
@@ -1224,9 +1238,11 @@ static int tar_enqueue(optr_comm c, const void* x, void* out, int64_t L, int dty
   unsigned long long* counts = (unsigned long long*)(loc + c->off_counts);
   float* Yp[kMaxW];
   float* Ap[kMaxW];
+  float* Gp[kMaxW];
   for (int i = 0; i < n; ++i) {
     Yp[i] = (float*)(c->peer[i] + c->off_y[par]);
     Ap[i] = (float*)(c->peer[i] + c->off_a[par]);
+    Gp[i] = (float*)(c->peer[i] + c->off_g[par]);
   }
   Shards sh = make_shards(dim, n);
 
@@ -1278,14 +1294,23 @@ static int tar_enqueue(optr_comm c, const void* x, void* out, int64_t L, int dty
   ag.r = r;
   ag.m = mv;
   ag.owner_base = me;
+  // Stage 2 fused into stage 1 (push): the owner writes its mean chunk into
+  // every rank's receive vector G while it pulls the next chunk, so the
+  // decode reads stage-2 data locally.  Needs the TMA aggregate.
+  const bool push = stage2_push() && agg_vec_ok(ag) && tma_enabled();
+  if (push) {
+    for (int i = 0; i < n; ++i) ag.G[i] = Gp[i];
+    ag.push = 1;
+  }
   int64_t smax = sh.base + (sh.extra ? 1 : 0);
   if ((rc = launch_aggregate(ag, 1, smax, st))) return rc;
   if ((rc = comm_barrier(c, par, st))) return rc;
 
-  // stage 2: pull every owner's aggregate over NVLink, fused into decode
+  // stage 2 receive fused into the first decode pass: from the local G
+  // (push) or pulled from every owner's aggregate over NVLink
   SrcGather ga;
   memset(&ga, 0, sizeof(ga));
-  for (int i = 0; i < n; ++i) ga.A[i] = Ap[i];
+  for (int i = 0; i < n; ++i) ga.A[i] = push ? Gp[me] + sh.off(owned_shard(i, r, n)) : Ap[i];
   ga.sh = sh;
   ga.n = n;
   ga.r = r;

@@ -826,6 +826,8 @@ __global__ void __launch_bounds__(256) smem_tile_kernel(PassGeom pg, int worker_
 struct AggArgs {
   const float* Y[kMaxW];  // wire vectors of every worker (peer-mapped in multi-GPU)
   float* A[kMaxW];        // aggregate shard of each owner
+  float* G[kMaxW];        // push mode (TMA aggregate only): every rank's receive vector
+  int push;
   Shards sh;
   int n, r;
   MaskView m;

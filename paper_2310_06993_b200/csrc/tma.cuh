@@ -400,6 +400,8 @@ namespace optr {
 struct TmaAggArgs {
   const float* Y[kMaxW];  // wire vector of each worker
   float* A[kMaxW];        // aggregate shard of each owner
+  float* G[kMaxW];        // push mode: every rank's stage-2 receive vector (peer-mapped)
+  int push;               // 1: write the mean into G[q] + off for every rank q (TAR stage 2 fused)
   Shards sh;
   int n, r, owner_base;
   MaskView m;
@@ -472,7 +474,18 @@ __global__ void __launch_bounds__(CH / 4) tma_agg_kernel(const __grid_constant__
     }
     __syncthreads();  // stage s has been read
     if (tid == 0 && c + 2 * stride < nchunks) issue(c + 2 * stride, s);
-    if (e + 4 <= len) st4(A + e, res);
+    if (e + 4 <= len) {
+      if (a.push) {
+        // stage 2 (collectives.py:133-137): the owner's mean goes to every rank
+#pragma unroll
+        for (int q = 0; q < (NW > 0 ? NW : kMaxW); ++q) {
+          if (NW == 0 && q >= n) break;
+          st4(a.G[q] + off + e, res);
+        }
+      } else {
+        st4(A + e, res);
+      }
+    }
   }
 }
 
