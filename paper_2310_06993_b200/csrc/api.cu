@@ -267,7 +267,7 @@ int tma_stages() {
   static int s = 0;
   if (!s) {
     const char* e = getenv("OPTR_TMA_STAGES");
-    s = (e && e[0] == '3') ? 3 : 2;
+    s = (e && e[0] == '3') ? 3 : ((e && e[0] == '1') ? 1 : 2);
   }
   return s;
 }
@@ -277,6 +277,8 @@ int launch_tma_pass(int cls, const TmaMaps& maps, const TmaMaps& dmaps, const Tm
                     int worker, int nworkers, cudaStream_t st) {
   if (tma_stages() == 3)
     return launch_tma_pass_s<T, 3, STRIDED, SK>(cls, maps, dmaps, a, snk, worker, nworkers, st);
+  if (tma_stages() == 1)
+    return launch_tma_pass_s<T, 1, STRIDED, SK>(cls, maps, dmaps, a, snk, worker, nworkers, st);
   return launch_tma_pass_s<T, 2, STRIDED, SK>(cls, maps, dmaps, a, snk, worker, nworkers, st);
 }
 

@@ -94,6 +94,7 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
 // XOR-linear swizzle: swzc(b | c) = swzc(b) ^ swzc(c) for disjoint b, c
@@ -339,7 +340,10 @@ __global__ void __launch_bounds__(1 << (T - 5)) tma_pass_kernel(const __grid_con
           if ((int64_t)b * a.box_rows < rows_full)
             tma_store_3d(&dst, sb + (size_t)b * a.box_rows * 8 * esz, c0, b * a.box_rows, 0);
         bulk_commit();
-        if (k >= 1) {
+        if constexpr (kStages == 1) {
+          bulk_wait_read0();
+          if (t + stride < a.ntiles) tile_issue<T, STRIDED, SK>(maps, a, worker, t + stride, base, &full[0]);
+        } else if (k >= 1) {
           bulk_wait_read1();
           const int64_t tn = t + (kStages - 1) * stride;
           const int sp = (k - 1) % kStages;
@@ -372,7 +376,10 @@ __global__ void __launch_bounds__(1 << (T - 5)) tma_pass_kernel(const __grid_con
         for (int b = 0; b < nbox; ++b)
           tma_store_3d(&dst, tile + (size_t)b * a.box_rows * 8, c0, b * a.box_rows, outer);
         bulk_commit();
-        if (k >= 1) {
+        if constexpr (kStages == 1) {
+          bulk_wait_read0();  // single stage: refill once this tile's store has left it
+          if (t + stride < a.ntiles) tile_issue<T, STRIDED, SK>(maps, a, worker, t + stride, base, &full[0]);
+        } else if (k >= 1) {
           bulk_wait_read1();  // the store of tile k-1 has left its stage
           const int64_t tn = t + (kStages - 1) * stride;
           const int sp = (k - 1) % kStages;
