@@ -102,6 +102,16 @@ int bind_device(void* stream) {
 constexpr int kContigBits = 13;
 constexpr int kColBits = 3;
 
+// OPTR_WIDE=0 keeps the 13+10 split with 32-byte strided rows at D = 2^23.
+bool wide_rows() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("OPTR_WIDE");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
 int plan_passes(int n, PassGeom* out, bool encode_order) {
   // A contiguous pass on 2^c-entry tiles plus strided passes of <= 11 row
   // bits on 2^ks x 8 tiles (T = ks + 3 <= 14: one CTA's registers).  Encode
@@ -112,6 +122,10 @@ int plan_passes(int n, PassGeom* out, bool encode_order) {
   int np = 0;
   if (n <= kContigBits) {
     p[np++] = PassGeom{0, n, 0, 1};
+  } else if (n == 23 && wide_rows()) {
+    // 16K-entry contiguous tiles + 512 x 32 strided tiles: 128-byte rows
+    p[np++] = PassGeom{0, 14, 0, 0};
+    p[np++] = PassGeom{14, 9, 5, 0};
   } else if (n <= kContigBits + 11) {
     p[np++] = PassGeom{0, kContigBits, 0, 0};
     p[np++] = PassGeom{kContigBits, n - kContigBits, kColBits, 0};
@@ -222,13 +236,13 @@ bool tma_enabled() {
   return g_tma_mode == 1;
 }
 
-// tensor [d2][d1][d0] (d0 contiguous) of fp32 / bf16, boxes of 8 x box1 x 1
+// tensor [d2][d1][d0] (d0 contiguous) of fp32 / bf16, boxes of box0 x box1 x 1
 bool make_map3(CUtensorMap* m, const void* base, uint64_t d0, uint64_t d1, uint64_t d2, uint32_t box1,
-               int dtype = OPTR_F32) {
+               int dtype = OPTR_F32, uint32_t box0 = 8) {
   const uint64_t esz = dtype == OPTR_BF16 ? 2 : 4;
   cuuint64_t dims[3] = {d0, d1, d2};
   cuuint64_t strides[2] = {d0 * esz, d0 * d1 * esz};
-  cuuint32_t box[3] = {8, box1, 1};
+  cuuint32_t box[3] = {box0, box1, 1};
   cuuint32_t es[3] = {1, 1, 1};
   CUresult r = g_encode_tiled(m, dtype == OPTR_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
                               3, const_cast<void*>(base), dims, strides, box,
@@ -238,11 +252,11 @@ bool make_map3(CUtensorMap* m, const void* base, uint64_t d0, uint64_t d1, uint6
   return r == CUDA_SUCCESS;
 }
 
-template <int T, int S, bool STRIDED, int SK, class Snk>
+template <int T, int S, bool STRIDED, int SK, class Snk, int CBW>
 int launch_tma_pass_s(int cls, const TmaMaps& maps, const TmaMaps& dmaps, const TmaArgs& a, const Snk& snk,
                       int worker, int nworkers, cudaStream_t st) {
   const size_t smem = tma_smem_bytes<T, S>();
-  auto kern = tma_pass_kernel<T, S, STRIDED, SK, Snk>;
+  auto kern = tma_pass_kernel<T, S, STRIDED, SK, Snk, CBW>;
   int rc = set_smem_attr(kern, smem);
   if (rc) return rc;
   static int nsm = 0;
@@ -272,14 +286,12 @@ int tma_stages() {
   return s;
 }
 
-template <int T, bool STRIDED, int SK, class Snk>
+template <int T, bool STRIDED, int SK, class Snk, int CBW = 3>
 int launch_tma_pass(int cls, const TmaMaps& maps, const TmaMaps& dmaps, const TmaArgs& a, const Snk& snk,
                     int worker, int nworkers, cudaStream_t st) {
-  if (tma_stages() == 3)
-    return launch_tma_pass_s<T, 3, STRIDED, SK>(cls, maps, dmaps, a, snk, worker, nworkers, st);
   if (tma_stages() == 1)
-    return launch_tma_pass_s<T, 1, STRIDED, SK>(cls, maps, dmaps, a, snk, worker, nworkers, st);
-  return launch_tma_pass_s<T, 2, STRIDED, SK>(cls, maps, dmaps, a, snk, worker, nworkers, st);
+    return launch_tma_pass_s<T, 1, STRIDED, SK, Snk, CBW>(cls, maps, dmaps, a, snk, worker, nworkers, st);
+  return launch_tma_pass_s<T, 2, STRIDED, SK, Snk, CBW>(cls, maps, dmaps, a, snk, worker, nworkers, st);
 }
 
 // A pass through the TMA ring kernel when the shapes allow it; -1 when the
@@ -314,11 +326,12 @@ int try_tma(int cls, const PassGeom& pg, int nlog, int worker, int nworkers, con
       a.got = src.got;
       a.dim = src.dim;
     }
-    if (pg.cb == 3) {  // strided: tensor boxes in, tensor boxes out
+    if (pg.cb == 3 || pg.cb == 5) {  // strided: tensor boxes in, tensor boxes out
       if constexpr (kEnc) {
         return -1;
       } else {
-        if (T < 12 || T > 14) return -1;
+        if (T < 12 || T > 14 || (pg.cb == 5 && T != 14)) return -1;
+        const uint32_t bw = 1u << pg.cb;
         const uint64_t d0 = 1ULL << pg.lo, d1 = 1ULL << pg.ks, d2 = 1ULL << (nlog - pg.lo - pg.ks);
         int box = (int)(d1 < 256 ? d1 : 256);
         if constexpr (kGather) {
@@ -326,25 +339,26 @@ int try_tma(int cls, const PassGeom& pg, int nlog, int worker, int nworkers, con
           const int64_t srows = 1LL << (src.pow2_shift - pg.lo);
           if (srows < box) box = (int)srows;
           for (int o = 0; o < src.n; ++o)
-            if (!make_map3(&maps.m[o], src.A[o], d0, (uint64_t)srows, 1, (uint32_t)box)) return -1;
+            if (!make_map3(&maps.m[o], src.A[o], d0, (uint64_t)srows, 1, (uint32_t)box, OPTR_F32, bw)) return -1;
         }
         for (int w = worker; w < worker + nworkers; ++w) {
           if constexpr (kBuf) {
-            if (!make_map3(&maps.m[w], src.y[w], d0, d1, d2, (uint32_t)box)) return -1;
+            if (!make_map3(&maps.m[w], src.y[w], d0, d1, d2, (uint32_t)box, OPTR_F32, bw)) return -1;
           }
           if constexpr (kSnkBuf) {
-            if (!make_map3(&dmaps.m[w], snk.y[w], d0, d1, d2, (uint32_t)box)) return -1;
+            if (!make_map3(&dmaps.m[w], snk.y[w], d0, d1, d2, (uint32_t)box, OPTR_F32, bw)) return -1;
           } else {  // decode epilogue: map over the full rows of `out`
             if (d2 != 1) return -1;
             const int64_t rows_full = snk.L >> pg.lo;
             if (rows_full > 0 &&
-                !make_map3(&dmaps.m[w], snk.out[w], d0, (uint64_t)rows_full, 1, (uint32_t)box, snk.dtype))
+                !make_map3(&dmaps.m[w], snk.out[w], d0, (uint64_t)rows_full, 1, (uint32_t)box, snk.dtype, bw))
               return -1;
             if (((uintptr_t)snk.out[w] & 15) || ((uintptr_t)snk.signs & 15)) return -1;
           }
         }
         if constexpr (kSnkBuf) a.scale = snk.scale;
         a.box_rows = box;
+        if (pg.cb == 5) return launch_tma_pass<14, true, SK, Snk, 5>(cls, maps, dmaps, a, snk, worker, nworkers, st);
         switch (T) {
           case 12: return launch_tma_pass<12, true, SK>(cls, maps, dmaps, a, snk, worker, nworkers, st);
           case 13: return launch_tma_pass<13, true, SK>(cls, maps, dmaps, a, snk, worker, nworkers, st);

@@ -110,19 +110,19 @@ __host__ __device__ constexpr size_t tma_smem_bytes() {
 }
 
 // Issue the loads of tile t into stage buffer `st` (sign words after the tile).
-template <int T, bool STRIDED, int SK>
+template <int T, bool STRIDED, int SK, int CBW>
 __device__ __forceinline__ void tile_issue(const TmaMaps& maps, const TmaArgs& a, int w, int64_t t,
                                            unsigned char* st, uint64_t* bar) {
   if constexpr (STRIDED) {
-    constexpr int KS = T - 3;
-    const int cgb = a.lo - 3;
-    const int c0 = (int)((t & ((1LL << cgb) - 1)) << 3);
+    constexpr int KS = T - CBW;
+    const int cgb = a.lo - CBW;
+    const int c0 = (int)((t & ((1LL << cgb) - 1)) << CBW);
     const int outer = (int)(t >> cgb);
     const int nbox = (1 << KS) / a.box_rows;
     mbar_expect_tx(bar, (uint32_t)(sizeof(float) << T));
     for (int b = 0; b < nbox; ++b) {
       const int row = b * a.box_rows;
-      float* dst = (float*)st + (size_t)row * 8;
+      float* dst = (float*)st + ((size_t)row << CBW);
       if (SK == TS_GATHER) {
         const int rsh = a.shard_shift - a.lo;  // rows per shard = 2^rsh (outer == 0)
         const int j = row >> rsh;
@@ -175,7 +175,7 @@ __device__ __forceinline__ float4 gather_mask4(const TmaArgs& a, int q, uint8_t*
   return make_float4(k0 ? v.x : 0.f, k1 ? v.y : 0.f, k2 ? v.z : 0.f, k3 ? v.w : 0.f);
 }
 
-template <int T, int kStages, bool STRIDED, int SK, class Snk>
+template <int T, int kStages, bool STRIDED, int SK, class Snk, int CBW>
 __global__ void __launch_bounds__(1 << (T - 5)) tma_pass_kernel(const __grid_constant__ TmaMaps maps,
                                                               const __grid_constant__ TmaMaps dmaps,
                                                               const __grid_constant__ TmaArgs a,
@@ -183,7 +183,8 @@ __global__ void __launch_bounds__(1 << (T - 5)) tma_pass_kernel(const __grid_con
   const int worker = worker_base + blockIdx.y;
   const CUtensorMap& dst = dmaps.m[worker];
   uint8_t* const gotw = (SK == TS_GATHER && a.got) ? a.got + (int64_t)worker * a.dim : nullptr;
-  constexpr int CB = STRIDED ? 3 : 0;
+  constexpr int CB = STRIDED ? CBW : 0;  // untransformed column bits (8 or 32 columns)
+  constexpr int CM = (1 << CB) - 1;
   constexpr RPlan P = make_rplan(T, CB);
   static_assert(P.nr == 3, "TMA pass expects three register rounds");
   static_assert(P.pos[0][0] == 0 && P.pos[0][1] == 1, "round A holds float4 groups");
@@ -212,10 +213,10 @@ __global__ void __launch_bounds__(1 << (T - 5)) tma_pass_kernel(const __grid_con
   if (tid == 0) {
     for (int s = 0; s < kStages; ++s) {
       const int64_t ts = blockIdx.x + s * stride;
-      if (ts < a.ntiles) tile_issue<T, STRIDED, SK>(maps, a, worker, ts, base + s * SB, &full[s]);
+      if (ts < a.ntiles) tile_issue<T, STRIDED, SK, CBW>(maps, a, worker, ts, base + s * SB, &full[s]);
     }
   }
-  const int cgb = STRIDED ? a.lo - 3 : 0;
+  const int cgb = STRIDED ? a.lo - CB : 0;
   int k = 0;
   for (int64_t t = blockIdx.x; t < a.ntiles; t += stride, ++k) {
     const int s = k % kStages;
@@ -223,7 +224,7 @@ __global__ void __launch_bounds__(1 << (T - 5)) tma_pass_kernel(const __grid_con
     float* const tile = (float*)sb;
     mbar_wait(&full[s], (uint32_t)((k / kStages) & 1));
     // global index of tile element 0
-    const int64_t g0 = STRIDED ? (((t >> cgb) << (a.lo + T - 3)) + ((t & ((1LL << cgb) - 1)) << 3)) : (t << T);
+    const int64_t g0 = STRIDED ? (((t >> cgb) << (a.lo + T - CB)) + ((t & ((1LL << cgb) - 1)) << CB)) : (t << T);
     float v[32];
     // ---- round A: dense tile, float4 groups, fused source transform
     int64_t bulk_end = 0;
@@ -236,7 +237,7 @@ __global__ void __launch_bounds__(1 << (T - 5)) tma_pass_kernel(const __grid_con
 #pragma unroll
     for (int m = 0; m < 8; ++m) {
       const int i = b0 + roff(P, 0, 4 * m);
-      const int64_t g = STRIDED ? (g0 + ((int64_t)(i >> 3) << a.lo) + (i & 7)) : (g0 + i);
+      const int64_t g = STRIDED ? (g0 + ((int64_t)(i >> CB) << a.lo) + (i & CM)) : (g0 + i);
       float4 q4;
       if constexpr (SK == TS_ENC) {
         if (a.dtype == OPTR_BF16) {
@@ -287,7 +288,7 @@ __global__ void __launch_bounds__(1 << (T - 5)) tma_pass_kernel(const __grid_con
     __syncthreads();  // the swizzled tile has been read: the stage is free
     if constexpr (!STRIDED) {
       if (tid == 0 && t + kStages * stride < a.ntiles)
-        tile_issue<T, STRIDED, SK>(maps, a, worker, t + kStages * stride, sb, &full[s]);
+        tile_issue<T, STRIDED, SK, CBW>(maps, a, worker, t + kStages * stride, sb, &full[s]);
       if constexpr (P.pos[2][0] == 0 && P.pos[2][1] == 1) {
 #pragma unroll
         for (int m = 0; m < 8; ++m)
@@ -307,7 +308,7 @@ __global__ void __launch_bounds__(1 << (T - 5)) tma_pass_kernel(const __grid_con
 #pragma unroll
       for (int m = 0; m < 8; ++m) {
         const int i = b2 + roff(P, 2, 4 * m);
-        const int64_t g = g0 + ((int64_t)(i >> 3) << a.lo) + (i & 7);
+        const int64_t g = g0 + ((int64_t)(i >> CB) << a.lo) + (i & CM);
         const uint32_t w = __ldg(d.signs + (g >> 5)) >> (g & 31);
         float4 o4 = make_float4(v[4 * m] * d.scale, v[4 * m + 1] * d.scale, v[4 * m + 2] * d.scale,
                                 v[4 * m + 3] * d.scale);
@@ -315,7 +316,7 @@ __global__ void __launch_bounds__(1 << (T - 5)) tma_pass_kernel(const __grid_con
                          __int_as_float(__float_as_int(o4.y) ^ ((~w & 2u) << 30)),
                          __int_as_float(__float_as_int(o4.z) ^ ((~w & 4u) << 29)),
                          __int_as_float(__float_as_int(o4.w) ^ ((~w & 8u) << 28)));
-        if ((i >> 3) >= rows_full) {  // partial last row / padding rows
+        if ((i >> CB) >= rows_full) {  // partial last row / padding rows
           const float r4[4] = {o4.x, o4.y, o4.z, o4.w};
           for (int c = 0; c < 4; ++c)
             if (g + c < d.L) store_elem(d.out, d.dtype, g + c, r4[c]);
@@ -333,21 +334,21 @@ __global__ void __launch_bounds__(1 << (T - 5)) tma_pass_kernel(const __grid_con
       fence_async_smem();
       __syncthreads();
       if (tid == 0) {
-        const int c0 = (int)((t & ((1LL << cgb) - 1)) << 3);
-        const int nbox = (1 << (T - 3)) / a.box_rows;
+        const int c0 = (int)((t & ((1LL << cgb) - 1)) << CB);
+        const int nbox = (1 << (T - CB)) / a.box_rows;
         const int esz = d.dtype == OPTR_BF16 ? 2 : 4;
         for (int b = 0; b < nbox; ++b)
           if ((int64_t)b * a.box_rows < rows_full)
-            tma_store_3d(&dst, sb + (size_t)b * a.box_rows * 8 * esz, c0, b * a.box_rows, 0);
+            tma_store_3d(&dst, sb + ((size_t)b * a.box_rows << CB) * esz, c0, b * a.box_rows, 0);
         bulk_commit();
         if constexpr (kStages == 1) {
           bulk_wait_read0();
-          if (t + stride < a.ntiles) tile_issue<T, STRIDED, SK>(maps, a, worker, t + stride, base, &full[0]);
+          if (t + stride < a.ntiles) tile_issue<T, STRIDED, SK, CBW>(maps, a, worker, t + stride, base, &full[0]);
         } else if (k >= 1) {
           bulk_wait_read1();
           const int64_t tn = t + (kStages - 1) * stride;
           const int sp = (k - 1) % kStages;
-          if (tn < a.ntiles) tile_issue<T, STRIDED, SK>(maps, a, worker, tn, base + sp * SB, &full[sp]);
+          if (tn < a.ntiles) tile_issue<T, STRIDED, SK, CBW>(maps, a, worker, tn, base + sp * SB, &full[sp]);
         }
       }
     } else {
@@ -370,20 +371,20 @@ __global__ void __launch_bounds__(1 << (T - 5)) tma_pass_kernel(const __grid_con
       fence_async_smem();
       __syncthreads();
       if (tid == 0) {
-        const int c0 = (int)((t & ((1LL << cgb) - 1)) << 3);
+        const int c0 = (int)((t & ((1LL << cgb) - 1)) << CB);
         const int outer = SK == TS_GATHER ? 0 : (int)(t >> cgb);
-        const int nbox = (1 << (T - 3)) / a.box_rows;
+        const int nbox = (1 << (T - CB)) / a.box_rows;
         for (int b = 0; b < nbox; ++b)
-          tma_store_3d(&dst, tile + (size_t)b * a.box_rows * 8, c0, b * a.box_rows, outer);
+          tma_store_3d(&dst, tile + ((size_t)b * a.box_rows << CB), c0, b * a.box_rows, outer);
         bulk_commit();
         if constexpr (kStages == 1) {
           bulk_wait_read0();  // single stage: refill once this tile's store has left it
-          if (t + stride < a.ntiles) tile_issue<T, STRIDED, SK>(maps, a, worker, t + stride, base, &full[0]);
+          if (t + stride < a.ntiles) tile_issue<T, STRIDED, SK, CBW>(maps, a, worker, t + stride, base, &full[0]);
         } else if (k >= 1) {
           bulk_wait_read1();  // the store of tile k-1 has left its stage
           const int64_t tn = t + (kStages - 1) * stride;
           const int sp = (k - 1) % kStages;
-          if (tn < a.ntiles) tile_issue<T, STRIDED, SK>(maps, a, worker, tn, base + sp * SB, &full[sp]);
+          if (tn < a.ntiles) tile_issue<T, STRIDED, SK, CBW>(maps, a, worker, tn, base + sp * SB, &full[sp]);
         }
       }
     }
