@@ -102,12 +102,14 @@ int bind_device(void* stream) {
 constexpr int kContigBits = 13;
 constexpr int kColBits = 3;
 
-// OPTR_WIDE=0 keeps the 13+10 split with 32-byte strided rows at D = 2^23.
+// OPTR_WIDE=1 uses a 14+9 split with 128-byte strided rows at D = 2^23
+// (fewer TMA requests, but 16K-entry tiles fit one CTA per SM: measured
+// slower than the default 13+10 split with three CTAs per SM).
 bool wide_rows() {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("OPTR_WIDE");
-    v = (e && e[0] == '0') ? 0 : 1;
+    v = (e && e[0] == '1') ? 1 : 0;
   }
   return v == 1;
 }

@@ -649,18 +649,40 @@ __device__ __forceinline__ int thread_base(const RPlan& p, int r, int tid) {
   return o;
 }
 
+// Packed fp32x2 add/sub (sm_100a FADD2): two butterflies per instruction.
+__device__ __forceinline__ void add_sub2(float& a0, float& a1, float& b0, float& b1) {
+  float s0, s1, d0, d1;
+  asm("{.reg .b64 ra, rb, rs, rd;\n"
+      " mov.b64 ra, {%4, %5};\n mov.b64 rb, {%6, %7};\n"
+      " add.rn.f32x2 rs, ra, rb;\n sub.rn.f32x2 rd, ra, rb;\n"
+      " mov.b64 {%0, %1}, rs;\n mov.b64 {%2, %3}, rd;}"
+      : "=f"(s0), "=f"(s1), "=f"(d0), "=f"(d1)
+      : "f"(a0), "f"(a1), "f"(b0), "f"(b1));
+  a0 = s0;
+  a1 = s1;
+  b0 = d0;
+  b1 = d1;
+}
+
+// Butterfly stages over the register-index bits set in XM.  Registers pair
+// up as (2m, 2m+1); stages over bits 1..4 run as packed FADD2 on pairs, the
+// stage over bit 0 (inside a pair) as scalar FADDs.
 template <unsigned XM>
 __device__ __forceinline__ void bfly32(float (&v)[32]) {
+  if constexpr ((XM & 1u) != 0) {
 #pragma unroll
-  for (int k = 0; k < 5; ++k) {
+    for (int j = 0; j < 32; j += 2) {
+      const float a = v[j], b = v[j + 1];
+      v[j] = a + b;
+      v[j + 1] = a - b;
+    }
+  }
+#pragma unroll
+  for (int k = 1; k < 5; ++k) {
     if ((XM >> k) & 1u) {
 #pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        if (((j >> k) & 1) == 0) {
-          float a = v[j], b = v[j | (1 << k)];
-          v[j] = a + b;
-          v[j | (1 << k)] = a - b;
-        }
+      for (int j = 0; j < 32; j += 2) {
+        if (((j >> k) & 1) == 0) add_sub2(v[j], v[j + 1], v[j | (1 << k)], v[(j | (1 << k)) + 1]);
       }
     }
   }
