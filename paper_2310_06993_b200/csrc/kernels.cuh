@@ -433,6 +433,12 @@ struct SrcGather {
           const int owner = shard_owner(j, p->r, p->n);
           return load4_in(p->A[owner], owner == q ? nullptr : p->m.row(1, q, owner), e, g);
         }
+      } else {  // general ceil split: one shard lookup per group
+        const int j = p->sh.of(g);
+        const int64_t e = g - p->sh.off(j);
+        const int owner = shard_owner(j, p->r, p->n);
+        if ((e & 3) == 0 && e + 4 <= p->sh.len(j) && (((uintptr_t)p->A[owner]) & 15) == 0)
+          return load4_in(p->A[owner], owner == q ? nullptr : p->m.row(1, q, owner), (uint32_t)e, g);
       }
       return make_float4(load1(g), load1(g + 1), load1(g + 2), load1(g + 3));
     }
@@ -945,8 +951,24 @@ struct AsmArgs {
 __global__ void __launch_bounds__(256) assemble_kernel(const __grid_constant__ AsmArgs a) {
   const int q = a.worker_base + blockIdx.y;
   auto s = a.gather.bind(q);
-  for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < a.L; g += (int64_t)gridDim.x * blockDim.x)
-    store_elem(a.out[q], a.dtype, g, s.load1(g));
+  void* const out = a.out[q];
+  // float4 groups (fast path inside equal power-of-two shards), scalar tail
+  const int64_t n4 = a.L >> 2;
+  for (int64_t g4 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g4 < n4; g4 += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t g = g4 * 4;
+    const float4 v = s.load4(g);
+    if (a.dtype == OPTR_F32 && (((uintptr_t)out) & 15) == 0) {
+      st4((float*)out + g, v);
+    } else {
+      store_elem(out, a.dtype, g, v.x);
+      store_elem(out, a.dtype, g + 1, v.y);
+      store_elem(out, a.dtype, g + 2, v.z);
+      store_elem(out, a.dtype, g + 3, v.w);
+    }
+  }
+  for (int64_t g = n4 * 4 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < a.L;
+       g += (int64_t)gridDim.x * blockDim.x)
+    store_elem(out, a.dtype, g, s.load1(g));
 }
 
 // fp32/bf16 -> fp32 copy (RHT off: the wire carries float32, runner.py:228)
