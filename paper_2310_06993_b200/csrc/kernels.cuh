@@ -371,6 +371,18 @@ struct SrcMasked {
   __device__ __forceinline__ B bind(int) const { return B{y, mask}; }
 };
 
+// received flags of 4 consecutive entries (the row base q*dim may be odd)
+__device__ __forceinline__ void put_got(uint8_t* p, bool a, bool b, bool c, bool d) {
+  if ((((uintptr_t)p) & 3) == 0) {
+    *reinterpret_cast<uchar4*>(p) = make_uchar4(a, b, c, d);
+  } else {
+    p[0] = a;
+    p[1] = b;
+    p[2] = c;
+    p[3] = d;
+  }
+}
+
 // TAR stage-2 receive of worker q (collectives.py:140-150): own shard from
 // its own aggregate, peer shards from the owner's aggregate (peer-mapped in
 // the multi-GPU path) under the stage-2 mask, zero-filled misses.
@@ -418,9 +430,9 @@ struct SrcGather {
         v.y = k1 ? v.y : 0.f;
         v.z = k2 ? v.z : 0.f;
         v.w = k3 ? v.w : 0.f;
-        if (p->got) *reinterpret_cast<uchar4*>(p->got + (int64_t)q * p->dim + g) = make_uchar4(k0, k1, k2, k3);
+        if (p->got) put_got(p->got + (int64_t)q * p->dim + g, k0, k1, k2, k3);
       } else if (p->got) {
-        *reinterpret_cast<uchar4*>(p->got + (int64_t)q * p->dim + g) = make_uchar4(1, 1, 1, 1);
+        put_got(p->got + (int64_t)q * p->dim + g, true, true, true, true);
       }
       return v;
     }
