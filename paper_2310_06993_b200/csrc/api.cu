@@ -332,7 +332,7 @@ int try_tma(int cls, const PassGeom& pg, int nlog, int worker, int nworkers, con
       if constexpr (kEnc) {
         return -1;
       } else {
-        if (T < 12 || T > 14 || (pg.cb == 5 && T != 14)) return -1;
+        if (T < 9 || T > 14 || (pg.cb == 5 && T != 14)) return -1;
         const uint32_t bw = 1u << pg.cb;
         const uint64_t d0 = 1ULL << pg.lo, d1 = 1ULL << pg.ks, d2 = 1ULL << (nlog - pg.lo - pg.ks);
         int box = (int)(d1 < 256 ? d1 : 256);
@@ -361,6 +361,16 @@ int try_tma(int cls, const PassGeom& pg, int nlog, int worker, int nworkers, con
         if constexpr (kSnkBuf) a.scale = snk.scale;
         a.box_rows = box;
         if (pg.cb == 5) return launch_tma_pass<14, true, SK, Snk, 5>(cls, maps, dmaps, a, snk, worker, nworkers, st);
+        if constexpr (kSnkBuf) {  // small strided tiles (3-pass plans of D >= 2^26)
+          switch (T) {
+            case 9: return launch_tma_pass<9, true, SK>(cls, maps, dmaps, a, snk, worker, nworkers, st);
+            case 10: return launch_tma_pass<10, true, SK>(cls, maps, dmaps, a, snk, worker, nworkers, st);
+            case 11: return launch_tma_pass<11, true, SK>(cls, maps, dmaps, a, snk, worker, nworkers, st);
+            default: break;
+          }
+        } else {
+          if (T < 12) return -1;  // the decode epilogue needs float4 groups in the last round
+        }
         switch (T) {
           case 12: return launch_tma_pass<12, true, SK>(cls, maps, dmaps, a, snk, worker, nworkers, st);
           case 13: return launch_tma_pass<13, true, SK>(cls, maps, dmaps, a, snk, worker, nworkers, st);

@@ -186,9 +186,10 @@ __global__ void __launch_bounds__(1 << (T - 5)) tma_pass_kernel(const __grid_con
   constexpr int CB = STRIDED ? CBW : 0;  // untransformed column bits (8 or 32 columns)
   constexpr int CM = (1 << CB) - 1;
   constexpr RPlan P = make_rplan(T, CB);
-  static_assert(P.nr == 3, "TMA pass expects three register rounds");
+  static_assert(P.nr == 2 || P.nr == 3, "TMA pass expects two or three register rounds");
+  constexpr int LR = P.nr - 1;  // last round
   static_assert(P.pos[0][0] == 0 && P.pos[0][1] == 1, "round A holds float4 groups");
-  static_assert(!STRIDED || !std::is_same<Snk, SnkDecode>::value || (P.pos[2][0] == 0 && P.pos[2][1] == 1),
+  static_assert(!STRIDED || !std::is_same<Snk, SnkDecode>::value || (P.pos[LR][0] == 0 && P.pos[LR][1] == 1),
                 "decode epilogue stores float4 groups");
   static_assert(sizeof(float) * pad(1 << T) <= tma_stage_bytes<T>(), "padded tile fits the stage");
   constexpr size_t SB = tma_stage_bytes<T>();
@@ -200,7 +201,7 @@ __global__ void __launch_bounds__(1 << (T - 5)) tma_pass_kernel(const __grid_con
   const int tid = threadIdx.x;
   const int b0 = thread_base<T>(P, 0, tid);
   const int b1 = thread_base<T>(P, 1, tid);
-  const int b2 = thread_base<T>(P, 2, tid);
+  const int b2 = thread_base<T>(P, LR, tid);  // last-round base
   const int p0 = pad(b0), p1 = pad(b1), p2 = pad(b2);
   const auto d = snk.bind(worker);
 
@@ -279,26 +280,28 @@ __global__ void __launch_bounds__(1 << (T - 5)) tma_pass_kernel(const __grid_con
 #pragma unroll
     for (int j = 0; j < 32; ++j) v[j] = tile[p1 + pad(roff(P, 1, j))];
     bfly32<P.xm[1]>(v);
+    if constexpr (P.nr == 3) {
 #pragma unroll
-    for (int j = 0; j < 32; ++j) tile[p1 + pad(roff(P, 1, j))] = v[j];
-    __syncthreads();
+      for (int j = 0; j < 32; ++j) tile[p1 + pad(roff(P, 1, j))] = v[j];
+      __syncthreads();
 #pragma unroll
-    for (int j = 0; j < 32; ++j) v[j] = tile[p2 + pad(roff(P, 2, j))];
-    bfly32<P.xm[2]>(v);
-    __syncthreads();  // the swizzled tile has been read: the stage is free
+      for (int j = 0; j < 32; ++j) v[j] = tile[p2 + pad(roff(P, 2, j))];
+      bfly32<P.xm[2]>(v);
+    }
+    __syncthreads();  // the padded tile has been read: the stage is free
     if constexpr (!STRIDED) {
       if (tid == 0 && t + kStages * stride < a.ntiles)
         tile_issue<T, STRIDED, SK, CBW>(maps, a, worker, t + kStages * stride, sb, &full[s]);
-      if constexpr (P.pos[2][0] == 0 && P.pos[2][1] == 1) {
+      if constexpr (P.pos[LR][0] == 0 && P.pos[LR][1] == 1) {
 #pragma unroll
         for (int m = 0; m < 8; ++m)
-          d.store4(g0 + b2 + roff(P, 2, 4 * m), make_float4(v[4 * m], v[4 * m + 1], v[4 * m + 2], v[4 * m + 3]));
-      } else if constexpr (P.pos[2][0] == 0) {
+          d.store4(g0 + b2 + roff(P, LR, 4 * m), make_float4(v[4 * m], v[4 * m + 1], v[4 * m + 2], v[4 * m + 3]));
+      } else if constexpr (P.pos[LR][0] == 0) {
 #pragma unroll
-        for (int m = 0; m < 16; ++m) d.store2(g0 + b2 + roff(P, 2, 2 * m), v[2 * m], v[2 * m + 1]);
+        for (int m = 0; m < 16; ++m) d.store2(g0 + b2 + roff(P, LR, 2 * m), v[2 * m], v[2 * m + 1]);
       } else {
 #pragma unroll
-        for (int j = 0; j < 32; ++j) d.store1(g0 + b2 + roff(P, 2, j), v[j]);
+        for (int j = 0; j < 32; ++j) d.store1(g0 + b2 + roff(P, LR, j), v[j]);
       }
     } else if constexpr (std::is_same<Snk, SnkDecode>::value) {
       // decode epilogue (hadamard.py:119-123, runner.py:253-256): scale,
@@ -307,7 +310,7 @@ __global__ void __launch_bounds__(1 << (T - 5)) tma_pass_kernel(const __grid_con
       const int64_t rows_full = d.L >> a.lo;
 #pragma unroll
       for (int m = 0; m < 8; ++m) {
-        const int i = b2 + roff(P, 2, 4 * m);
+        const int i = b2 + roff(P, LR, 4 * m);
         const int64_t g = g0 + ((int64_t)(i >> CB) << a.lo) + (i & CM);
         const uint32_t w = __ldg(d.signs + (g >> 5)) >> (g & 31);
         float4 o4 = make_float4(v[4 * m] * d.scale, v[4 * m + 1] * d.scale, v[4 * m + 2] * d.scale,
@@ -355,18 +358,18 @@ __global__ void __launch_bounds__(1 << (T - 5)) tma_pass_kernel(const __grid_con
       // dense result -> TMA tensor store; the previous stage is refilled once
       // its own store has finished reading shared memory
       const float sc = a.scale;
-      if constexpr (P.pos[2][0] == 0 && P.pos[2][1] == 1) {
+      if constexpr (P.pos[LR][0] == 0 && P.pos[LR][1] == 1) {
 #pragma unroll
         for (int m = 0; m < 8; ++m)
-          *reinterpret_cast<float4*>(tile + b2 + roff(P, 2, 4 * m)) =
+          *reinterpret_cast<float4*>(tile + b2 + roff(P, LR, 4 * m)) =
               make_float4(v[4 * m] * sc, v[4 * m + 1] * sc, v[4 * m + 2] * sc, v[4 * m + 3] * sc);
-      } else if constexpr (P.pos[2][0] == 0) {
+      } else if constexpr (P.pos[LR][0] == 0) {
 #pragma unroll
         for (int m = 0; m < 16; ++m)
-          *reinterpret_cast<float2*>(tile + b2 + roff(P, 2, 2 * m)) = make_float2(v[2 * m] * sc, v[2 * m + 1] * sc);
+          *reinterpret_cast<float2*>(tile + b2 + roff(P, LR, 2 * m)) = make_float2(v[2 * m] * sc, v[2 * m + 1] * sc);
       } else {
 #pragma unroll
-        for (int j = 0; j < 32; ++j) tile[b2 + roff(P, 2, j)] = v[j] * sc;
+        for (int j = 0; j < 32; ++j) tile[b2 + roff(P, LR, j)] = v[j] * sc;
       }
       fence_async_smem();
       __syncthreads();
