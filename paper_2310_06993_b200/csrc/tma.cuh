@@ -100,9 +100,11 @@ __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.a
 // XOR-linear swizzle: swzc(b | c) = swzc(b) ^ swzc(c) for disjoint b, c
 __host__ __device__ constexpr int swzc(int i) { return i ^ ((i >> 5) & 31); }
 
+// tile + its sign words, rounded to 1 KB so every stage (a TMA destination)
+// stays 128-byte aligned
 template <int T>
 __host__ __device__ constexpr size_t tma_stage_bytes() {
-  return (sizeof(float) << T) + (sizeof(uint32_t) << (T - 5));  // tile + its sign words
+  return ((sizeof(float) << T) + (sizeof(uint32_t) << (T - 5)) + 1023) / 1024 * 1024;
 }
 template <int T, int S>
 __host__ __device__ constexpr size_t tma_smem_bytes() {
