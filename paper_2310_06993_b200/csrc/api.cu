@@ -219,6 +219,35 @@ int launch_smem(int cls, const PassGeom& pg, int worker_base, int nworkers, cons
 }
 
 
+
+// Launch with programmatic stream serialization (PDL) so the kernel is
+// scheduled while its predecessor drains; the kernels call
+// griddepcontrol.wait before touching dependent memory.  OPTR_PDL=0 disables.
+bool pdl_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("OPTR_PDL");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
+template <class K, class... Args>
+cudaError_t launch_ex(K kernel, dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg;
+  memset(&cfg, 0, sizeof(cfg));
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() && !g_timing ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, args...);
+}
+
 // ------------------------------------------------------------ TMA strided
 PFN_cuTensorMapEncodeTiled_v12000 g_encode_tiled = nullptr;
 int g_tma_mode = -1;  // -1 unknown, 0 off, 1 on
@@ -273,7 +302,7 @@ int launch_tma_pass_s(int cls, const TmaMaps& maps, const TmaMaps& dmaps, const 
   int64_t gx = ((int64_t)nsm * per_sm + nworkers - 1) / nworkers;
   if (gx > a.ntiles) gx = a.ntiles;
   KScope ks(cls, st, nworkers);
-  kern<<<dim3((unsigned)gx, (unsigned)nworkers), 1 << (T - 5), smem, st>>>(maps, dmaps, a, snk, worker);
+  launch_ex(kern, dim3((unsigned)gx, (unsigned)nworkers), dim3(1 << (T - 5)), smem, st, maps, dmaps, a, snk, worker);
   return launch_check(kern, STRIDED ? "tma_strided" : "tma_contig", T, STRIDED ? 3 : 0, (int)gx, nworkers,
                       1 << (T - 5), smem);
 }
@@ -438,7 +467,7 @@ int launch_tma_aggregate(const AggArgs& ag, int nowners, int64_t smax, cudaStrea
   if (gx < 1) gx = 1;
   if (gx > nchunks) gx = nchunks;
   KScope ks(OPTR_K_AGG, st, nowners);
-  kern<<<dim3((unsigned)gx, (unsigned)nowners), kAggChunk / 4, smem, st>>>(a);
+  launch_ex(kern, dim3((unsigned)gx, (unsigned)nowners), dim3(kAggChunk / 4), smem, st, a);
   return launch_check(kern, "tma_aggregate", 0, 0, (int)gx, nowners, kAggChunk / 4, smem);
 }
 

@@ -212,6 +212,11 @@ __global__ void __launch_bounds__(1 << (T - 5)) tma_pass_kernel(const __grid_con
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
+  // programmatic dependent launch: let the next kernel in the stream get
+  // scheduled now, and wait here until the previous one's memory is visible
+  // (both are no-ops for a normal launch)
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   const int64_t stride = gridDim.x;
   if (tid == 0) {
     for (int s = 0; s < kStages; ++s) {
@@ -444,6 +449,11 @@ __global__ void __launch_bounds__(CH / 4) tma_agg_kernel(const __grid_constant__
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
+  // programmatic dependent launch: let the next kernel in the stream get
+  // scheduled now, and wait here until the previous one's memory is visible
+  // (both are no-ops for a normal launch)
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   auto issue = [&](int64_t c, int s) {
     const int64_t e0 = c * CH;
     int64_t cnt = len - e0;
