@@ -216,7 +216,7 @@ def run_ours(args):
     import torch
 
     from paper_2310_06993_b200 import _lib
-    from paper_2310_06993_b200.collectives import MaskSpec, tar_allreduce_local
+    from paper_2310_06993_b200.collectives import MaskSpec, local_join, tar_allreduce_local
 
     total, per, dt_name, desc = WORKLOADS[args.workload]
     dtype = torch.bfloat16 if dt_name == "bf16" else torch.float32
@@ -262,9 +262,11 @@ def run_ours(args):
                                generation=gen, bucket_id=b, masks=masks, async_op=True)
             else:
                 tar_allreduce_local((src or grads)[b], rotation=r, ht=ht, job_seed=7, generation=gen,
-                                    bucket_id=b, masks=masks, out=(dst or outs)[b])
+                                    bucket_id=b, masks=masks, out=(dst or outs)[b], async_op=True)
         if multi:
             comm.join()
+        else:
+            local_join()
         state["gen"] += 1
 
     def barrier():

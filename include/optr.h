@@ -123,6 +123,19 @@ int optr_tar_local(const void* const* x, void* const* out, int n, int64_t L,
                    size_t workspace_bytes, uint64_t* received_out, uint8_t* got_out,
                    void* stream);
 
+/* Same as optr_tar_local but the caller's stream does not wait: the call
+ * runs on the library's work stream of `slot` (0 or 1) after the caller's
+ * prior work, so two consecutive buckets overlap.  Calls on the same slot
+ * run in order; x, out, workspace and the outputs of a slot must stay
+ * untouched until optr_local_join. */
+int optr_tar_local_async(const void* const* x, void* const* out, int n, int64_t L,
+                         int dtype_in, int dtype_out, uint64_t job_seed, uint64_t bucket_id,
+                         uint64_t generation, int rotation, int ht, const optr_mask_spec* masks,
+                         void* workspace, size_t workspace_bytes, uint64_t* received_out,
+                         uint8_t* got_out, int slot, void* stream);
+/* Make `stream` wait for every optr_tar_local_async call issued so far. */
+int optr_local_join(void* stream);
+
 /* --------------------------------------- TAR+RHT, one worker per GPU (IPC) */
 typedef struct optr_comm_s* optr_comm;
 

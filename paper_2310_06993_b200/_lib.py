@@ -63,6 +63,10 @@ SIGNATURES = {
     "optr_tar_local": (_int, [ctypes.POINTER(_vp), ctypes.POINTER(_vp), _int, _i64, _int, _int, _u64,
                               _u64, _u64, _int, _int, ctypes.POINTER(optr_mask_spec), _vp,
                               ctypes.c_size_t, _vp, _vp, _vp]),
+    "optr_tar_local_async": (_int, [ctypes.POINTER(_vp), ctypes.POINTER(_vp), _int, _i64, _int, _int, _u64,
+                                    _u64, _u64, _int, _int, ctypes.POINTER(optr_mask_spec), _vp,
+                                    ctypes.c_size_t, _vp, _vp, _int, _vp]),
+    "optr_local_join": (_int, [_vp]),
     "optr_comm_create": (_int, [ctypes.POINTER(_vp), _int, _int, _int, _i64, _int]),
     "optr_comm_handle_bytes": (ctypes.c_size_t, []),
     "optr_comm_get_handle": (_int, [_vp, _vp]),

@@ -178,18 +178,29 @@ class AllReduceResult:
 
 # -------------------------------------------------------- n workers, 1 GPU
 _WS: dict = {}
+_SLOT: dict = {}
 
 
-def _workspace(n: int, L: int, ht: bool, epp: int, device):
+def _workspace(n: int, L: int, ht: bool, epp: int, device, slot: int = -1):
+    """Cached workspace per device (and per async slot)."""
     import torch
 
     need = int(lib().optr_tar_local_workspace(n, L, int(ht), epp))
-    key = str(device)
+    key = (str(device), slot)
     ws = _WS.get(key)
     if ws is None or ws.numel() < need:
         ws = torch.empty(max(need, 1), dtype=torch.uint8, device=device)
         _WS[key] = ws
     return ws, need
+
+
+def local_join(stream=None):
+    """Make ``stream`` (default: current) wait for every async
+    ``tar_allreduce_local(..., async_op=True)`` call."""
+    import torch
+
+    st = stream if stream is not None else torch.cuda.current_stream()
+    check(lib().optr_local_join(st.cuda_stream), "local_join")
 
 
 def _dtype_code(t) -> int:
@@ -205,7 +216,8 @@ def _dtype_code(t) -> int:
 def tar_allreduce_local(buckets: list, *, rotation: int = 0, ht: bool = False, job_seed: int = 0,
                         generation: int = 0, bucket_id: int | None = None,
                         masks: MaskSpec | None = None, out: list | None = None,
-                        out_dtype=None, want_received: bool = False, stream=None):
+                        out_dtype=None, want_received: bool = False, stream=None,
+                        async_op: bool = False):
     """One TAR(+RHT) generation for ``n = len(buckets)`` workers whose buckets
     all live on one GPU (the reference's SimSession shape, runner.py:211-276
     with the channel replaced by ``masks``).
@@ -214,6 +226,10 @@ def tar_allreduce_local(buckets: list, *, rotation: int = 0, ht: bool = False, j
     tensor ``[2, n]`` of received entries per (stage, dst), and (if
     ``want_received``) the ``[n, dim]`` bool AllReduceResult.received.
     Everything is enqueued on ``stream`` (default: current); no host sync.
+    ``async_op=True``: the call runs on one of two library streams (two
+    buckets in flight); ``out`` (and ``counts``/``got`` when requested) are
+    ready only after ``local_join()``; keep every tensor passed in alive and
+    untouched until then.
     ``bucket_id`` defaults to ``generation % 65536`` like the runner
     (runner.py:219-222); the RHT seed is derive_seed(job_seed, bucket_id,
     generation).
@@ -235,19 +251,32 @@ def tar_allreduce_local(buckets: list, *, rotation: int = 0, ht: bool = False, j
     if out is None:
         out = [torch.empty(L, dtype=out_dtype, device=dev) for _ in range(n)]
     dim = (1 << max(0, (L - 1).bit_length())) if ht else L
-    counts = torch.zeros((2, n), dtype=torch.int64, device=dev)
+    # async calls run on a library stream the caching allocator does not know
+    # about, so they only write caller-owned tensors: no counts unless asked
+    counts = torch.zeros((2, n), dtype=torch.int64, device=dev) if (not async_op or want_received) else None
     got = torch.empty((n, dim), dtype=torch.uint8, device=dev) if want_received else None
-    ws, need = _workspace(n, L, ht, masks.epp, dev)
     xs = (ctypes.c_void_p * n)(*[b.data_ptr() for b in buckets])
     os_ = (ctypes.c_void_p * n)(*[o.data_ptr() for o in out])
     spec = masks.to_c()
     st = stream if stream is not None else torch.cuda.current_stream(dev)
-    check(lib().optr_tar_local(xs, os_, n, L, _dtype_code(buckets[0]), _dtype_code(out[0]),
-                               int(job_seed), int(generation % 65536 if bucket_id is None else bucket_id),
-                               int(generation), int(rotation), int(bool(ht)),
-                               ctypes.byref(spec), ws.data_ptr(), need, counts.data_ptr(),
-                               got.data_ptr() if got is not None else None, st.cuda_stream),
-          "tar_allreduce_local")
+    args = (xs, os_, n, L, _dtype_code(buckets[0]), _dtype_code(out[0]), int(job_seed),
+            int(generation % 65536 if bucket_id is None else bucket_id), int(generation), int(rotation),
+            int(bool(ht)), ctypes.byref(spec))
+    if async_op:
+        # two in-flight buckets: alternate slots (and their workspaces)
+        key = str(dev)
+        slot = _SLOT.get(key, 0)
+        _SLOT[key] = slot ^ 1
+        ws, need = _workspace(n, L, ht, masks.epp, dev, slot)
+        check(lib().optr_tar_local_async(*args, ws.data_ptr(), need,
+                                         counts.data_ptr() if counts is not None else None,
+                                         got.data_ptr() if got is not None else None, slot, st.cuda_stream),
+              "tar_allreduce_local")
+    else:
+        ws, need = _workspace(n, L, ht, masks.epp, dev)
+        check(lib().optr_tar_local(*args, ws.data_ptr(), need, counts.data_ptr(),
+                                   got.data_ptr() if got is not None else None, st.cuda_stream),
+              "tar_allreduce_local")
     return out, counts, (got.bool() if got is not None else None)
 
 

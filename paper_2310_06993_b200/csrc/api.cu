@@ -851,12 +851,13 @@ struct Helpers {
   cudaEvent_t join[kHelpers];
   std::mutex mu;
 };
-Helpers g_help[64];
+// set 0: synchronous calls; sets 1, 2: async calls of slot 0, 1
+Helpers g_help[64][3];
 
-Helpers* helpers() {
+Helpers* helpers(int set) {
   int dev = 0;
   cudaGetDevice(&dev);
-  Helpers* h = &g_help[dev & 63];
+  Helpers* h = &g_help[dev & 63][set];
   std::lock_guard<std::mutex> lk(g_attr_mu);
   if (!h->init) {
     for (int i = 0; i < kHelpers; ++i) {
@@ -886,10 +887,10 @@ int join_helpers(Helpers* h, cudaStream_t st) {
 // Run `fn(worker_base, nworkers, stream)` over all n workers: batched while
 // they fit in L2 together, else one worker per launch on the helper streams.
 template <class F>
-int for_workers(int64_t dim, int n, cudaStream_t st, F fn) {
+int for_workers(int64_t dim, int n, cudaStream_t st, int set, F fn) {
   const int k = workers_per_launch(dim, n);
   if (k >= n) return fn(0, n, st);
-  Helpers* h = helpers();
+  Helpers* h = helpers(set);
   if (!h) {
     for (int w0 = 0; w0 < n; w0 += k) {
       int rc = fn(w0, (n - w0 < k ? n - w0 : k), st);
@@ -908,6 +909,39 @@ int for_workers(int64_t dim, int n, cudaStream_t st, F fn) {
   int rc2 = join_helpers(h, st);
   return rc ? rc : rc2;
 }
+
+// Async co-resident calls: two slots, each with its own work stream and
+// helper-stream set, so consecutive buckets overlap (one bucket's aggregate
+// and decode with the next one's encode).
+struct LocalAsync {
+  bool init = false;
+  cudaStream_t ws[2];
+  cudaEvent_t fork[2], done[2];
+  bool recorded[2] = {false, false};
+  std::mutex mu;
+};
+LocalAsync g_lasync[64];
+
+LocalAsync* local_async() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  LocalAsync* a = &g_lasync[dev & 63];
+  std::lock_guard<std::mutex> lk(g_attr_mu);
+  if (!a->init) {
+    for (int i = 0; i < 2; ++i) {
+      if (cudaStreamCreateWithFlags(&a->ws[i], cudaStreamNonBlocking) != cudaSuccess) return nullptr;
+      if (cudaEventCreateWithFlags(&a->fork[i], cudaEventDisableTiming) != cudaSuccess) return nullptr;
+      if (cudaEventCreateWithFlags(&a->done[i], cudaEventDisableTiming) != cudaSuccess) return nullptr;
+    }
+    a->init = true;
+  }
+  return a;
+}
+
+int tar_local_impl(const void* const* x, void* const* out, int n, int64_t L, int dtype_in, int dtype_out,
+                   uint64_t job_seed, uint64_t bucket_id, uint64_t generation, int rotation, int ht,
+                   const optr_mask_spec* masks, void* workspace, size_t workspace_bytes,
+                   uint64_t* received_out, uint8_t* got_out, cudaStream_t st, int set);
 }  // namespace
 
 extern "C" {
@@ -948,6 +982,47 @@ int optr_tar_local(const void* const* x, void* const* out, int n, int64_t L, int
                    uint64_t job_seed, uint64_t bucket_id, uint64_t generation, int rotation, int ht,
                    const optr_mask_spec* masks, void* workspace, size_t workspace_bytes,
                    uint64_t* received_out, uint8_t* got_out, void* stream) {
+  bind_device(stream);
+  return tar_local_impl(x, out, n, L, dtype_in, dtype_out, job_seed, bucket_id, generation, rotation, ht, masks,
+                        workspace, workspace_bytes, received_out, got_out, (cudaStream_t)stream, 0);
+}
+
+int optr_tar_local_async(const void* const* x, void* const* out, int n, int64_t L, int dtype_in, int dtype_out,
+                         uint64_t job_seed, uint64_t bucket_id, uint64_t generation, int rotation, int ht,
+                         const optr_mask_spec* masks, void* workspace, size_t workspace_bytes,
+                         uint64_t* received_out, uint8_t* got_out, int slot, void* stream) {
+  if (slot < 0 || slot > 1) return OPTR_EINVAL;
+  bind_device(stream);
+  LocalAsync* la = local_async();
+  if (!la) return OPTR_ECUDA;
+  std::lock_guard<std::mutex> lk(la->mu);
+  const cudaStream_t ws = la->ws[slot];
+  CK(cudaEventRecord(la->fork[slot], (cudaStream_t)stream));
+  CK(cudaStreamWaitEvent(ws, la->fork[slot], 0));
+  int rc = tar_local_impl(x, out, n, L, dtype_in, dtype_out, job_seed, bucket_id, generation, rotation, ht, masks,
+                          workspace, workspace_bytes, received_out, got_out, ws, 1 + slot);
+  CK(cudaEventRecord(la->done[slot], ws));
+  la->recorded[slot] = true;
+  return rc;
+}
+
+int optr_local_join(void* stream) {
+  bind_device(stream);
+  LocalAsync* la = local_async();
+  if (!la) return OPTR_ECUDA;
+  std::lock_guard<std::mutex> lk(la->mu);
+  for (int i = 0; i < 2; ++i)
+    if (la->recorded[i]) CK(cudaStreamWaitEvent((cudaStream_t)stream, la->done[i], 0));
+  return OPTR_OK;
+}
+
+}  // extern "C"
+
+namespace {
+int tar_local_impl(const void* const* x, void* const* out, int n, int64_t L, int dtype_in, int dtype_out,
+                   uint64_t job_seed, uint64_t bucket_id, uint64_t generation, int rotation, int ht,
+                   const optr_mask_spec* masks, void* workspace, size_t workspace_bytes,
+                   uint64_t* received_out, uint8_t* got_out, cudaStream_t st, int set) {
   int rc = check_common(n, L, dtype_in, dtype_out, masks);
   if (rc) return rc;
   if (!x || !out || !workspace) return OPTR_EINVAL;
@@ -955,8 +1030,6 @@ int optr_tar_local(const void* const* x, void* const* out, int n, int64_t L, int
   LocalLayout lay = local_layout(n, L, ht, epp);
   if (workspace_bytes < lay.total) return OPTR_EINVAL;
   if (L == 0) return OPTR_OK;
-  bind_device(stream);
-  cudaStream_t st = (cudaStream_t)stream;
   char* ws = (char*)workspace;
   const int64_t dim = lay.dim;
   const int r = ((rotation % n) + n) % n;
@@ -995,7 +1068,7 @@ int optr_tar_local(const void* const* x, void* const* out, int n, int64_t L, int
       Yw[w] = Y + (size_t)w * dim;
     }
     snk.scale = (float)(1.0 / sqrt((double)dim));
-    rc = for_workers(dim, n, st, [&](int w0, int nw, cudaStream_t s2) {
+    rc = for_workers(dim, n, st, set, [&](int w0, int nw, cudaStream_t s2) {
       return run_transform(log2_exact(dim), true, w0, nw, src, buf, snk, s2, OPTR_K_ENC_FIRST);
     });
     if (rc) return rc;
@@ -1054,7 +1127,7 @@ int optr_tar_local(const void* const* x, void* const* out, int n, int64_t L, int
     snk.count_extra = counts + n;  // stage-2 row
     snk.count_stride = 1;
     snk.dim = (double)dim;
-    rc = for_workers(dim, n, st, [&](int w0, int nw, cudaStream_t s2) {
+    rc = for_workers(dim, n, st, set, [&](int w0, int nw, cudaStream_t s2) {
       return run_transform(log2_exact(dim), decode_contig_first(false), w0, nw, ga, buf, snk, s2, OPTR_K_DEC_FIRST);
     });
     if (rc) return rc;
@@ -1074,6 +1147,9 @@ int optr_tar_local(const void* const* x, void* const* out, int n, int64_t L, int
   if (received_out) CK(cudaMemcpyAsync(received_out, counts, (size_t)2 * n * 8, cudaMemcpyDeviceToDevice, st));
   return OPTR_OK;
 }
+}  // namespace
+
+extern "C" {
 
 // ------------------------------------------------ TAR, one worker per GPU
 struct optr_comm_s {

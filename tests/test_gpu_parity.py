@@ -290,3 +290,26 @@ def test_headline_size_lossless_properties(dev):
     for o in outs:
         e = ((o.double() - mean).norm() / mean.norm()).item()
         assert e < 0.3  # lossy by design (SURVEY finding 6)
+
+
+def test_async_local_two_in_flight_matches_sync(dev):
+    """optr_tar_local_async: consecutive buckets overlap on two slots; results
+    equal the synchronous call's."""
+    from paper_2310_06993_b200.collectives import local_join
+
+    n, L = 4, 300_000
+    sets = [[torch.randn(L, device=dev) for _ in range(n)] for _ in range(4)]
+    want = []
+    for g, xs in enumerate(sets):
+        o, _, _ = tar_allreduce_local(xs, rotation=g % n, ht=True, job_seed=2, generation=g,
+                                      masks=MaskSpec.coin(40 + g, 0.02))
+        want.append([t.clone() for t in o])
+    outs = [[torch.empty(L, device=dev) for _ in range(n)] for _ in sets]
+    for g, xs in enumerate(sets):
+        tar_allreduce_local(xs, rotation=g % n, ht=True, job_seed=2, generation=g,
+                            masks=MaskSpec.coin(40 + g, 0.02), out=outs[g], async_op=True)
+    local_join()
+    torch.cuda.synchronize()
+    for g in range(len(sets)):
+        for w in range(n):
+            assert torch.equal(outs[g][w], want[g][w])
