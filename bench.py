@@ -140,6 +140,10 @@ def kernel_bytes(cls: str, dim: int, L: int, n: int, s_in: int, s_out: int) -> i
         "dec_last": Y + s_out * L,     # read scratch, write output
         "assemble": Y + s_out * L,
         "prep": dim // 8,
+        # persistent two-pass chains: the intermediate between the passes is
+        # not counted (it is meant to stay in L2), so these are the minimum
+        "enc_chain": s_in * L + Y,     # read x, write the wire
+        "dec_chain": Y + s_out * L,    # gather the aggregates, write the output
     }.get(cls, 0)
 
 
@@ -251,6 +255,7 @@ def run_ours(args):
     stream = torch.cuda.current_stream(dev)
     drop = args.drop
     state = {"gen": 0}
+    overlap = os.environ.get("OPTR_BENCH_SYNC", "0") != "1"  # A/B switch: buckets in order
 
     def one_step(src=None, dst=None):
         gen = state["gen"]
@@ -259,10 +264,10 @@ def run_ours(args):
             r = gen % n_workers
             if multi:
                 comm.allreduce((src or grads)[b], (dst or outs)[b], rotation=r, ht=ht, job_seed=7,
-                               generation=gen, bucket_id=b, masks=masks, async_op=True)
+                               generation=gen, bucket_id=b, masks=masks, async_op=overlap)
             else:
                 tar_allreduce_local((src or grads)[b], rotation=r, ht=ht, job_seed=7, generation=gen,
-                                    bucket_id=b, masks=masks, out=(dst or outs)[b], async_op=True)
+                                    bucket_id=b, masks=masks, out=(dst or outs)[b], async_op=overlap)
         if multi:
             comm.join()
         else:

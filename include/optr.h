@@ -187,7 +187,9 @@ int optr_comm_barrier(optr_comm c, void* stream);
 #define OPTR_K_ASSEMBLE 8   /* stage-2 gather without RHT                   */
 #define OPTR_K_BARRIER 9
 #define OPTR_K_OTHER 10
-#define OPTR_K_CLASSES 11
+#define OPTR_K_ENC_CHAIN 11 /* both encode passes, all workers, one launch  */
+#define OPTR_K_DEC_CHAIN 12 /* gather + both decode passes, one launch      */
+#define OPTR_K_CLASSES 13
 /* Enable (1) / disable (0) CUDA-event timing of every kernel launch. */
 int optr_timing_enable(int on);
 /* Synchronise recorded events and return, per class, the summed device

@@ -307,22 +307,31 @@ int launch_tma_pass_s(int cls, const TmaMaps& maps, const TmaMaps& dmaps, const 
                       1 << (T - 5), smem);
 }
 
-// ring depth of the TMA pass kernels (OPTR_TMA_STAGES=3 for three)
-int tma_stages() {
-  static int s = 0;
-  if (!s) {
-    const char* e = getenv("OPTR_TMA_STAGES");
-    s = (e && e[0] == '3') ? 3 : ((e && e[0] == '1') ? 1 : 2);
+// ring depth of the TMA pass kernels: 2, strided T = 14 tiles 3 (D = 2^25:
+// the strided pass waits on its 32-byte-row TMA boxes with one CTA per SM;
+// a third stage takes it from 90 to 60 us; contiguous is flat from 2 up).
+// OPTR_TMA_STAGES (1..3) overrides both, OPTR_TMA_STAGES_C / _S one kind.
+int tma_stages(bool strided) {
+  static int s[2] = {0, 0};
+  int& v = s[strided ? 1 : 0];
+  if (!v) {
+    const char* e = getenv(strided ? "OPTR_TMA_STAGES_S" : "OPTR_TMA_STAGES_C");
+    if (!e) e = getenv("OPTR_TMA_STAGES");
+    v = (e && e[0] >= '1' && e[0] <= '3') ? e[0] - '0' : -1;  // -1: per-shape default
   }
-  return s;
+  return v;
 }
 
 template <int T, bool STRIDED, int SK, class Snk, int CBW = 3>
 int launch_tma_pass(int cls, const TmaMaps& maps, const TmaMaps& dmaps, const TmaArgs& a, const Snk& snk,
                     int worker, int nworkers, cudaStream_t st) {
-  if (tma_stages() == 1)
-    return launch_tma_pass_s<T, 1, STRIDED, SK, Snk, CBW>(cls, maps, dmaps, a, snk, worker, nworkers, st);
-  return launch_tma_pass_s<T, 2, STRIDED, SK, Snk, CBW>(cls, maps, dmaps, a, snk, worker, nworkers, st);
+  int S = tma_stages(STRIDED);
+  if (S < 0) S = (STRIDED && T >= 14) ? 3 : 2;  // T = 13 strided keeps three CTAs per SM
+  switch (S) {
+    case 1: return launch_tma_pass_s<T, 1, STRIDED, SK, Snk, CBW>(cls, maps, dmaps, a, snk, worker, nworkers, st);
+    case 3: return launch_tma_pass_s<T, 3, STRIDED, SK, Snk, CBW>(cls, maps, dmaps, a, snk, worker, nworkers, st);
+    default: return launch_tma_pass_s<T, 2, STRIDED, SK, Snk, CBW>(cls, maps, dmaps, a, snk, worker, nworkers, st);
+  }
 }
 
 // A pass through the TMA ring kernel when the shapes allow it; -1 when the
@@ -426,6 +435,163 @@ int try_tma(int cls, const PassGeom& pg, int nlog, int worker, int nworkers, con
     }
     if (T == 13) return launch_tma_pass<13, false, SK>(cls, maps, dmaps, a, snk, worker, nworkers, st);
     return launch_tma_pass<14, false, SK>(cls, maps, dmaps, a, snk, worker, nworkers, st);
+  }
+}
+
+// ---------------------------------------------- persistent two-pass chain
+// OPTR_CHAIN=1 opts in (measured slower than the separate pass launches on
+// the default workloads: the per-tile pipeline, not launch ramps, limits).
+bool chain_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("OPTR_CHAIN");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
+
+constexpr int kChainCtrWords = 2 + kMaxW;
+
+// Self-resetting ticket/dependency counters of the chain kernel, one block
+// per stream that launches chains (zeroed once, on that stream).
+unsigned int* chain_counters(int key, cudaStream_t st) {
+  static unsigned int* pool[64][8] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(g_attr_mu);
+  unsigned int*& p = pool[dev & 63][key & 7];
+  if (!p) {
+    if (cudaMalloc(&p, kChainCtrWords * sizeof(unsigned int)) != cudaSuccess) {
+      p = nullptr;
+      return nullptr;
+    }
+    if (cudaMemsetAsync(p, 0, kChainCtrWords * sizeof(unsigned int), st) != cudaSuccess) return nullptr;
+  }
+  return p;
+}
+
+template <int T, int S, int SK0, class Snk1>
+int launch_chain_s(int cls, const TmaMaps& maps1, const TmaMaps& dmaps1, const TmaArgs& a0, const TmaArgs& a1,
+                   const SnkBuf& snk0, const Snk1& snk1, const ChainSched& cs, int nworkers, cudaStream_t st) {
+  const size_t smem = tma_chain_smem_bytes<T, S>();
+  auto kern = tma_chain_kernel<T, S, SK0, Snk1, 3>;
+  int rc = set_smem_attr(kern, smem);
+  if (rc) return rc;
+  static int nsm = 0;
+  if (!nsm) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    if (nsm <= 0) nsm = 148;
+  }
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 1 << (T - 5), smem) != cudaSuccess ||
+      per_sm < 1)
+    per_sm = 1;
+  int64_t gx = (int64_t)nsm * per_sm;
+  const int64_t total = cs.jstart[cs.njobs];
+  if (gx > total) gx = total;
+  KScope ks(cls, st, nworkers);
+  launch_ex(kern, dim3((unsigned)gx), dim3(1 << (T - 5)), smem, st, maps1, dmaps1, a0, a1, snk0, snk1, cs);
+  return launch_check(kern, "tma_chain", T, 3, (int)gx, 1, 1 << (T - 5), smem);
+}
+
+// Both passes of a two-pass transform for workers [wb, wb+nw) in one
+// persistent launch (contiguous pass first, fused source; strided pass
+// second, fused sink).  -1 when the plan or the buffers do not fit it.
+template <class Src, class Snk>
+int try_chain(int cls, int nlog, int wb, int nw, const Src& src, const SrcBuf& buf, const Snk& snk,
+              unsigned int* ctr, cudaStream_t st) {
+  constexpr bool kBuf = std::is_same<Src, SrcBuf>::value;
+  constexpr bool kEnc = std::is_same<Src, SrcEncode>::value;
+  constexpr bool kGather = std::is_same<Src, SrcGather>::value;
+  constexpr bool kSnkBuf = std::is_same<Snk, SnkBuf>::value;
+  constexpr bool kSnkDec = std::is_same<Snk, SnkDecode>::value;
+  if constexpr (!(kBuf || kEnc || kGather) || !(kSnkBuf || kSnkDec)) {
+    return -1;
+  } else {
+    if (!ctr || !chain_enabled() || !tma_enabled()) return -1;
+    PassGeom ps[3];
+    if (plan_passes(nlog, ps, true) != 2) return -1;
+    const int T = ps[0].ks;
+    if (ps[0].cb != 0 || ps[0].lo != 0 || (T != 13 && T != 14)) return -1;
+    if (ps[1].cb != 3 || ps[1].lo != T || ps[1].ks + 3 != T) return -1;
+    TmaArgs a0, a1;
+    memset(&a0, 0, sizeof(a0));
+    memset(&a1, 0, sizeof(a1));
+    TmaMaps maps1, dmaps1;
+    memset(&maps1, 0, sizeof(maps1));
+    memset(&dmaps1, 0, sizeof(dmaps1));
+    a0.ntiles = ps[0].ntiles;
+    for (int w = wb; w < wb + nw; ++w) {
+      if constexpr (kBuf) a0.xw[w] = src.y[w];
+      if constexpr (kEnc) {
+        a0.xw[w] = src.x[w];
+        if (((uintptr_t)a0.xw[w] & 15) || ((uintptr_t)src.signs & 15)) return -1;
+      }
+    }
+    if constexpr (kEnc) {
+      a0.dtype = src.dtype;
+      a0.L = src.L;
+      a0.signs = src.signs;
+    }
+    if constexpr (kGather) {
+      if (src.pow2_shift < T) return -1;
+      for (int o = 0; o < src.n; ++o) a0.A[o] = src.A[o];
+      a0.n = src.n;
+      a0.r = src.r;
+      a0.shard_shift = src.pow2_shift;
+      a0.m = src.m;
+      a0.got = src.got;
+      a0.dim = src.dim;
+    }
+    const uint64_t d0 = 1ULL << T, d1 = 1ULL << ps[1].ks;
+    const int box = (int)(d1 < 256 ? d1 : 256);
+    for (int w = wb; w < wb + nw; ++w) {
+      if (!make_map3(&maps1.m[w], buf.y[w], d0, d1, 1, (uint32_t)box)) return -1;
+      if constexpr (kSnkBuf) {
+        if (!make_map3(&dmaps1.m[w], snk.y[w], d0, d1, 1, (uint32_t)box)) return -1;
+      } else {
+        const int64_t rows_full = snk.L >> T;
+        if (rows_full > 0 && !make_map3(&dmaps1.m[w], snk.out[w], d0, (uint64_t)rows_full, 1, (uint32_t)box,
+                                        snk.dtype))
+          return -1;
+        if (((uintptr_t)snk.out[w] & 15) || ((uintptr_t)snk.signs & 15)) return -1;
+      }
+    }
+    a1.ntiles = ps[1].ntiles;
+    a1.lo = T;
+    a1.box_rows = box;
+    if constexpr (kSnkBuf) a1.scale = snk.scale;
+    SnkBuf mid;
+    memset(&mid, 0, sizeof(mid));
+    for (int i = 0; i < kMaxW; ++i) mid.y[i] = buf.y[i];
+    mid.scale = 1.f;
+    ChainSched cs;
+    memset(&cs, 0, sizeof(cs));
+    cs.ctr = ctr;
+    cs.nw = kMaxW;
+    cs.nt0 = ps[0].ntiles;
+    cs.nt1 = ps[1].ntiles;
+    // w0.p0, w1.p0, w0.p1, w2.p0, w1.p1, ...: a worker's second pass follows
+    // one other worker's first pass
+    int64_t tk = 0;
+    auto add = [&](int pass, int w) {
+      cs.jpass[cs.njobs] = (int8_t)pass;
+      cs.jw[cs.njobs] = (int8_t)w;
+      cs.jstart[cs.njobs] = tk;
+      tk += pass == 0 ? cs.nt0 : cs.nt1;
+      ++cs.njobs;
+    };
+    for (int i = 0; i < nw; ++i) {
+      add(0, wb + i);
+      if (i > 0) add(1, wb + i - 1);
+    }
+    add(1, wb + nw - 1);
+    cs.jstart[cs.njobs] = tk;
+    constexpr int SK0 = kBuf ? TS_BUF : (kEnc ? TS_ENC : TS_GATHER);
+    if (T == 13) return launch_chain_s<13, 2, SK0>(cls, maps1, dmaps1, a0, a1, mid, snk, cs, nw, st);
+    return launch_chain_s<14, 2, SK0>(cls, maps1, dmaps1, a0, a1, mid, snk, cs, nw, st);
   }
 }
 
@@ -777,7 +943,7 @@ int optr_rht_encode(const void* x, int dtype_in, int64_t L, float* y, int64_t di
     memset(&snk, 0, sizeof(snk));
     snk.y[0] = y;
     snk.scale = (float)(1.0 / sqrt((double)dim));
-    rc = run_transform(log2_exact(dim), true, 0, 1, src, buf, snk, st);
+    rc = run_transform(log2_exact(dim), true, 0, 1, src, buf, snk, st, OPTR_K_ENC_FIRST);
   }
   cudaFreeAsync(signs, st);
   return rc;
@@ -828,7 +994,7 @@ int optr_rht_decode(const float* y, const uint8_t* mask, int64_t dim, int64_t L,
     snk.count_extra = nullptr;
     snk.count_base[0] = (int64_t)count;
     snk.dim = (double)dim;
-    rc = run_transform(log2_exact(dim), false, 0, 1, src, buf, snk, st);
+    rc = run_transform(log2_exact(dim), false, 0, 1, src, buf, snk, st, OPTR_K_DEC_FIRST);
   }
   cudaFreeAsync(tmp, st);
   cudaFreeAsync(signs, st);
@@ -898,12 +1064,18 @@ int for_workers(int64_t dim, int n, cudaStream_t st, int set, F fn) {
     }
     return OPTR_OK;
   }
+  static int chains = -1;
+  if (chains < 0) {
+    const char* e = getenv("OPTR_CHAINS");
+    chains = e ? atoi(e) : kHelpers;
+    if (chains < 1 || chains > kHelpers) chains = kHelpers;
+  }
   std::lock_guard<std::mutex> lk(h->mu);
   int rc = fork_helpers(h, st);
   if (rc) return rc;
   int i = 0;
   for (int w0 = 0; w0 < n; w0 += k, ++i) {
-    rc = fn(w0, (n - w0 < k ? n - w0 : k), h->s[i % kHelpers]);
+    rc = fn(w0, (n - w0 < k ? n - w0 : k), h->s[i % chains]);
     if (rc) break;
   }
   int rc2 = join_helpers(h, st);
@@ -949,7 +1121,7 @@ extern "C" {
 // -------------------------------------------------- TAR, n workers, one GPU
 struct LocalLayout {
   size_t y, a, signs, bitmap, counts, total;
-  int64_t dim, smax, pw;
+  int64_t dim, smax, astride, pw;
 };
 
 static LocalLayout local_layout(int n, int64_t L, int ht, int epp) {
@@ -957,12 +1129,13 @@ static LocalLayout local_layout(int n, int64_t L, int ht, int epp) {
   l.dim = ht ? next_pow2_i(L) : L;
   Shards sh = make_shards(l.dim, n);
   l.smax = sh.base + (sh.extra ? 1 : 0);
+  l.astride = (l.smax + 63) / 64 * 64;  // owner aggregates 256-byte aligned (float4 / TMA)
   l.pw = mask_words(l.dim, n, epp);
   size_t off = 0;
   l.y = off;
   off = align_up(off + (size_t)n * l.dim * 4, 256);
   l.a = off;
-  off = align_up(off + (size_t)n * (l.smax > 0 ? l.smax : 1) * 4, 256);
+  off = align_up(off + (size_t)n * (l.astride > 0 ? l.astride : 1) * 4, 256);
   l.signs = off;
   off = align_up(off + (size_t)((l.dim + 31) / 32 + 2) * 4, 256);
   l.bitmap = off;
@@ -1068,9 +1241,11 @@ int tar_local_impl(const void* const* x, void* const* out, int n, int64_t L, int
       Yw[w] = Y + (size_t)w * dim;
     }
     snk.scale = (float)(1.0 / sqrt((double)dim));
-    rc = for_workers(dim, n, st, set, [&](int w0, int nw, cudaStream_t s2) {
-      return run_transform(log2_exact(dim), true, w0, nw, src, buf, snk, s2, OPTR_K_ENC_FIRST);
-    });
+    rc = try_chain(OPTR_K_ENC_CHAIN, log2_exact(dim), 0, n, src, buf, snk, chain_counters(set, st), st);
+    if (rc < 0)
+      rc = for_workers(dim, n, st, set, [&](int w0, int nw, cudaStream_t s2) {
+        return run_transform(log2_exact(dim), true, w0, nw, src, buf, snk, s2, OPTR_K_ENC_FIRST);
+      });
     if (rc) return rc;
   } else {
     for (int w = 0; w < n; ++w) {
@@ -1091,7 +1266,7 @@ int tar_local_impl(const void* const* x, void* const* out, int n, int64_t L, int
   memset(&ag, 0, sizeof(ag));
   for (int w = 0; w < n; ++w) {
     ag.Y[w] = Yw[w];
-    ag.A[w] = A + (size_t)w * lay.smax;
+    ag.A[w] = A + (size_t)w * lay.astride;
   }
   ag.sh = sh;
   ag.n = n;
@@ -1127,9 +1302,12 @@ int tar_local_impl(const void* const* x, void* const* out, int n, int64_t L, int
     snk.count_extra = counts + n;  // stage-2 row
     snk.count_stride = 1;
     snk.dim = (double)dim;
-    rc = for_workers(dim, n, st, set, [&](int w0, int nw, cudaStream_t s2) {
-      return run_transform(log2_exact(dim), decode_contig_first(false), w0, nw, ga, buf, snk, s2, OPTR_K_DEC_FIRST);
-    });
+    rc = try_chain(OPTR_K_DEC_CHAIN, log2_exact(dim), 0, n, ga, buf, snk, chain_counters(set, st), st);
+    if (rc < 0)
+      rc = for_workers(dim, n, st, set, [&](int w0, int nw, cudaStream_t s2) {
+        return run_transform(log2_exact(dim), decode_contig_first(false), w0, nw, ga, buf, snk, s2,
+                             OPTR_K_DEC_FIRST);
+      });
     if (rc) return rc;
   } else {
     AsmArgs as;
@@ -1162,7 +1340,8 @@ struct optr_comm_s {
   char* peer[OPTR_MAX_WORKERS];
   bool opened[OPTR_MAX_WORKERS];
   char* local;  // two parities of signs | bitmap | counts
-  size_t off_signs, off_bitmap, off_counts, local_bytes;  // within one parity
+  size_t off_signs, off_bitmap, off_counts, off_chain, local_bytes;  // within one parity
+  unsigned int* chain_ctr[2];  // chain-kernel counters of each parity (self-resetting)
   unsigned long long epoch[3];
   cudaStream_t ws[2];       // per-parity work streams
   cudaEvent_t fork[2];
@@ -1213,6 +1392,8 @@ int optr_comm_create(optr_comm* out, int device, int rank, int n, int64_t max_le
   off = align_up(off + (size_t)2 * n * n * pw * 4, 256);
   c->off_counts = off;
   off = align_up(off + (size_t)2 * n * 8, 256);
+  c->off_chain = off;
+  off = align_up(off + kChainCtrWords * sizeof(unsigned int), 256);
   c->local_bytes = off;
   if (cudaMalloc((void**)&c->sym, c->sym_bytes) != cudaSuccess ||
       cudaMalloc((void**)&c->local, 2 * c->local_bytes) != cudaSuccess) {
@@ -1221,6 +1402,8 @@ int optr_comm_create(optr_comm* out, int device, int rank, int n, int64_t max_le
     return OPTR_ENOMEM;
   }
   CK(cudaMemset(c->sym, 0, c->sym_bytes));
+  CK(cudaMemset(c->local, 0, 2 * c->local_bytes));
+  for (int p = 0; p < 2; ++p) c->chain_ctr[p] = (unsigned int*)(c->local + p * c->local_bytes + c->off_chain);
   CK(cudaStreamCreateWithFlags(&c->pstream, cudaStreamNonBlocking));
   for (int p = 0; p < 2; ++p) {
     CK(cudaEventCreateWithFlags(&c->prep_ready[p], cudaEventDisableTiming));
@@ -1407,7 +1590,9 @@ static int tar_enqueue(optr_comm c, const void* x, void* out, int64_t L, int dty
     memset(&snk, 0, sizeof(snk));
     snk.y[me] = Yp[me];
     snk.scale = (float)(1.0 / sqrt((double)dim));
-    if ((rc = run_transform(log2_exact(dim), true, me, 1, src, buf, snk, st, OPTR_K_ENC_FIRST))) return rc;
+    rc = try_chain(OPTR_K_ENC_CHAIN, log2_exact(dim), me, 1, src, buf, snk, c->chain_ctr[par], st);
+    if (rc < 0) rc = run_transform(log2_exact(dim), true, me, 1, src, buf, snk, st, OPTR_K_ENC_FIRST);
+    if (rc) return rc;
   } else {
     KScope ks(OPTR_K_OTHER, st);
     cast_copy_kernel<<<1184, 256, 0, st>>>(x, dtype_in, Yp[me], dim);
@@ -1465,7 +1650,11 @@ static int tar_enqueue(optr_comm c, const void* x, void* out, int64_t L, int dty
     snk.count_extra = counts + n;
     snk.count_stride = 1;
     snk.dim = (double)dim;
-    if ((rc = run_transform(log2_exact(dim), decode_contig_first(true), me, 1, ga, buf, snk, st, OPTR_K_DEC_FIRST))) return rc;
+    rc = decode_contig_first(true)
+             ? try_chain(OPTR_K_DEC_CHAIN, log2_exact(dim), me, 1, ga, buf, snk, c->chain_ctr[par], st)
+             : -1;
+    if (rc < 0) rc = run_transform(log2_exact(dim), decode_contig_first(true), me, 1, ga, buf, snk, st, OPTR_K_DEC_FIRST);
+    if (rc) return rc;
   } else {
     AsmArgs as;
     memset(&as, 0, sizeof(as));

@@ -405,6 +405,7 @@ struct SrcGather {
     __device__ __forceinline__ void begin_tile(int64_t g0, int64_t g1) {
       int j0 = p->sh.of(g0), j1 = p->sh.of(g1);
       uj = j0 == j1 ? j0 : -1;
+      if (uj >= 0 && (((uintptr_t)p->A[shard_owner(uj, p->r, p->n)]) & 15)) uj = -1;  // float4 needs 16B
       if (uj >= 0) {
         int owner = shard_owner(uj, p->r, p->n);
         uoff = p->sh.off(uj);

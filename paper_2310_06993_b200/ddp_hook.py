@@ -15,9 +15,13 @@ generation) (hadamard.py:31-34).  NVLink is lossless, so by default nothing is
 dropped; ``drop_prob > 0`` emulates the paper's lossy transport with the
 seeded datagram coin (per generation and bucket).
 
-The hook enqueues work and returns an already-completed future: every
-kernel runs on the stream DDP's reducer uses, so the reducer's copy of the
-result back into the gradients is ordered after them.
+The hook enqueues work and returns an already-completed future.  With
+``overlap=True`` (default) buckets are enqueued with ``optr_tar_async`` so a
+bucket's encode and stage 1 run behind the previous bucket's decode; the
+last bucket of the pass joins them onto the reducer's stream.  That is safe
+because the reducer copies the hook results back into the gradients only in
+its end-of-backward finalisation, after every bucket's hook has run, on the
+same stream.  ``overlap=False`` orders every bucket on the stream.
 """
 
 from __future__ import annotations
@@ -39,8 +43,10 @@ class OptiReduceState:
     drop_prob: float = 0.0
     max_payload: int = 1400
     generation: int = 0
+    overlap: bool = True
     comm: object = field(default=None, repr=False)
     received: list = field(default_factory=list, repr=False)  # per-bucket [2] counts of the last pass
+    _pending: list = field(default_factory=list, repr=False)  # buffers async calls still use
 
     def communicator(self, device, needed_len: int = 0):
         """The NVLink communicator, (re)created collectively when a bucket is
@@ -84,7 +90,13 @@ def optireduce_hook(state: OptiReduceState, bucket):
     world = comm.world
     comm.allreduce(buf, out, rotation=state.generation % world, ht=state.ht, job_seed=state.seed,
                    generation=state.generation, bucket_id=bucket.index(), masks=state.masks(bucket.index()),
-                   received=rec)
+                   received=rec, async_op=state.overlap)
+    if state.overlap:
+        # keep every buffer the queued kernels touch alive until the join
+        state._pending.append((buf, out, rec))
+        if bucket.is_last():
+            comm.join()
+            state._pending = []
     if bucket.index() == 0:
         state.received = []
     state.received.append(rec)

@@ -10,9 +10,12 @@ calls ``TarCommunicator.allreduce`` with its own bucket:
 * device barrier (flags over NVLink);
 * stage 1: pull its owned shard from every peer's wire buffer over NVLink
   and take the masked fp64 mean (collectives.py:113-125);
-* device barrier;
-* stage 2: pull every owner's aggregate over NVLink, masked, fused into the
-  first pass of its own decode (collectives.py:127-150, runner.py:248-256).
+* stage 2, fused into the same kernel: the owner pushes its aggregate into
+  every peer's symmetric gather buffer over NVLink (collectives.py:127-150);
+* device barrier; masked decode from the local gather buffer
+  (runner.py:248-256).  (``OPTR_STAGE2=pull`` selects the older variant:
+  a second barrier, then every rank pulls the owners' aggregates inside the
+  first decode pass.)
 
 torch.distributed (NCCL) only carries the one-time IPC handle exchange and
 host barriers; the data path is peer loads inside the kernels.
@@ -94,8 +97,6 @@ class TarCommunicator:
         if len(x) != len(out) or len(x) > self.max_len:
             raise ValueError("bucket longer than the communicator's max_len")
         masks = masks or MaskSpec.none(self.epp * 4)
-        if masks.epp != self.epp and masks.kind != "none":
-            pass  # epp is per call; buffers only bound the packet count
         spec = masks.to_c()
         st = stream if stream is not None else torch.cuda.current_stream(self.device)
         fn = lib().optr_tar_async if async_op else lib().optr_tar

@@ -313,3 +313,51 @@ def test_async_local_two_in_flight_matches_sync(dev):
     for g in range(len(sets)):
         for w in range(n):
             assert torch.equal(outs[g][w], want[g][w])
+
+
+# ------------------------------------------------ persistent chain kernel
+@pytest.mark.parametrize("n,L,dtype", [(4, 5_000_000, "f32"), (3, 4_500_000, "f32"), (2, 25_000_000, "bf16"),
+                                       (8, 7_000_000, "f32")])
+def test_chain_matches_pass_launches(dev, n, L, dtype, tmp_path):
+    """The two-pass chain kernel (one persistent launch for both passes of
+    every worker, D = 2^23 / 2^25) is bit-identical to the separate pass
+    launches in the same order (subprocess, OPTR_CHAIN=0 and contiguous-first
+    decode), masks and received flags included."""
+    import os
+    import subprocess
+    import sys
+
+    import chain_case
+
+    here = os.path.dirname(os.path.abspath(__file__))
+    z = {}
+    for chain in ("1", "0"):
+        path = str(tmp_path / f"c{chain}.npz")
+        env = dict(os.environ, OPTR_CHAIN=chain, OPTR_DEC_ORDER="contig")
+        env["PYTHONPATH"] = os.pathsep.join([os.path.dirname(here), here, env.get("PYTHONPATH", "")])
+        subprocess.run([sys.executable, os.path.join(here, "chain_case.py"), str(n), str(L), dtype, "1", path],
+                       check=True, env=env, timeout=600)
+        z[chain] = np.load(path)
+    for k in ("counts", "got", "res"):
+        np.testing.assert_array_equal(z["1"][k], z["0"][k])
+    # and the default path (strided-first local decode) agrees within the codec error
+    res, counts, got, _ = chain_case.run(n, L, dtype, seed=1)
+    np.testing.assert_array_equal(counts, z["1"]["counts"])
+    np.testing.assert_array_equal(got, z["1"]["got"])
+    assert rel_err(res, z["1"]["res"]) < (REL if dtype == "f32" else 1e-2)  # bf16 output rounding
+
+
+def test_chain_vs_oracle_d23(dev):
+    """Default pass path (n=4, D=2^23, datagram coin) against the oracle; the
+    chain kernel is pinned to it bit-exactly by the test above."""
+    n, L, p, gen = 4, 4_500_001, 0.01, 3
+    seed, coin_seed = 21, 555
+    r = gen % n
+    dim = O.next_pow2(L)
+    buckets = O.make_buckets(seed, n, L)
+    masks = O.datagram_masks(coin_seed, dim, n, r, p)
+    want, _, tar = O.run_generation(buckets, seed, gen, True, masks=masks, r=r, return_wire=True)
+    outs, counts, got = _run_local(buckets, r, True, seed, gen, MaskSpec.coin(coin_seed, p), dev)
+    for node in range(n):
+        assert rel_err(outs[node], want[node]) < REL, node
+        np.testing.assert_array_equal(got[node].astype(bool), tar[node][1])

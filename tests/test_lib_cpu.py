@@ -123,3 +123,15 @@ def test_invalid_arguments_rejected_without_gpu():
         pkg.RhtContext(dim=6, seed=0, orig_len=3)
     with pytest.raises(ValueError):
         pkg.RhtContext(dim=4, seed=0, orig_len=5)
+
+
+def test_kernel_class_names_match_header():
+    """_lib.K_NAMES indexes optr_timing_collect's arrays (optr.h OPTR_K_*)."""
+    import re
+
+    from paper_2310_06993_b200 import _lib
+
+    hdr = open(os.path.join(ROOT, "include", "optr.h")).read()
+    consts = {m.group(1): int(m.group(2)) for m in re.finditer(r"#define OPTR_K_(\w+) (\d+)", hdr)}
+    assert consts.pop("CLASSES") == len(_lib.K_NAMES)
+    assert sorted(consts.values()) == list(range(len(_lib.K_NAMES)))

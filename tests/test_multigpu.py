@@ -143,24 +143,28 @@ def _ddp_worker(rank, world, port, outdir):
     dev = torch.device("cuda", rank)
     dist.init_process_group("nccl", rank=rank, world_size=world, device_id=dev)
     grads = {}
-    for mode in ("nccl", "optireduce"):
+    for mode in ("nccl", "overlap", "ordered"):
         torch.manual_seed(0)
         model = nn.Sequential(nn.Linear(512, 1024), nn.ReLU(), nn.Linear(1024, 700), nn.ReLU(),
                               nn.Linear(700, 10)).to(dev)
         ddp = DDP(model, device_ids=[rank], bucket_cap_mb=1)
-        if mode == "optireduce":
-            state = OptiReduceState(max_bucket_len=max_bucket_len_for(model, 1), ht=True, seed=3)
+        if mode != "nccl":
+            state = OptiReduceState(max_bucket_len=max_bucket_len_for(model, 1), ht=True, seed=3,
+                                    overlap=(mode == "overlap"))
             ddp.register_comm_hook(state, optireduce_hook)
         g = torch.Generator(device=dev).manual_seed(100 + rank)
-        x = torch.randn(64, 512, device=dev, generator=g)
-        loss = ddp(x).square().mean()
-        loss.backward()
+        for _step in range(2):  # second pass reuses the buffers at the next generation
+            model.zero_grad(set_to_none=True)
+            x = torch.randn(64, 512, device=dev, generator=g)
+            loss = ddp(x).square().mean()
+            loss.backward()
         torch.cuda.synchronize()
         grads[mode] = torch.cat([p.grad.flatten() for p in model.parameters()]).cpu().numpy()
-        if mode == "optireduce":
-            assert state.generation == 1
+        if mode != "nccl":
+            assert state.generation == 2
+            assert len(state.received) >= 2 and not state._pending
             state.comm.close()
-    np.save(os.path.join(outdir, f"ddp_r{rank}.npy"), np.stack([grads["nccl"], grads["optireduce"]]))
+    np.save(os.path.join(outdir, f"ddp_r{rank}.npy"), np.stack([grads["nccl"], grads["overlap"], grads["ordered"]]))
     dist.destroy_process_group()
 
 
@@ -177,6 +181,8 @@ def test_ddp_comm_hook_lossless_matches_mean():
     with tempfile.TemporaryDirectory() as d:
         mp.spawn(_ddp_worker, args=(world, _free_port(), d), nprocs=world, join=True)
         for r in range(world):
-            ref, got = np.load(os.path.join(d, f"ddp_r{r}.npy"))
-            rel = np.linalg.norm(got.astype(np.float64) - ref) / np.linalg.norm(ref)
-            assert rel < 1e-5, rel
+            ref, ovl, ordered = np.load(os.path.join(d, f"ddp_r{r}.npy"))
+            for got in (ovl, ordered):
+                rel = np.linalg.norm(got.astype(np.float64) - ref) / np.linalg.norm(ref)
+                assert rel < 1e-5, rel
+            np.testing.assert_array_equal(ovl, ordered)  # same kernels, same order of arithmetic
