@@ -144,6 +144,10 @@ def kernel_bytes(cls: str, dim: int, L: int, n: int, s_in: int, s_out: int) -> i
         # not counted (it is meant to stay in L2), so these are the minimum
         "enc_chain": s_in * L + Y,     # read x, write the wire
         "dec_chain": Y + s_out * L,    # gather the aggregates, write the output
+        # multi-GPU fused kernel: contiguous encode pass in place (2Y), owner
+        # shard in from n wire vectors + mean out to n receive vectors (local
+        # side only: S in, S out), contiguous decode pass in place (2Y)
+        "fused": 4 * Y + 2 * S,
     }.get(cls, 0)
 
 
@@ -378,13 +382,15 @@ def run_ours(args):
         for L in buckets:
             dim = next_pow2(L) if ht else L
             if nvlink:
-                per_b += 4 * dim * (n_workers - 1) // n_workers
+                # stage 1 in (+ stage 2 in for the fused kernel), per direction
+                k = 2 if cls == "fused" else 1
+                per_b += k * 4 * dim * (n_workers - 1) // n_workers
             else:
                 per_b += kernel_bytes(cls, dim, L, n_workers, s_in, s_out)
         return units * per_b / len(buckets)
 
     achieved = class_bytes(dom) / (dom_ms * 1e-3) / 1e9
-    if multi and dom in ("aggregate", "dec_first"):
+    if multi and dom in ("aggregate", "dec_first", "fused"):
         nv_ach = class_bytes(dom, nvlink=True) / (dom_ms * 1e-3) / 1e9
         roof = {"bound": "nvlink", "achieved": round(nv_ach, 1), "peak": NVLINK_GBS, "unit": "GB/s",
                 "frac": round(nv_ach / NVLINK_GBS, 4), "kernel": dom, "peak_src": "measured peer copy",

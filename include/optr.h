@@ -189,9 +189,14 @@ int optr_comm_barrier(optr_comm c, void* stream);
 #define OPTR_K_OTHER 10
 #define OPTR_K_ENC_CHAIN 11 /* both encode passes, all workers, one launch  */
 #define OPTR_K_DEC_CHAIN 12 /* gather + both decode passes, one launch      */
-#define OPTR_K_CLASSES 13
+#define OPTR_K_FUSED 13     /* multi-GPU: contiguous encode + stage 1 + stage 2
+                               + contiguous decode, one persistent launch  */
+#define OPTR_K_CLASSES 14
 /* Enable (1) / disable (0) CUDA-event timing of every kernel launch. */
 int optr_timing_enable(int on);
+/* Debug: event trace of the fused multi-GPU kernel into a device buffer of
+ * gridDim * per_cta uint4 records (null disables).  Not thread-safe. */
+int optr_debug_trace(void* dev_buf, int64_t per_cta);
 /* Synchronise recorded events and return, per class, the summed device
  * milliseconds, the launch count and the worker-passes those launches
  * covered (a launch over k co-resident workers counts k) since the last

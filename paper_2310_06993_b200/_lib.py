@@ -30,7 +30,8 @@ MAX_WORKERS = 16
 
 # kernel classes of optr_timing_collect (optr.h OPTR_K_*)
 K_NAMES = ["prep", "enc_first", "enc_mid", "enc_last", "aggregate", "dec_first", "dec_mid",
-           "dec_last", "assemble", "barrier", "other", "enc_chain", "dec_chain"]
+           "dec_last", "assemble", "barrier", "other", "enc_chain", "dec_chain",
+           "fused"]
 
 
 class optr_mask_spec(ctypes.Structure):
@@ -81,6 +82,7 @@ SIGNATURES = {
     "optr_timing_enable": (_int, [_int]),
     "optr_timing_collect": (_int, [ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_i64), ctypes.POINTER(_i64)]),
     "optr_launch_count": (_i64, []),
+    "optr_debug_trace": (_int, [_vp, _i64]),
     "optr_probe_enable_peer": (_int, [_int, _int]),
     "optr_probe_copy": (_int, [_vp, _vp, _i64, _int, _int, _vp]),
 }

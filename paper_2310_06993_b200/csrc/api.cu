@@ -368,7 +368,28 @@ int try_tma(int cls, const PassGeom& pg, int nlog, int worker, int nworkers, con
     }
     if (pg.cb == 3 || pg.cb == 5) {  // strided: tensor boxes in, tensor boxes out
       if constexpr (kEnc) {
-        return -1;
+        // strided-first encode (the fused multi-GPU path): x as [rows_full][2^lo]
+        if (pg.cb != 3 || (T != 13 && T != 14)) return -1;
+        const uint64_t d0 = 1ULL << pg.lo, d1 = 1ULL << pg.ks;
+        if (nlog != pg.lo + pg.ks) return -1;  // two-pass plans only (no outer blocks)
+        const int64_t rows_full = src.L >> pg.lo;
+        if (rows_full < 1) return -1;
+        const int box = (int)(d1 < 256 ? d1 : 256);
+        for (int w = worker; w < worker + nworkers; ++w) {
+          if (((uintptr_t)src.x[w] & 15) || !make_map3(&maps.m[w], src.x[w], d0, (uint64_t)rows_full, 1,
+                                                         (uint32_t)box, src.dtype))
+            return -1;
+          a.xw[w] = src.x[w];
+          if (!make_map3(&dmaps.m[w], snk.y[w], d0, d1, 1, (uint32_t)box)) return -1;
+        }
+        a.dtype = src.dtype;
+        a.L = src.L;
+        a.signs = src.signs;
+        a.signs_t = src.signs_t;
+        a.scale = snk.scale;
+        a.box_rows = box;
+        if (T == 13) return launch_tma_pass<13, true, SK>(cls, maps, dmaps, a, snk, worker, nworkers, st);
+        return launch_tma_pass<14, true, SK>(cls, maps, dmaps, a, snk, worker, nworkers, st);
       } else {
         if (T < 9 || T > 14 || (pg.cb == 5 && T != 14)) return -1;
         const uint32_t bw = 1u << pg.cb;
@@ -397,6 +418,9 @@ int try_tma(int cls, const PassGeom& pg, int nlog, int worker, int nworkers, con
           }
         }
         if constexpr (kSnkBuf) a.scale = snk.scale;
+        if constexpr (!kSnkBuf) {
+          if (pg.cb == 3) a.signs_t = snk.signs_t;
+        }
         a.box_rows = box;
         if (pg.cb == 5) return launch_tma_pass<14, true, SK, Snk, 5>(cls, maps, dmaps, a, snk, worker, nworkers, st);
         if constexpr (kSnkBuf) {  // small strided tiles (3-pass plans of D >= 2^26)
@@ -1335,13 +1359,16 @@ struct optr_comm_s {
   int64_t max_dim;
   // two parities of [Y | A] so consecutive calls can overlap; three flag
   // sets (one per parity, one for the public barrier)
-  size_t off_flags[3], off_y[2], off_a[2], off_g[2], sym_bytes;
+  size_t off_flags[3], off_y[2], off_a[2], off_g[2], off_ef[2], off_gf[2], sym_bytes;
   char* sym;
   char* peer[OPTR_MAX_WORKERS];
   bool opened[OPTR_MAX_WORKERS];
   char* local;  // two parities of signs | bitmap | counts
-  size_t off_signs, off_bitmap, off_counts, off_chain, local_bytes;  // within one parity
-  unsigned int* chain_ctr[2];  // chain-kernel counters of each parity (self-resetting)
+  size_t off_signs, off_signs_t, off_bitmap, off_counts, off_chain, local_bytes;  // within one parity
+  unsigned int* chain_ctr[2];  // chain / fused kernel counters of each parity (self-resetting)
+  unsigned int fepoch[2];      // fused-kernel tile-flag epochs of each parity
+  cudaEvent_t fused_done[2];   // fused kernels of consecutive calls never overlap
+  bool fused_recorded[2];
   unsigned long long epoch[3];
   cudaStream_t ws[2];       // per-parity work streams
   cudaEvent_t fork[2];
@@ -1382,12 +1409,18 @@ int optr_comm_create(optr_comm* out, int device, int rank, int n, int64_t max_le
     off = align_up(off + (size_t)smax * 4, 1024);
     c->off_g[p] = off;  // stage-2 receive vector, written by every owner's push
     off = align_up(off + (size_t)c->max_dim * 4, 1024);
+    c->off_ef[p] = off;  // fused kernel: per-tile encode / receive flags
+    off = align_up(off + (size_t)(c->max_dim >> 13 > 0 ? c->max_dim >> 13 : 1) * 4, 256);
+    c->off_gf[p] = off;
+    off = align_up(off + (size_t)(c->max_dim >> 13 > 0 ? c->max_dim >> 13 : 1) * 4, 1024);
   }
   c->sym_bytes = off;
   int64_t pw = mask_words(c->max_dim, n, 1);  // epp >= 1 bound
   off = 0;
   c->off_signs = off;
   off = align_up(off + (size_t)((c->max_dim + 31) / 32 + 2) * 4, 256);
+  c->off_signs_t = off;  // transposed sign bytes for the fused path's strided passes
+  off = align_up(off + (size_t)(c->max_dim / 8 + 16), 256);
   c->off_bitmap = off;
   off = align_up(off + (size_t)2 * n * n * pw * 4, 256);
   c->off_counts = off;
@@ -1409,6 +1442,7 @@ int optr_comm_create(optr_comm* out, int device, int rank, int n, int64_t max_le
     CK(cudaEventCreateWithFlags(&c->prep_ready[p], cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&c->done[p], cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&c->fork[p], cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&c->fused_done[p], cudaEventDisableTiming));
     CK(cudaStreamCreateWithFlags(&c->ws[p], cudaStreamNonBlocking));
   }
   CK(cudaDeviceSynchronize());
@@ -1454,6 +1488,7 @@ int optr_comm_destroy(optr_comm c) {
     cudaEventDestroy(c->prep_ready[p]);
     cudaEventDestroy(c->done[p]);
     cudaEventDestroy(c->fork[p]);
+    cudaEventDestroy(c->fused_done[p]);
     cudaStreamDestroy(c->ws[p]);
   }
   free(c);
@@ -1524,6 +1559,61 @@ int optr_tar_async(optr_comm c, const void* x, void* out, int64_t L, int dtype_i
                      received_out, stream, true);
 }
 
+}  // extern "C"
+
+namespace {
+void* g_fused_trace = nullptr;  // optr_debug_trace
+int g_fused_trace_cap = 0;
+// OPTR_FUSED=0 keeps the barrier-separated encode / aggregate / decode path.
+bool fused_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("OPTR_FUSED");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
+template <int T, int NW>
+int launch_fused_t(const TmaArgs& ae, const TmaArgs& ad, const SnkBuf& se, const SnkBuf& sd, const FusedArgs& f,
+                   cudaStream_t st) {
+  constexpr int S = 2;
+  const size_t smem = tma_fused_smem_bytes<T, S>();
+  auto kern = tma_fused_kernel<T, S, NW>;
+  int rc = set_smem_attr(kern, smem);
+  if (rc) return rc;
+  static int nsm = 0;
+  if (!nsm) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    if (nsm <= 0) nsm = 148;
+  }
+  int per_sm = 0;
+  const int threads = (1 << (T - 5)) + kAggThreads;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem) != cudaSuccess || per_sm < 1)
+    per_sm = 1;
+  KScope ks(OPTR_K_FUSED, st);
+  launch_ex(kern, dim3((unsigned)(nsm * per_sm)), dim3(threads), smem, st, ae, ad, se, sd, f);
+  return launch_check(kern, "tma_fused", T, 0, nsm * per_sm, 1, threads, smem);
+}
+
+int launch_fused(int T, const TmaArgs& ae, const TmaArgs& ad, const SnkBuf& se, const SnkBuf& sd,
+                 const FusedArgs& f, cudaStream_t st) {
+  switch (T * 100 + f.n) {
+    case 1302: return launch_fused_t<13, 2>(ae, ad, se, sd, f, st);
+    case 1304: return launch_fused_t<13, 4>(ae, ad, se, sd, f, st);
+    case 1308: return launch_fused_t<13, 8>(ae, ad, se, sd, f, st);
+    case 1402: return launch_fused_t<14, 2>(ae, ad, se, sd, f, st);
+    case 1404: return launch_fused_t<14, 4>(ae, ad, se, sd, f, st);
+    case 1408: return launch_fused_t<14, 8>(ae, ad, se, sd, f, st);
+    default: return -1;
+  }
+}
+}  // namespace
+
+extern "C" {
+
 static int tar_enqueue(optr_comm c, const void* x, void* out, int64_t L, int dtype_in, int dtype_out,
                        uint64_t job_seed, uint64_t bucket_id, uint64_t generation, int rotation, int ht,
                        const optr_mask_spec* masks, uint64_t* received_out, void* stream, bool async) {
@@ -1562,18 +1652,128 @@ static int tar_enqueue(optr_comm c, const void* x, void* out, int64_t L, int dty
   }
   Shards sh = make_shards(dim, n);
 
+  // ---- fused path: strided encode pass, then ONE persistent kernel for the
+  // contiguous encode pass + stage 1 + stage 2 + contiguous decode pass with
+  // per-tile flags over NVLink (no barriers), then the strided decode pass.
+  // Decided before prep, which also lays out the signs for it.
+  PassGeom fps[3];
+  const int nlog = ht ? log2_exact(dim) : 0;
+  const int np = ht ? plan_passes(nlog, fps, true) : 0;
+  const int Tc = np == 2 ? fps[0].ks : 0;
+  const bool fused = ht && fused_enabled() && tma_enabled() && stage2_push() && np == 2 && fps[0].cb == 0 &&
+                     (Tc == 13 || Tc == 14) && fps[1].cb == 3 && (fps[1].ks + 3 == 13 || fps[1].ks + 3 == 14) &&
+                     (n == 2 || n == 4 || n == 8) && sh.extra == 0 && (sh.base >> Tc) >= 1 &&
+                     ((sh.base >> Tc) << Tc) == sh.base && (L >> fps[1].lo) >= 1;
+  // (every input of this decision is the same on all ranks: a rank taking the
+  // other path would leave its peers waiting; the strided passes fall back
+  // per rank on their own, e.g. for unaligned x / out)
   const cudaStream_t ps = c->pstream;
   if (c->done_recorded[par]) CK(cudaStreamWaitEvent(ps, c->done[par], 0));
   CK(cudaMemsetAsync(counts, 0, (size_t)2 * n * 8, ps));
   PrepArgs pa;
   memset(&pa, 0, sizeof(pa));
   if (ht) fill_sign_args(pa, signs, dim, derive_seed(job_seed, bucket_id, generation));
+  uint8_t* const signs_t = fused ? (uint8_t*)(loc + c->off_signs_t) : nullptr;
+  if (fused) {
+    pa.signs_t = signs_t;
+    pa.t_lo = fps[1].lo;
+    pa.t_ks = fps[1].ks;
+  }
   const uint32_t* cbits = nullptr;
   if ((rc = setup_masks(pa, masks, dim, n, r, epp, bitmap, counts, me, me + 1, &cbits))) return rc;
   if ((rc = launch_prep(pa, ps))) return rc;
   CK(cudaEventRecord(c->prep_ready[par], ps));
   CK(cudaStreamWaitEvent(st, c->prep_ready[par], 0));
   MaskView mv{cbits, pa.pw, n, epp, make_divider((uint32_t)epp)};
+
+  if (fused) {
+    // fused kernels of consecutive calls never overlap (each spins on peers)
+    if (c->fused_recorded[par ^ 1]) CK(cudaStreamWaitEvent(st, c->fused_done[par ^ 1], 0));
+    {  // strided encode pass: x -> Y (signs, pad, upcast fused)
+      SrcEncode src;
+      memset(&src, 0, sizeof(src));
+      src.x[me] = x;
+      src.dtype = dtype_in;
+      src.L = L;
+      src.signs = signs;
+      src.signs_t = signs_t;
+      SnkBuf snk;
+      memset(&snk, 0, sizeof(snk));
+      snk.y[me] = Yp[me];
+      snk.scale = 1.f;
+      if ((rc = launch_pass(OPTR_K_ENC_FIRST, fps[1], nlog, me, 1, src, snk, st))) return rc;
+    }
+    TmaArgs ae, ad;
+    memset(&ae, 0, sizeof(ae));
+    memset(&ad, 0, sizeof(ad));
+    ae.ntiles = fps[0].ntiles;
+    ae.xw[me] = Yp[me];
+    ad.ntiles = fps[0].ntiles;
+    for (int o = 0; o < n; ++o) ad.A[o] = Ap[o];  // stage 2: pull from the owners
+    ad.n = n;
+    ad.r = r;
+    ad.shard_shift = log2_exact(sh.base);
+    ad.m = mv;
+    ad.dim = dim;
+    SnkBuf se, sd;
+    memset(&se, 0, sizeof(se));
+    memset(&sd, 0, sizeof(sd));
+    se.y[me] = Yp[me];
+    se.scale = (float)(1.0 / sqrt((double)dim));
+    sd.y[me] = Gp[me];
+    sd.scale = 1.f;
+    FusedArgs f;
+    memset(&f, 0, sizeof(f));
+    for (int i = 0; i < n; ++i) {
+      f.Y[i] = Yp[i];
+      f.A[i] = Ap[i];
+      f.eflag[i] = (unsigned int*)(c->peer[i] + c->off_ef[par]);
+      f.gflag[i] = (unsigned int*)(c->peer[i] + c->off_gf[par]);
+    }
+    f.ctr = c->chain_ctr[par];
+    f.epoch = ++c->fepoch[par];
+    f.n = n;
+    f.me = me;
+    f.r = r;
+    f.own = owned_shard(me, r, n);
+    f.ns = sh.base >> Tc;
+    f.shard_len = sh.base;
+    f.m = mv;
+    f.trace = (uint4*)g_fused_trace;
+    f.trace_cap = g_fused_trace_cap;
+    {
+      const char* e = getenv("OPTR_FUSED_EXP");
+      f.exp = (e && e[0] == '1') ? 1 : 0;
+    }
+    if ((rc = launch_fused(Tc, ae, ad, se, sd, f, st))) return rc < 0 ? OPTR_ECUDA : rc;
+    CK(cudaEventRecord(c->fused_done[par], st));
+    c->fused_recorded[par] = true;
+    {  // strided decode pass: G -> out (scale, signs, truncate, cast)
+      SrcBuf gb;
+      memset(&gb, 0, sizeof(gb));
+      gb.y[me] = Gp[me];
+      SnkDecode snk;
+      memset(&snk, 0, sizeof(snk));
+      snk.out[me] = out;
+      snk.count_base[me] = sh.len(owned_shard(me, r, n));
+      snk.dtype = dtype_out;
+      snk.L = L;
+      snk.signs = signs;
+      snk.signs_t = signs_t;
+      snk.count_extra = counts + n;
+      snk.count_stride = 1;
+      snk.dim = (double)dim;
+      if ((rc = launch_pass(OPTR_K_DEC_LAST, fps[1], nlog, me, 1, gb, snk, st))) return rc;
+    }
+    if (received_out) {
+      CK(cudaMemcpyAsync(received_out, counts + me, 8, cudaMemcpyDeviceToDevice, st));
+      CK(cudaMemcpyAsync(received_out + 1, counts + n + me, 8, cudaMemcpyDeviceToDevice, st));
+    }
+    CK(cudaEventRecord(c->done[par], st));
+    c->done_recorded[par] = true;
+    if (!async) CK(cudaStreamWaitEvent(caller, c->done[par], 0));
+    return OPTR_OK;
+  }
 
   // encode into my symmetric wire buffer
   if (ht) {
@@ -1680,6 +1880,12 @@ static int tar_enqueue(optr_comm c, const void* x, void* out, int64_t L, int dty
 }
 
 // ------------------------------------------------------ instrumentation
+int optr_debug_trace(void* dev_buf, int64_t per_cta) {
+  g_fused_trace = dev_buf;
+  g_fused_trace_cap = (int)per_cta;
+  return OPTR_OK;
+}
+
 int optr_timing_enable(int on) {
   std::lock_guard<std::mutex> lk(g_tmu);
   g_timing = on != 0;

@@ -174,6 +174,10 @@ struct PrepArgs {
   int64_t dim;
   u128 sign_state, sign_inc;
   int64_t sign_threads;
+  // optional second layout for strided passes (tma.cuh): sign byte of
+  // entries row*2^t_lo + 8*cg .. +7 at signs_t[cg * 2^t_ks + row]
+  uint8_t* signs_t;
+  int t_lo, t_ks;
   // masks
   int kind;
   int n, r, epp;
@@ -210,10 +214,20 @@ __device__ __forceinline__ uint64_t coin_base(const PrepArgs& a, int stage, int 
 __global__ void __launch_bounds__(256) prep_kernel(const __grid_constant__ PrepArgs a) {
   int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t < a.sign_threads) {
-    // signs 128t .. 128t+127 = outputs 64t .. 64t+63; Lemire bit of u32 halves
-    u128 s = jump(a.sign_state, a.sign_inc, (uint64_t)t * 64 + 1);
+    // signs 128c .. 128c+127 = outputs 64c .. 64c+63; Lemire bit of u32 halves.
+    // Natural layout: chunk c = t.  With the transposed layout too, a warp
+    // takes 32 consecutive rows of one 128-column chunk (coalesced bytes).
+    int64_t c = t, row = 0, cg16 = 0;
+    if (a.signs_t) {
+      const int64_t rows = 1LL << a.t_ks;
+      const int64_t w = t >> 5;
+      row = ((w % (rows >> 5)) << 5) | (t & 31);
+      cg16 = w / (rows >> 5);
+      c = ((row << a.t_lo) >> 7) + cg16;
+    }
+    u128 s = jump(a.sign_state, a.sign_inc, (uint64_t)c * 64 + 1);
     const int64_t nwords = (a.dim + 31) >> 5;
-    const int64_t w0 = t * 4;
+    const int64_t w0 = c * 4;
 #pragma unroll
     for (int wd = 0; wd < 4; ++wd) {
       uint32_t word = 0;
@@ -229,6 +243,12 @@ __global__ void __launch_bounds__(256) prep_kernel(const __grid_constant__ PrepA
         int64_t valid = a.dim - wi * 32;  // zero the bits past dim
         if (valid < 32) word &= (1u << valid) - 1u;
         a.signs[wi] = word;
+        if (a.signs_t) {
+          const int64_t rows = 1LL << a.t_ks;
+#pragma unroll
+          for (int b = 0; b < 4; ++b)
+            a.signs_t[(cg16 * 16 + wd * 4 + b) * rows + row] = (uint8_t)(word >> (8 * b));
+        }
       }
     }
     return;
@@ -306,6 +326,7 @@ struct SrcEncode {
   int dtype;
   int64_t L;
   const uint32_t* signs;
+  const uint8_t* signs_t;  // optional transposed sign bytes (strided TMA pass, PrepArgs)
   struct B {
     const void* x;
     int dtype;
@@ -492,6 +513,7 @@ struct SnkDecode {
   int dtype;
   int64_t L;
   const uint32_t* signs;
+  const uint8_t* signs_t;  // optional transposed sign bytes (strided TMA pass, PrepArgs)
   const unsigned long long* count_extra;  // device: + received entries (may be null)
   int64_t count_base[kMaxW];              // host-known part of count
   int count_stride;

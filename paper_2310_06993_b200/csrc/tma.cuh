@@ -43,6 +43,9 @@ struct TmaArgs {
   int dtype;
   int64_t L;
   const uint32_t* signs;
+  // strided passes: transposed sign bytes (one 2^ks-byte column per 8-column
+  // tile, loaded with the tile) for the encode source / decode epilogue
+  const uint8_t* signs_t;
   // TS_GATHER (collectives.py:140-150): owner shards, stage-2 masks
   const float* A[kMaxW];
   int n, r;
@@ -71,6 +74,9 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
       "}\n" ::"r"(smem_u32(b)),
       "r"(parity)
       : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
 }
 __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
                                             int c2) {
@@ -111,6 +117,33 @@ __host__ __device__ constexpr size_t tma_smem_bytes() {
   return S * tma_stage_bytes<T>() + 64 + 1024;
 }
 
+// Issue the bulk loads of contiguous tile t into stage buffer `st` (sign
+// words after the tile for the encode source).
+template <int T, int SK>
+__device__ __forceinline__ void tile_issue_contig(const TmaArgs& a, int w, int64_t t, unsigned char* st,
+                                                  uint64_t* bar) {
+  const int64_t g0 = t << T;
+  if (SK == TS_GATHER) {
+    const int j = (int)(g0 >> a.shard_shift);
+    const int64_t e0 = g0 - ((int64_t)j << a.shard_shift);
+    mbar_expect_tx(bar, (uint32_t)(sizeof(float) << T));
+    bulk_load(st, a.A[shard_owner(j, a.r, a.n)] + e0, (uint32_t)(sizeof(float) << T), bar);
+  } else if (SK == TS_BUF) {
+    mbar_expect_tx(bar, (uint32_t)(sizeof(float) << T));
+    bulk_load(st, (const float*)a.xw[w] + g0, (uint32_t)(sizeof(float) << T), bar);
+  } else {
+    const int lsh = a.dtype == OPTR_BF16 ? 1 : 2;
+    int64_t valid = a.L - g0;
+    if (valid > (1 << T)) valid = 1 << T;
+    if (valid < 0) valid = 0;
+    const uint32_t bytes = (uint32_t)((valid << lsh) & ~15LL);
+    const uint32_t sbytes = (uint32_t)(sizeof(uint32_t) << (T - 5));
+    mbar_expect_tx(bar, bytes + sbytes);
+    if (bytes) bulk_load(st, (const unsigned char*)a.xw[w] + (g0 << lsh), bytes, bar);
+    bulk_load(st + (sizeof(float) << T), a.signs + (g0 >> 5), sbytes, bar);
+  }
+}
+
 // Issue the loads of tile t into stage buffer `st` (sign words after the tile).
 template <int T, bool STRIDED, int SK, int CBW>
 __device__ __forceinline__ void tile_issue(const TmaMaps& maps, const TmaArgs& a, int w, int64_t t,
@@ -121,7 +154,27 @@ __device__ __forceinline__ void tile_issue(const TmaMaps& maps, const TmaArgs& a
     const int c0 = (int)((t & ((1LL << cgb) - 1)) << CBW);
     const int outer = (int)(t >> cgb);
     const int nbox = (1 << KS) / a.box_rows;
-    mbar_expect_tx(bar, (uint32_t)(sizeof(float) << T));
+    if (SK == TS_ENC) {
+      // x as a [rows_full][2^lo] tensor (dtype of x): boxes of the full rows;
+      // rows past the map come back zero-filled (full-box transaction) and
+      // round A reads the partial row from global memory
+      const int esz = a.dtype == OPTR_BF16 ? 2 : 4;
+      const int64_t rows_full = a.L >> a.lo;
+      uint32_t bytes = 0;
+      for (int b = 0; b < nbox; ++b)
+        if ((int64_t)b * a.box_rows < rows_full) bytes += (uint32_t)(esz * a.box_rows) << CBW;
+      const uint32_t sbytes = a.signs_t ? (1u << KS) : 0u;  // the tile's sign column
+      mbar_expect_tx(bar, bytes + sbytes);
+      for (int b = 0; b < nbox; ++b) {
+        const int row = b * a.box_rows;
+        if (row < rows_full) tma_load_3d(st + ((size_t)row << CBW) * esz, &maps.m[w], bar, c0, row, 0);
+      }
+      if (sbytes) bulk_load(st + (sizeof(float) << T), a.signs_t + ((size_t)(c0 >> CBW) << KS), sbytes, bar);
+      return;
+    }
+    const uint32_t sbytes = (SK == TS_BUF && a.signs_t) ? (1u << KS) : 0u;  // decode epilogue signs
+    mbar_expect_tx(bar, (uint32_t)(sizeof(float) << T) + sbytes);
+    if (sbytes) bulk_load(st + (sizeof(float) << T), a.signs_t + ((size_t)(c0 >> CBW) << KS), sbytes, bar);
     for (int b = 0; b < nbox; ++b) {
       const int row = b * a.box_rows;
       float* dst = (float*)st + ((size_t)row << CBW);
@@ -134,26 +187,7 @@ __device__ __forceinline__ void tile_issue(const TmaMaps& maps, const TmaArgs& a
       }
     }
   } else {
-    const int64_t g0 = t << T;
-    if (SK == TS_GATHER) {
-      const int j = (int)(g0 >> a.shard_shift);
-      const int64_t e0 = g0 - ((int64_t)j << a.shard_shift);
-      mbar_expect_tx(bar, (uint32_t)(sizeof(float) << T));
-      bulk_load(st, a.A[shard_owner(j, a.r, a.n)] + e0, (uint32_t)(sizeof(float) << T), bar);
-    } else if (SK == TS_BUF) {
-      mbar_expect_tx(bar, (uint32_t)(sizeof(float) << T));
-      bulk_load(st, (const float*)a.xw[w] + g0, (uint32_t)(sizeof(float) << T), bar);
-    } else {
-      const int lsh = a.dtype == OPTR_BF16 ? 1 : 2;
-      int64_t valid = a.L - g0;
-      if (valid > (1 << T)) valid = 1 << T;
-      if (valid < 0) valid = 0;
-      const uint32_t bytes = (uint32_t)((valid << lsh) & ~15LL);
-      const uint32_t sbytes = (uint32_t)(sizeof(uint32_t) << (T - 5));
-      mbar_expect_tx(bar, bytes + sbytes);
-      if (bytes) bulk_load(st, (const unsigned char*)a.xw[w] + (g0 << lsh), bytes, bar);
-      bulk_load(st + (sizeof(float) << T), a.signs + (g0 >> 5), sbytes, bar);
-    }
+    tile_issue_contig<T, SK>(a, w, t, st, bar);
   }
 }
 
@@ -177,13 +211,24 @@ __device__ __forceinline__ float4 gather_mask4(const TmaArgs& a, int q, uint8_t*
   return make_float4(k0 ? v.x : 0.f, k1 ? v.y : 0.f, k2 ? v.z : 0.f, k3 ? v.w : 0.f);
 }
 
+// CTA barrier (BAR = 0) or named barrier BAR over the first NT threads, for
+// kernels whose CTA holds several independent warp groups.
+template <int BAR, int NT>
+__device__ __forceinline__ void group_sync() {
+  if constexpr (BAR == 0) {
+    __syncthreads();
+  } else {
+    asm volatile("bar.sync %0, %1;" ::"n"(BAR), "n"(NT) : "memory");
+  }
+}
+
 // One tile of a TMA pass, from its filled stage buffer `sb` to its issued
 // result.  `refill()` is called by thread 0 once the stage may be reused for
 // the next load: for a contiguous tile right after the tile has been read
 // (the results then leave by STG), for a strided tile after its TMA store
 // group is committed (the refill policy decides which stage to wait for).
-template <int T, bool STRIDED, int SK, class Snk, int CBW, class Refill>
-__device__ __forceinline__ void tma_tile(const TmaMaps& maps, const CUtensorMap& dst, const TmaArgs& a,
+template <int T, bool STRIDED, int SK, class Snk, int CBW, int BAR = 0, class Refill>
+__device__ __forceinline__ void tma_tile(const TmaMaps* maps, const CUtensorMap* dst, const TmaArgs& a,
                                          const typename Snk::B& d, int worker, uint8_t* gotw, int64_t t,
                                          unsigned char* sb, Refill&& refill) {
   constexpr int CB = STRIDED ? CBW : 0;  // untransformed column bits (8 or 32 columns)
@@ -208,7 +253,7 @@ __device__ __forceinline__ void tma_tile(const TmaMaps& maps, const CUtensorMap&
   // ---- round A: dense tile, float4 groups, fused source transform
   int64_t bulk_end = 0;
   bool enc_fast = true;
-  if constexpr (SK == TS_ENC) {
+  if constexpr (SK == TS_ENC && !STRIDED) {
     const int lsh = a.dtype == OPTR_BF16 ? 1 : 2;
     bulk_end = g0 + ((((a.L - g0) << lsh) & ~15LL) >> lsh);
     enc_fast = g0 + (1 << T) <= bulk_end;
@@ -218,7 +263,31 @@ __device__ __forceinline__ void tma_tile(const TmaMaps& maps, const CUtensorMap&
     const int i = b0 + roff(P, 0, 4 * m);
     const int64_t g = STRIDED ? (g0 + ((int64_t)(i >> CB) << a.lo) + (i & CM)) : (g0 + i);
     float4 q4;
-    if constexpr (SK == TS_ENC) {
+    if constexpr (SK == TS_ENC && STRIDED) {
+      // strided encode (hadamard.py:93-102 with the passes reordered): the
+      // tile's full rows came by TMA; the partial row and padding rows here
+      if (a.dtype == OPTR_BF16) {
+        const uint2 u = *reinterpret_cast<const uint2*>(sb + (size_t)i * 2);
+        const float2 fa = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.x));
+        const float2 fb = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.y));
+        q4 = make_float4(fa.x, fa.y, fb.x, fb.y);
+      } else {
+        q4 = *reinterpret_cast<const float4*>(tile + i);
+      }
+      if ((g >> a.lo) >= (a.L >> a.lo)) {
+        float e[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+          if (g + c < a.L) e[c] = load_elem(a.xw[worker], a.dtype, g + c);
+        q4 = make_float4(e[0], e[1], e[2], e[3]);
+      }
+      const uint32_t sw = a.signs_t ? (uint32_t)sb[(sizeof(float) << T) + (i >> CB)] >> (i & 7)
+                                    : __ldg(a.signs + (g >> 5)) >> (g & 31);
+      q4 = make_float4(__int_as_float(__float_as_int(q4.x) ^ ((~sw & 1u) << 31)),
+                       __int_as_float(__float_as_int(q4.y) ^ ((~sw & 2u) << 30)),
+                       __int_as_float(__float_as_int(q4.z) ^ ((~sw & 4u) << 29)),
+                       __int_as_float(__float_as_int(q4.w) ^ ((~sw & 8u) << 28)));
+    } else if constexpr (SK == TS_ENC) {
       if (a.dtype == OPTR_BF16) {
         const uint2 u = *reinterpret_cast<const uint2*>(sb + (size_t)i * 2);
         const float2 fa = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.x));
@@ -249,24 +318,36 @@ __device__ __forceinline__ void tma_tile(const TmaMaps& maps, const CUtensorMap&
     v[4 * m + 3] = q4.w;
   }
   bfly32<P.xm[0]>(v);
-  __syncthreads();  // the dense tile has been read
+  // strided decode epilogue with transposed signs: take this thread's
+  // last-round sign nibbles now, before the padded layout covers them
+  uint32_t dsig = 0;
+  if constexpr (STRIDED && std::is_same<Snk, SnkDecode>::value) {
+    if (a.signs_t) {
+#pragma unroll
+      for (int m = 0; m < 8; ++m) {
+        const int i = b2 + roff(P, LR, 4 * m);
+        dsig |= (((uint32_t)sb[(sizeof(float) << T) + (i >> CB)] >> (i & 7)) & 0xFu) << (4 * m);
+      }
+    }
+  }
+  group_sync<BAR, (1 << (T - 5))>();  // the dense tile has been read
   // rounds B, C in the padded layout (it ends exactly where the stage's
   // sign words end; those were consumed in round A)
 #pragma unroll
   for (int j = 0; j < 32; ++j) tile[p0 + pad(roff(P, 0, j))] = v[j];
-  __syncthreads();
+  group_sync<BAR, (1 << (T - 5))>();
 #pragma unroll
   for (int j = 0; j < 32; ++j) v[j] = tile[p1 + pad(roff(P, 1, j))];
   bfly32<P.xm[1]>(v);
   if constexpr (P.nr == 3) {
 #pragma unroll
     for (int j = 0; j < 32; ++j) tile[p1 + pad(roff(P, 1, j))] = v[j];
-    __syncthreads();
+    group_sync<BAR, (1 << (T - 5))>();
 #pragma unroll
     for (int j = 0; j < 32; ++j) v[j] = tile[p2 + pad(roff(P, 2, j))];
     bfly32<P.xm[2]>(v);
   }
-  __syncthreads();  // the padded tile has been read: the stage is free
+  group_sync<BAR, (1 << (T - 5))>();  // the padded tile has been read: the stage is free
   if constexpr (!STRIDED) {
     if (tid == 0) refill();
     if constexpr (P.pos[LR][0] == 0 && P.pos[LR][1] == 1) {
@@ -289,7 +370,7 @@ __device__ __forceinline__ void tma_tile(const TmaMaps& maps, const CUtensorMap&
     for (int m = 0; m < 8; ++m) {
       const int i = b2 + roff(P, LR, 4 * m);
       const int64_t g = g0 + ((int64_t)(i >> CB) << a.lo) + (i & CM);
-      const uint32_t w = __ldg(d.signs + (g >> 5)) >> (g & 31);
+      const uint32_t w = a.signs_t ? dsig >> (4 * m) : __ldg(d.signs + (g >> 5)) >> (g & 31);
       float4 o4 = make_float4(v[4 * m] * d.scale, v[4 * m + 1] * d.scale, v[4 * m + 2] * d.scale,
                               v[4 * m + 3] * d.scale);
       o4 = make_float4(__int_as_float(__float_as_int(o4.x) ^ ((~w & 1u) << 31)),
@@ -312,14 +393,14 @@ __device__ __forceinline__ void tma_tile(const TmaMaps& maps, const CUtensorMap&
       }
     }
     fence_async_smem();
-    __syncthreads();
+    group_sync<BAR, (1 << (T - 5))>();
     if (tid == 0) {
       const int c0 = (int)((t & ((1LL << cgb) - 1)) << CB);
       const int nbox = (1 << (T - CB)) / a.box_rows;
       const int esz = d.dtype == OPTR_BF16 ? 2 : 4;
       for (int b = 0; b < nbox; ++b)
         if ((int64_t)b * a.box_rows < rows_full)
-          tma_store_3d(&dst, sb + ((size_t)b * a.box_rows << CB) * esz, c0, b * a.box_rows, 0);
+          tma_store_3d(dst, sb + ((size_t)b * a.box_rows << CB) * esz, c0, b * a.box_rows, 0);
       bulk_commit();
       refill();
     }
@@ -340,13 +421,13 @@ __device__ __forceinline__ void tma_tile(const TmaMaps& maps, const CUtensorMap&
       for (int j = 0; j < 32; ++j) tile[b2 + roff(P, LR, j)] = v[j] * sc;
     }
     fence_async_smem();
-    __syncthreads();
+    group_sync<BAR, (1 << (T - 5))>();
     if (tid == 0) {
       const int c0 = (int)((t & ((1LL << cgb) - 1)) << CB);
       const int outer = SK == TS_GATHER ? 0 : (int)(t >> cgb);
       const int nbox = (1 << (T - CB)) / a.box_rows;
       for (int b = 0; b < nbox; ++b)
-        tma_store_3d(&dst, tile + ((size_t)b * a.box_rows << CB), c0, b * a.box_rows, outer);
+        tma_store_3d(dst, tile + ((size_t)b * a.box_rows << CB), c0, b * a.box_rows, outer);
       bulk_commit();
       refill();
     }
@@ -391,7 +472,7 @@ __global__ void __launch_bounds__(1 << (T - 5)) tma_pass_kernel(const __grid_con
     const int s = k % kStages;
     unsigned char* const sb = base + s * SB;
     mbar_wait(&full[s], (uint32_t)((k / kStages) & 1));
-    tma_tile<T, STRIDED, SK, Snk, CBW>(maps, dst, a, d, worker, gotw, t, sb, [&]() {
+    tma_tile<T, STRIDED, SK, Snk, CBW>(&maps, &dst, a, d, worker, gotw, t, sb, [&]() {
       if constexpr (!STRIDED) {
         // contiguous: the stage was read; refill it while the results leave by STG
         if (t + kStages * stride < a.ntiles)
@@ -448,9 +529,6 @@ __device__ __forceinline__ unsigned int ld_acquire_gpu(const unsigned int* p) {
 }
 __device__ __forceinline__ void fence_proxy_async_global() {
   asm volatile("fence.proxy.async.global;" ::: "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
 }
 
 template <int T, int kStages, int SK0, class Snk1, int CBW>
@@ -537,7 +615,7 @@ __global__ void __launch_bounds__(1 << (T - 5)) tma_chain_kernel(const __grid_co
     const int64_t t = slot_tile[s];  // read before tma_tile's first barrier; refills come after it
     if (cs.jpass[j] == 0) {
       uint8_t* const gotw = (SK0 == TS_GATHER && a0.got) ? a0.got + (int64_t)w * a0.dim : nullptr;
-      tma_tile<T, false, SK0, SnkBuf, CBW>(maps1, dmaps1.m[w], a0, snk0.bind(w), w, gotw, t, sb, [&]() {
+      tma_tile<T, false, SK0, SnkBuf, CBW>(&maps1, &dmaps1.m[w], a0, snk0.bind(w), w, gotw, t, sb, [&]() {
         if (lag >= 0) {
           bulk_wait_read0();
           claim_issue(lag);
@@ -552,7 +630,7 @@ __global__ void __launch_bounds__(1 << (T - 5)) tma_chain_kernel(const __grid_co
         atomicAdd(done + w, 1u);
       }
     } else {
-      tma_tile<T, true, TS_BUF, Snk1, CBW>(maps1, dmaps1.m[w], a1, snk1.bind(w), w, nullptr, t, sb, [&]() {
+      tma_tile<T, true, TS_BUF, Snk1, CBW>(&maps1, &dmaps1.m[w], a1, snk1.bind(w), w, nullptr, t, sb, [&]() {
         if (lag >= 0) {
           bulk_wait_read1();  // the previous strided store has left its slot
           claim_issue(lag);
@@ -678,6 +756,372 @@ __global__ void __launch_bounds__(CH / 4) tma_agg_kernel(const __grid_constant__
       } else {
         st4(A + e, res);
       }
+    }
+  }
+}
+
+}  // namespace optr
+
+namespace optr {
+
+// ------------------------------------ fused multi-GPU TAR core (one rank)
+// The encode's last (contiguous) pass, TAR stage 1 at the owner, stage 2
+// (owner push) and the decode's first (contiguous) pass of one rank in ONE
+// persistent kernel, so NVLink traffic overlaps the FWHT tile by tile
+// (collectives.py:97-150 between the runner's encode and decode,
+// runner.py:219-258).  The strided passes run before and after it.
+//
+// Tiles t hold 2^T entries; shard j = tiles [j*ns, (j+1)*ns).  Each CTA has
+// two warp groups with their own ticket queues:
+//   E/D group (2^(T-5) threads): all E tickets (row order, row k = tiles
+//     {j*ns + k}), then all D tickets (row order)
+//     E(t)  encode tile t of my wire vector Y in place (scale 1/sqrt(dim)),
+//           then eflag[t] = epoch in my memory (peers poll it over NVLink)
+//     D(t)  once my gflag[t] == epoch: pull tile t from its owner's aggregate
+//           (one TMA bulk copy over NVLink, stage-2 masks applied as it is
+//           read) and decode it into my G
+//   A group (kAggThreads threads): tiles of my shard in order; for each, wait
+//     for eflag[t] at every rank, stream the tile from every rank's Y in
+//     kAggCh-entry chunks through a ring, masked fp64 mean in ascending node
+//     order into my aggregate A; then gflag[t] = epoch at every rank.
+// E jobs wait for nothing, A jobs only for E jobs, D jobs only for A jobs of
+// the same row, and every queue is claimed in the same order on all ranks,
+// so nothing waits on a job that cannot run.  A D job's load is deferred
+// (never spun on at claim time) until its CTA has finished every earlier job.
+struct FusedArgs {
+  const float* Y[kMaxW];       // every rank's wire vector (peer-mapped)
+  float* A[kMaxW];             // every rank's owner-shard aggregate (peer-mapped)
+  unsigned int* eflag[kMaxW];  // every rank's encode-tile flags
+  unsigned int* gflag[kMaxW];  // every rank's receive-tile flags
+  unsigned int* ctr;           // local [0] E/D ticket, [1] CTAs done, [2] A ticket (reset by the last CTA)
+  unsigned int epoch;
+  int n, me, r, own;
+  int64_t ns;                  // tiles per shard
+  int64_t shard_len;
+  MaskView m;
+  uint4* trace;   // debug (optr_debug_trace): per CTA [cap/2 E/D jobs | cap/2 A tiles]
+  int trace_cap;
+  int exp;        // experiment (OPTR_FUSED_EXP=1): E / D keep their flags and waits, skip the tiles
+};
+
+__device__ __forceinline__ unsigned int ld_acquire_sys(const unsigned int* p) {
+  unsigned int v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(unsigned int* p, unsigned int v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+// Flags of the fused kernel.  Every reader reaches the flagged data through
+// the writer GPU's L2 (its own HBM or NVLink peer requests), so a writer
+// needs its data visible at GPU scope (__threadfence after a group barrier,
+// cumulative) before a relaxed system-scope flag store; a reader polls with
+// relaxed loads and issues its (TMA) reads only after seeing the flag.
+// System-scope releases / fences here cost microseconds each under NVLink load.
+__device__ __forceinline__ unsigned int ld_relaxed_sys(const unsigned int* p) {
+  unsigned int v;
+  asm volatile("ld.relaxed.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed_sys(unsigned int* p, unsigned int v) {
+  asm volatile("st.relaxed.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// Spin until *p >= v (acquire, system scope).  A peer that never arrives is
+// a protocol bug: trap after 10 s instead of hanging the GPU.
+__device__ __noinline__ void spin_ge_sys(const unsigned int* p, unsigned int v) {
+  if (ld_relaxed_sys(p) >= v) return;
+  const uint64_t t0 = globaltimer_ns();
+  while (ld_relaxed_sys(p) < v) {
+    __nanosleep(64);
+    if (globaltimer_ns() - t0 > 10000000000ull) {
+      printf("optr: fused kernel wait timed out (flag %p, have %u, want %u)\n", p, ld_relaxed_sys(p), v);
+      __trap();
+    }
+  }
+}
+
+constexpr int kAggThreads = 256;
+// entries per rank per aggregate chunk: 4096/n (>= one float4 per thread)
+__host__ __device__ constexpr int agg_chunk(int n) { return 4096 / n > 1024 ? 4096 / n : 1024; }
+constexpr int kAggBytes = 64 * 1024;  // A-group ring
+
+template <int T, int S>
+__host__ __device__ constexpr size_t tma_fused_smem_bytes() {
+  return S * tma_stage_bytes<T>() + kAggBytes + 256 + 1024;
+}
+
+enum FusedJob { FJ_END = -1, FJ_E = 0, FJ_D = 2, FJ_NOP = 3 };
+
+template <int T, int kStages, int NW>
+__global__ void __launch_bounds__((1 << (T - 5)) + kAggThreads)
+    tma_fused_kernel(const __grid_constant__ TmaArgs ae, const __grid_constant__ TmaArgs ad,
+                     const __grid_constant__ SnkBuf se, const __grid_constant__ SnkBuf sd,
+                     const __grid_constant__ FusedArgs f) {
+  constexpr int NED = 1 << (T - 5);
+  constexpr size_t SB = tma_stage_bytes<T>();
+  constexpr int kAggCh = agg_chunk(NW);
+  constexpr int SA = kAggBytes / (NW * kAggCh * 4) < 16 ? kAggBytes / (NW * kAggCh * 4) : 16;
+  static_assert(NW >= 2 && SA >= 2, "aggregate ring needs two stages");
+  extern __shared__ __align__(16) unsigned char smraw[];
+  unsigned char* const base = smraw + ((1024u - (smem_u32(smraw) & 1023u)) & 1023u);
+  float* const abuf = reinterpret_cast<float*>(base + kStages * SB);
+  uint64_t* const full = reinterpret_cast<uint64_t*>(base + kStages * SB + kAggBytes);
+  uint64_t* const abar = full + kStages;
+  int* const slot_kind = reinterpret_cast<int*>(abar + SA);
+  int64_t* const slot_tile = reinterpret_cast<int64_t*>(slot_kind + 4);
+  int* const aslot = reinterpret_cast<int*>(slot_tile + 4);  // A ring: (tile << 8 | chunk), -1 end
+  const int tid = threadIdx.x;
+  constexpr int n = NW;
+  const int me = f.me;
+  const int64_t ns = f.ns;
+
+  if (tid == 0) {
+    for (int s = 0; s < kStages; ++s) mbar_init(&full[s], 1);
+    for (int s = 0; s < SA; ++s) mbar_init(&abar[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+
+  if (tid < NED) {
+    // ------------------------------------------------ E/D warp group
+    // tickets [0, n*ns): E in row order; [n*ns, 2*n*ns): D in row order (E
+    // never queues behind a D; the D rows drain as the owners publish)
+    const int64_t nt = (int64_t)n * ns;
+    const int64_t total = 2 * nt;
+    bool ended = false;
+    unsigned deferred = 0;
+    int64_t pend_e = -1;  // thread 0: encoded tile whose eflag is not yet released
+    auto release_e = [&]() {
+      if (pend_e >= 0) {
+        __threadfence();  // cumulative over the group (its stores came before a group barrier)
+        st_relaxed_sys(f.eflag[me] + pend_e, f.epoch);
+        pend_e = -1;
+      }
+    };
+    auto claim_issue = [&](int s) {
+      int kind = FJ_END;
+      int64_t t = 0;
+      if (!ended) {
+        const int64_t tk = atomicAdd(f.ctr, 1u);
+        if (tk >= total) {
+          ended = true;
+        } else {
+          const int64_t row = (tk % nt) / n;
+          const int u = (int)(tk % n);
+          kind = tk < nt ? FJ_E : FJ_D;
+          t = (int64_t)u * ns + row;
+        }
+      }
+      slot_kind[s] = kind;
+      slot_tile[s] = t;
+      if (kind == FJ_E && !f.exp) {
+        tile_issue_contig<T, TS_BUF>(ae, me, t, base + s * SB, &full[s]);
+      } else if (kind == FJ_D) {
+        if (ld_relaxed_sys(f.gflag[me] + t) >= f.epoch) {
+          fence_proxy_async_global();
+          if (f.exp) mbar_arrive(&full[s]);
+          else tile_issue_contig<T, TS_GATHER>(ad, me, t, base + s * SB, &full[s]);
+        } else {
+          deferred |= 1u << s;
+        }
+      } else {
+        mbar_arrive(&full[s]);  // no-op / end: nothing through the ring
+      }
+    };
+    if (tid == 0)
+      for (int s = 0; s < kStages; ++s) claim_issue(s);
+    uint4* const tr = f.trace ? f.trace + (size_t)blockIdx.x * f.trace_cap : nullptr;
+    for (int k = 0;; ++k) {
+      const int s = k % kStages;
+      unsigned char* const sb = base + s * SB;
+      const uint32_t tb = tr && tid == 0 ? (uint32_t)globaltimer_ns() : 0u;
+      if (tid == 0 && (deferred >> s & 1u)) {
+        release_e();  // never wait while holding an unreleased encode
+        const int64_t t = slot_tile[s];
+        spin_ge_sys(f.gflag[me] + t, f.epoch);
+        fence_proxy_async_global();
+        if (f.exp) mbar_arrive(&full[s]);
+        else tile_issue_contig<T, TS_GATHER>(ad, me, t, sb, &full[s]);
+        deferred &= ~(1u << s);
+      }
+      mbar_wait(&full[s], (uint32_t)((k / kStages) & 1));
+      const int kind = slot_kind[s];
+      const int64_t t = slot_tile[s];
+      if (kind == FJ_END) {
+        if (tid == 0) release_e();
+        break;
+      }
+      if (tid == 0 && kind != FJ_E) release_e();
+      const uint32_t trd = tr && tid == 0 ? (uint32_t)globaltimer_ns() : 0u;
+      if (f.exp && kind != FJ_NOP) {
+        group_sync<1, NED>();
+        if (tid == 0) {
+          if (kind == FJ_E) st_relaxed_sys(f.eflag[me] + t, f.epoch);
+          claim_issue(s);
+        }
+      } else if (kind == FJ_E) {
+        tma_tile<T, false, TS_BUF, SnkBuf, 3, 1>(nullptr, nullptr, ae, se.bind(me), me, nullptr, t, sb,
+                                                 [&]() { claim_issue(s); });
+        // released after the group's next job (or before any wait / exit), so
+        // the fence finds the tile's stores drained instead of stalling on them
+        group_sync<1, NED>();
+        if (tid == 0) {
+          release_e();
+          pend_e = t;
+        }
+      } else if (kind == FJ_D) {
+        tma_tile<T, false, TS_GATHER, SnkBuf, 3, 1>(nullptr, nullptr, ad, sd.bind(me), me, nullptr, t, sb,
+                                                    [&]() { claim_issue(s); });
+      } else {
+        // no-op ticket: every thread has read the slot (it is only rewritten
+        // after this barrier)
+        group_sync<1, NED>();
+        if (tid == 0) claim_issue(s);
+      }
+      if (tr && tid == 0 && k < f.trace_cap / 2)
+        tr[k] = make_uint4(((uint32_t)kind << 28) | (uint32_t)t, tb, trd, (uint32_t)globaltimer_ns());
+    }
+  } else {
+    // ------------------------------------------------ A warp group
+    // TAR stage 1 + stage-2 push (collectives.py:113-137) of my shard's tiles
+    const int ta = tid - NED;
+    constexpr int cpt = (1 << T) / kAggCh;  // chunks per tile
+    const int64_t soff = (int64_t)f.own * f.shard_len;
+    // producer state (ta == 0).  A new tile whose encodes are not all in is
+    // not waited for here: its stages are queued (pend_*) and the wait
+    // happens when the consumer reaches its first chunk, i.e. after the
+    // previous tile's gflag is published (peers' E jobs may be queued
+    // behind D jobs that wait for exactly that flag).
+    int64_t cur = -1;  // current tile (index inside my shard)
+    int nxt = cpt;     // next chunk of it to issue
+    bool aend = false;
+    int pend_first = -1, pend_count = 0;
+    uint4* const tra = f.trace ? f.trace + (size_t)blockIdx.x * f.trace_cap + f.trace_cap / 2 : nullptr;
+    int ntr = 0;
+    uint32_t t_claim = 0, t_ready = 0;
+    auto tile_ready = [&](int64_t k) {
+      const int64_t t = (int64_t)f.own * ns + k;
+      unsigned int v[NW];
+#pragma unroll
+      for (int q = 0; q < n; ++q) v[q] = ld_relaxed_sys(f.eflag[q] + t);  // n loads in flight
+      bool ok = true;
+#pragma unroll
+      for (int q = 0; q < n; ++q) ok = ok && v[q] >= f.epoch;
+      return ok;
+    };
+    auto issue_chunk = [&](int s) {
+      aslot[s] = (int)((cur << 8) | nxt);
+      const uint32_t bytes = kAggCh * sizeof(float);
+      const int64_t e = (cur << T) + (int64_t)nxt * kAggCh;  // entry inside my shard
+      mbar_expect_tx(&abar[s], bytes * n);
+      for (int i = 0; i < n; ++i)
+        bulk_load(abuf + ((size_t)s * n + i) * kAggCh, f.Y[i] + soff + e, bytes, &abar[s]);
+      ++nxt;
+    };
+    auto issue_next = [&](int s) {
+      if (pend_first >= 0) {  // the queued tile takes this stage too (SA <= cpt)
+        ++pend_count;
+        return;
+      }
+      if (!aend && nxt == cpt) {
+        const int64_t k = atomicAdd(f.ctr + 2, 1u);
+        if (k >= ns) {
+          aend = true;
+        } else {
+          cur = k;
+          nxt = 0;
+          if (tra) t_claim = (uint32_t)globaltimer_ns();
+          if (!tile_ready(k)) {
+            pend_first = s;
+            pend_count = 1;
+            return;
+          }
+          if (tra) t_ready = (uint32_t)globaltimer_ns();
+          fence_proxy_async_global();
+        }
+      }
+      if (aend) {
+        aslot[s] = -1;
+        mbar_arrive(&abar[s]);
+        return;
+      }
+      issue_chunk(s);
+    };
+    if (ta == 0)
+      for (int s = 0; s < SA; ++s) issue_next(s);
+    static_assert(SA <= (1 << T) / kAggCh, "a queued tile covers every queued stage");
+    static_assert(kAggCh % (4 * kAggThreads) == 0, "whole float4 groups per thread");
+    for (int k = 0;; ++k) {
+      const int s = k % SA;
+      if (ta == 0 && s == pend_first) {
+        const int64_t t = (int64_t)f.own * ns + cur;
+        for (int q = 0; q < n; ++q) spin_ge_sys(f.eflag[q] + t, f.epoch);
+        if (tra) t_ready = (uint32_t)globaltimer_ns();
+        fence_proxy_async_global();
+        const int first = pend_first, cnt = pend_count;
+        pend_first = -1;
+        pend_count = 0;
+        for (int i = 0; i < cnt; ++i) issue_chunk((first + i) % SA);
+      }
+      mbar_wait(&abar[s], (uint32_t)((k / SA) & 1));
+      const int code = aslot[s];
+      if (code < 0) break;
+      const int64_t tl = code >> 8;
+      const int chunk = code & 255;
+#pragma unroll
+      for (int v = 0; v < kAggCh / (4 * kAggThreads); ++v) {
+        const int off = 4 * (ta + v * kAggThreads);
+        const int64_t e = (tl << T) + (int64_t)chunk * kAggCh + off;
+        const float* src = abuf + (size_t)s * n * kAggCh + off;
+        double acc[4] = {0.0, 0.0, 0.0, 0.0};
+        uint32_t c4[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+        for (int i = 0; i < n; ++i) {
+          const float4 x4 = *reinterpret_cast<const float4*>(src + (size_t)i * kAggCh);
+          const uint32_t kk = i == me ? 0xFu : keep4(f.m.row(0, me, i), (uint32_t)e, f.m);
+          acc[0] += (kk & 1u) ? (double)x4.x : 0.0;  // misses add +0.0 like the reference
+          acc[1] += (kk & 2u) ? (double)x4.y : 0.0;
+          acc[2] += (kk & 4u) ? (double)x4.z : 0.0;
+          acc[3] += (kk & 8u) ? (double)x4.w : 0.0;
+          c4[0] += kk & 1u;
+          c4[1] += (kk >> 1) & 1u;
+          c4[2] += (kk >> 2) & 1u;
+          c4[3] += (kk >> 3) & 1u;
+        }
+        const float4 res = make_float4(mean_of(acc[0], (double)c4[0]), mean_of(acc[1], (double)c4[1]),
+                                       mean_of(acc[2], (double)c4[2]), mean_of(acc[3], (double)c4[3]));
+        st4(f.A[me] + e, res);  // my shard's aggregate; peers pull it in their D jobs
+      }
+      const bool last = chunk == cpt - 1;
+      group_sync<2, kAggThreads>();  // stage s consumed (and the tile's results stored, when last)
+      if (ta == 0) {
+        if (last) {
+          __threadfence();  // cumulative: the group's results are in my L2 before the flags
+          const int64_t t = (int64_t)f.own * ns + tl;
+          for (int q = 0; q < n; ++q) st_relaxed_sys(f.gflag[q] + t, f.epoch);
+          if (tra && ntr < f.trace_cap / 2)
+            tra[ntr++] = make_uint4((1u << 28) | (uint32_t)t, t_claim, t_ready, (uint32_t)globaltimer_ns());
+        }
+        issue_next(s);
+      }
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    const unsigned int prev = atomicAdd(f.ctr + 1, 1u);
+    if (prev == gridDim.x - 1) {
+      f.ctr[0] = 0;
+      f.ctr[1] = 0;
+      f.ctr[2] = 0;
+      __threadfence();
     }
   }
 }

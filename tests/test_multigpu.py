@@ -60,6 +60,10 @@ CASES = [
     (25_000_000, 0.01, 1, True, "f32"),
     (12_345, 0.05, 2, False, "f32"),
     (1 << 20, 0.02, 4, True, "bf16"),
+    # fused multi-GPU kernel (D = 2^23, 2^25): against the oracle / exact mean
+    (5_000_000, 0.02, 6, True, "f32"),
+    (4_200_000, 0.01, 7, True, "bf16"),
+    (25_000_000, 0.0, 2, True, "f32"),
 ]
 
 
@@ -117,7 +121,8 @@ def test_tar_rht_multi_gpu_vs_oracle():
                     out = np.load(os.path.join(d, f"c{ci}_r{rank}.npy")).astype(np.float64)
                     rec = np.load(os.path.join(d, f"c{ci}_r{rank}_rec.npy"))
                     assert rec[0] == sc[(1, rank)][0] and rec[1] == sc[(2, rank)][0]
-                    assert np.linalg.norm(out - mean) / np.linalg.norm(mean) < 0.3
+                    rel = np.linalg.norm(out - mean) / np.linalg.norm(mean)
+                    assert rel < (1e-5 if p == 0 else 0.3), (ci, rank, rel)
                 continue
             want = O.run_generation(buckets, 9, gen, ht, masks=masks, r=r)
             for rank in range(world):
@@ -186,3 +191,59 @@ def test_ddp_comm_hook_lossless_matches_mean():
                 rel = np.linalg.norm(got.astype(np.float64) - ref) / np.linalg.norm(ref)
                 assert rel < 1e-5, rel
             np.testing.assert_array_equal(ovl, ordered)  # same kernels, same order of arithmetic
+
+
+# ------------------------------------------- fused kernel vs barrier path
+def _seq_worker(rank, world, port, outdir, fused):
+    os.environ["OPTR_FUSED"] = "1" if fused else "0"
+    import torch.distributed as dist
+
+    from paper_2310_06993_b200.collectives import MaskSpec
+    from paper_2310_06993_b200.dist import TarCommunicator
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(rank)
+    dev = torch.device("cuda", rank)
+    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=dev)
+    lens = [5_000_000, 8_388_608, 3_000_000, 16_000_000, 5_000_000]
+    comm = TarCommunicator(max_len=max(lens))
+    g = torch.Generator(device=dev).manual_seed(50 + rank)
+    xs = [torch.randn(L, device=dev, generator=g) for L in lens]
+    outs = [torch.empty_like(x) for x in xs]
+    recs = [torch.zeros(2, dtype=torch.int64, device=dev) for _ in lens]
+    for rep in range(2):  # second pass: both parities reused at the next epochs
+        for b, L in enumerate(lens):
+            gen = rep * len(lens) + b
+            comm.allreduce(xs[b], outs[b], rotation=gen % world, ht=True, job_seed=4, generation=gen,
+                           masks=MaskSpec.coin(300 + gen, 0.02), received=recs[b], async_op=True)
+        comm.join()
+    torch.cuda.synchronize()
+    for b in range(len(lens)):
+        np.save(os.path.join(outdir, f"f{int(fused)}_b{b}_r{rank}.npy"), outs[b].cpu().numpy())
+        np.save(os.path.join(outdir, f"f{int(fused)}_b{b}_r{rank}_rec.npy"), recs[b].cpu().numpy())
+    comm.close()
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.multigpu
+def test_fused_kernel_matches_barrier_path_async():
+    """Async back-to-back buckets through the fused per-tile-flag kernel give
+    the barrier-separated path's results (float32 codec tolerance; the pass
+    order differs) and identical received counts."""
+    import torch.multiprocessing as mp
+
+    if not torch.cuda.is_available() or torch.cuda.device_count() < 2:
+        pytest.skip("needs >= 2 GPUs")
+    world = min(torch.cuda.device_count(), 8)
+    with tempfile.TemporaryDirectory() as d:
+        for fused in (True, False):
+            mp.spawn(_seq_worker, args=(world, _free_port(), d, fused), nprocs=world, join=True)
+        for b in range(5):
+            for r in range(world):
+                a = np.load(os.path.join(d, f"f1_b{b}_r{r}.npy")).astype(np.float64)
+                c = np.load(os.path.join(d, f"f0_b{b}_r{r}.npy")).astype(np.float64)
+                assert np.linalg.norm(a - c) / np.linalg.norm(c) < 1e-5, (b, r)
+                np.testing.assert_array_equal(np.load(os.path.join(d, f"f1_b{b}_r{r}_rec.npy")),
+                                              np.load(os.path.join(d, f"f0_b{b}_r{r}_rec.npy")))
