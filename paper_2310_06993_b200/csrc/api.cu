@@ -1593,9 +1593,15 @@ int launch_fused_t(const TmaArgs& ae, const TmaArgs& ad, const SnkBuf& se, const
   const int threads = (1 << (T - 5)) + kAggThreads;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem) != cudaSuccess || per_sm < 1)
     per_sm = 1;
+  int grid = nsm * per_sm;
+  {  // OPTR_FUSED_GRID caps the grid (several ranks sharing one GPU in tests:
+     // every rank's persistent grid must fit on the GPU at once)
+    const char* e = getenv("OPTR_FUSED_GRID");
+    if (e && atoi(e) > 0 && atoi(e) < grid) grid = atoi(e);
+  }
   KScope ks(OPTR_K_FUSED, st);
-  launch_ex(kern, dim3((unsigned)(nsm * per_sm)), dim3(threads), smem, st, ae, ad, se, sd, f);
-  return launch_check(kern, "tma_fused", T, 0, nsm * per_sm, 1, threads, smem);
+  launch_ex(kern, dim3((unsigned)grid), dim3(threads), smem, st, ae, ad, se, sd, f);
+  return launch_check(kern, "tma_fused", T, 0, grid, 1, threads, smem);
 }
 
 int launch_fused(int T, const TmaArgs& ae, const TmaArgs& ad, const SnkBuf& se, const SnkBuf& sd,

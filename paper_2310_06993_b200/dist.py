@@ -37,7 +37,7 @@ def all_gather_bytes(blob: bytes, group=None, device=None) -> list:
 
     world = dist.get_world_size(group)
     t = torch.tensor(list(blob), dtype=torch.uint8)
-    if device is not None:
+    if device is not None and dist.get_backend(group) != "gloo":
         t = t.to(device)
     parts = [torch.empty_like(t) for _ in range(world)]
     dist.all_gather(parts, t, group=group)

@@ -18,6 +18,29 @@ import oracle as O
 torch = pytest.importorskip("torch")
 
 
+def _world():
+    """Ranks for the multi-GPU tests: one per GPU (<= 8), or OPTR_TEST_WORLD
+    ranks round-robin over the GPUs (e.g. 8 ranks on 4 GPUs, with
+    OPTR_FUSED_GRID capping each persistent grid so two fit on a GPU)."""
+    env = os.environ.get("OPTR_TEST_WORLD")
+    return int(env) if env else min(torch.cuda.device_count(), 8)
+
+
+def _dev(rank):
+    return rank % torch.cuda.device_count()
+
+
+def _init(rank, world, dev):
+    """NCCL with one rank per GPU; gloo (host-side handle exchange only) when
+    ranks share GPUs, which NCCL refuses."""
+    import torch.distributed as dist
+
+    if world > torch.cuda.device_count():
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+    else:
+        dist.init_process_group("nccl", rank=rank, world_size=world, device_id=dev)
+
+
 def _free_port():
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
@@ -75,9 +98,9 @@ def _gpu_worker(rank, world, port, outdir):
 
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
-    torch.cuda.set_device(rank)
-    dev = torch.device("cuda", rank)
-    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=dev)
+    torch.cuda.set_device(_dev(rank))
+    dev = torch.device("cuda", _dev(rank))
+    _init(rank, world, dev)
     comm = TarCommunicator(max_len=max(c[0] for c in CASES))
     for ci, (L, p, gen, ht, dt) in enumerate(CASES):
         buckets = O.make_buckets(100 + ci, world, L)
@@ -102,7 +125,7 @@ def test_tar_rht_multi_gpu_vs_oracle():
 
     if not torch.cuda.is_available() or torch.cuda.device_count() < 2:
         pytest.skip("needs >= 2 GPUs")
-    world = min(torch.cuda.device_count(), 8)
+    world = _world()
     with tempfile.TemporaryDirectory() as d:
         mp.spawn(_gpu_worker, args=(world, _free_port(), d), nprocs=world, join=True)
         for ci, (L, p, gen, ht, dt) in enumerate(CASES):
@@ -144,8 +167,8 @@ def _ddp_worker(rank, world, port, outdir):
 
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
-    torch.cuda.set_device(rank)
-    dev = torch.device("cuda", rank)
+    torch.cuda.set_device(_dev(rank))
+    dev = torch.device("cuda", _dev(rank))
     dist.init_process_group("nccl", rank=rank, world_size=world, device_id=dev)
     grads = {}
     for mode in ("nccl", "overlap", "ordered"):
@@ -182,7 +205,9 @@ def test_ddp_comm_hook_lossless_matches_mean():
 
     if not torch.cuda.is_available() or torch.cuda.device_count() < 2:
         pytest.skip("needs >= 2 GPUs")
-    world = min(torch.cuda.device_count(), 8)
+    world = _world()
+    if world > torch.cuda.device_count():
+        pytest.skip("DDP over NCCL needs one rank per GPU")
     with tempfile.TemporaryDirectory() as d:
         mp.spawn(_ddp_worker, args=(world, _free_port(), d), nprocs=world, join=True)
         for r in range(world):
@@ -203,9 +228,9 @@ def _seq_worker(rank, world, port, outdir, fused):
 
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
-    torch.cuda.set_device(rank)
-    dev = torch.device("cuda", rank)
-    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=dev)
+    torch.cuda.set_device(_dev(rank))
+    dev = torch.device("cuda", _dev(rank))
+    _init(rank, world, dev)
     lens = [5_000_000, 8_388_608, 3_000_000, 16_000_000, 5_000_000]
     comm = TarCommunicator(max_len=max(lens))
     g = torch.Generator(device=dev).manual_seed(50 + rank)
@@ -236,7 +261,7 @@ def test_fused_kernel_matches_barrier_path_async():
 
     if not torch.cuda.is_available() or torch.cuda.device_count() < 2:
         pytest.skip("needs >= 2 GPUs")
-    world = min(torch.cuda.device_count(), 8)
+    world = _world()
     with tempfile.TemporaryDirectory() as d:
         for fused in (True, False):
             mp.spawn(_seq_worker, args=(world, _free_port(), d, fused), nprocs=world, join=True)
