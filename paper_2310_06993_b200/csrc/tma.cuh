@@ -777,13 +777,14 @@ namespace optr {
 //     {j*ns + k}), then all D tickets (row order)
 //     E(t)  encode tile t of my wire vector Y in place (scale 1/sqrt(dim)),
 //           then eflag[t] = epoch in my memory (peers poll it over NVLink)
-//     D(t)  once my gflag[t] == epoch: pull tile t from its owner's aggregate
+//     D(t)  once my gflag[t] counts every unit of tile t: pull it from its owner's aggregate
 //           (one TMA bulk copy over NVLink, stage-2 masks applied as it is
 //           read) and decode it into my G
-//   A group (kAggThreads threads): tiles of my shard in order; for each, wait
-//     for eflag[t] at every rank, stream the tile from every rank's Y in
-//     kAggCh-entry chunks through a ring, masked fp64 mean in ascending node
-//     order into my aggregate A; then gflag[t] = epoch at every rank.
+//   A group (kAggThreads threads): units (1/UPT tile) of my shard in order;
+//     for each, wait for eflag[t] at every rank, stream the unit from every
+//     rank's Y in kAggCh-entry chunks through a ring, masked fp64 mean in
+//     ascending node order into my aggregate A; then add 1 to gflag[t] at
+//     every rank (the consuming D job re-arms it to 0).
 // E jobs wait for nothing, A jobs only for E jobs, D jobs only for A jobs of
 // the same row, and every queue is claimed in the same order on all ranks,
 // so nothing waits on a job that cannot run.  A D job's load is deferred
@@ -826,6 +827,9 @@ __device__ __forceinline__ unsigned int ld_relaxed_sys(const unsigned int* p) {
 __device__ __forceinline__ void st_relaxed_sys(unsigned int* p, unsigned int v) {
   asm volatile("st.relaxed.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+__device__ __forceinline__ void red_add_relaxed_sys(unsigned int* p, unsigned int v) {
+  asm volatile("red.relaxed.sys.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 __device__ __forceinline__ uint64_t globaltimer_ns() {
   uint64_t t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -866,6 +870,11 @@ __global__ void __launch_bounds__((1 << (T - 5)) + kAggThreads)
   constexpr size_t SB = tma_stage_bytes<T>();
   constexpr int kAggCh = agg_chunk(NW);
   constexpr int SA = kAggBytes / (NW * kAggCh * 4) < 16 ? kAggBytes / (NW * kAggCh * 4) : 16;
+  // aggregate work unit = 1/UPT of a tile (finer units shorten the A tail);
+  // a unit must cover every ring stage queued behind a not-ready unit
+  constexpr int kCpt = (1 << T) / kAggCh;
+  constexpr int UPT = kCpt / SA >= 4 ? 4 : (kCpt / SA >= 2 ? 2 : 1);
+  constexpr int kCpu = kCpt / UPT;  // chunks per unit
   static_assert(NW >= 2 && SA >= 2, "aggregate ring needs two stages");
   extern __shared__ __align__(16) unsigned char smraw[];
   unsigned char* const base = smraw + ((1024u - (smem_u32(smraw) & 1023u)) & 1023u);
@@ -924,7 +933,7 @@ __global__ void __launch_bounds__((1 << (T - 5)) + kAggThreads)
       if (kind == FJ_E && !f.exp) {
         tile_issue_contig<T, TS_BUF>(ae, me, t, base + s * SB, &full[s]);
       } else if (kind == FJ_D) {
-        if (ld_relaxed_sys(f.gflag[me] + t) >= f.epoch) {
+        if (ld_relaxed_sys(f.gflag[me] + t) >= (unsigned)UPT) {
           fence_proxy_async_global();
           if (f.exp) mbar_arrive(&full[s]);
           else tile_issue_contig<T, TS_GATHER>(ad, me, t, base + s * SB, &full[s]);
@@ -945,7 +954,7 @@ __global__ void __launch_bounds__((1 << (T - 5)) + kAggThreads)
       if (tid == 0 && (deferred >> s & 1u)) {
         release_e();  // never wait while holding an unreleased encode
         const int64_t t = slot_tile[s];
-        spin_ge_sys(f.gflag[me] + t, f.epoch);
+        spin_ge_sys(f.gflag[me] + t, (unsigned)UPT);
         fence_proxy_async_global();
         if (f.exp) mbar_arrive(&full[s]);
         else tile_issue_contig<T, TS_GATHER>(ad, me, t, sb, &full[s]);
@@ -959,6 +968,10 @@ __global__ void __launch_bounds__((1 << (T - 5)) + kAggThreads)
         break;
       }
       if (tid == 0 && kind != FJ_E) release_e();
+      // a D tile's data has landed: re-arm its counter for the next call on
+      // this parity (the owner adds to it again only after seeing my next
+      // encode flag, which is released after this store)
+      if (tid == 0 && kind == FJ_D) st_relaxed_sys(f.gflag[me] + t, 0u);
       const uint32_t trd = tr && tid == 0 ? (uint32_t)globaltimer_ns() : 0u;
       if (f.exp && kind != FJ_NOP) {
         group_sync<1, NED>();
@@ -992,22 +1005,22 @@ __global__ void __launch_bounds__((1 << (T - 5)) + kAggThreads)
     // ------------------------------------------------ A warp group
     // TAR stage 1 + stage-2 push (collectives.py:113-137) of my shard's tiles
     const int ta = tid - NED;
-    constexpr int cpt = (1 << T) / kAggCh;  // chunks per tile
+    const int64_t nunits = ns * UPT;
     const int64_t soff = (int64_t)f.own * f.shard_len;
-    // producer state (ta == 0).  A new tile whose encodes are not all in is
+    // producer state (ta == 0).  A new unit whose encodes are not all in is
     // not waited for here: its stages are queued (pend_*) and the wait
     // happens when the consumer reaches its first chunk, i.e. after the
-    // previous tile's gflag is published (peers' E jobs may be queued
-    // behind D jobs that wait for exactly that flag).
-    int64_t cur = -1;  // current tile (index inside my shard)
-    int nxt = cpt;     // next chunk of it to issue
+    // previous unit is published (peers' E jobs may be queued behind D jobs
+    // that wait for exactly that unit).
+    int64_t cur = -1;  // current unit (tile-in-shard * UPT + part)
+    int nxt = kCpu;    // next chunk of it to issue
     bool aend = false;
     int pend_first = -1, pend_count = 0;
     uint4* const tra = f.trace ? f.trace + (size_t)blockIdx.x * f.trace_cap + f.trace_cap / 2 : nullptr;
     int ntr = 0;
     uint32_t t_claim = 0, t_ready = 0;
-    auto tile_ready = [&](int64_t k) {
-      const int64_t t = (int64_t)f.own * ns + k;
+    auto tile_ready = [&](int64_t u) {
+      const int64_t t = (int64_t)f.own * ns + u / UPT;
       unsigned int v[NW];
 #pragma unroll
       for (int q = 0; q < n; ++q) v[q] = ld_relaxed_sys(f.eflag[q] + t);  // n loads in flight
@@ -1019,20 +1032,20 @@ __global__ void __launch_bounds__((1 << (T - 5)) + kAggThreads)
     auto issue_chunk = [&](int s) {
       aslot[s] = (int)((cur << 8) | nxt);
       const uint32_t bytes = kAggCh * sizeof(float);
-      const int64_t e = (cur << T) + (int64_t)nxt * kAggCh;  // entry inside my shard
+      const int64_t e = ((cur / UPT) << T) + ((int64_t)(cur % UPT) * kCpu + nxt) * kAggCh;  // inside my shard
       mbar_expect_tx(&abar[s], bytes * n);
       for (int i = 0; i < n; ++i)
         bulk_load(abuf + ((size_t)s * n + i) * kAggCh, f.Y[i] + soff + e, bytes, &abar[s]);
       ++nxt;
     };
     auto issue_next = [&](int s) {
-      if (pend_first >= 0) {  // the queued tile takes this stage too (SA <= cpt)
+      if (pend_first >= 0) {  // the queued unit takes this stage too (SA <= kCpu)
         ++pend_count;
         return;
       }
-      if (!aend && nxt == cpt) {
+      if (!aend && nxt == kCpu) {
         const int64_t k = atomicAdd(f.ctr + 2, 1u);
-        if (k >= ns) {
+        if (k >= nunits) {
           aend = true;
         } else {
           cur = k;
@@ -1056,12 +1069,12 @@ __global__ void __launch_bounds__((1 << (T - 5)) + kAggThreads)
     };
     if (ta == 0)
       for (int s = 0; s < SA; ++s) issue_next(s);
-    static_assert(SA <= (1 << T) / kAggCh, "a queued tile covers every queued stage");
+    static_assert(SA <= kCpu, "a queued unit covers every queued stage");
     static_assert(kAggCh % (4 * kAggThreads) == 0, "whole float4 groups per thread");
     for (int k = 0;; ++k) {
       const int s = k % SA;
       if (ta == 0 && s == pend_first) {
-        const int64_t t = (int64_t)f.own * ns + cur;
+        const int64_t t = (int64_t)f.own * ns + cur / UPT;
         for (int q = 0; q < n; ++q) spin_ge_sys(f.eflag[q] + t, f.epoch);
         if (tra) t_ready = (uint32_t)globaltimer_ns();
         fence_proxy_async_global();
@@ -1073,12 +1086,12 @@ __global__ void __launch_bounds__((1 << (T - 5)) + kAggThreads)
       mbar_wait(&abar[s], (uint32_t)((k / SA) & 1));
       const int code = aslot[s];
       if (code < 0) break;
-      const int64_t tl = code >> 8;
-      const int chunk = code & 255;
+      const int64_t un = code >> 8;  // unit
+      const int chunk = code & 255;  // chunk inside the unit
 #pragma unroll
       for (int v = 0; v < kAggCh / (4 * kAggThreads); ++v) {
         const int off = 4 * (ta + v * kAggThreads);
-        const int64_t e = (tl << T) + (int64_t)chunk * kAggCh + off;
+        const int64_t e = ((un / UPT) << T) + ((int64_t)(un % UPT) * kCpu + chunk) * kAggCh + off;
         const float* src = abuf + (size_t)s * n * kAggCh + off;
         double acc[4] = {0.0, 0.0, 0.0, 0.0};
         uint32_t c4[4] = {0u, 0u, 0u, 0u};
@@ -1099,13 +1112,13 @@ __global__ void __launch_bounds__((1 << (T - 5)) + kAggThreads)
                                        mean_of(acc[2], (double)c4[2]), mean_of(acc[3], (double)c4[3]));
         st4(f.A[me] + e, res);  // my shard's aggregate; peers pull it in their D jobs
       }
-      const bool last = chunk == cpt - 1;
-      group_sync<2, kAggThreads>();  // stage s consumed (and the tile's results stored, when last)
+      const bool last = chunk == kCpu - 1;
+      group_sync<2, kAggThreads>();  // stage s consumed (and the unit's results stored, when last)
       if (ta == 0) {
         if (last) {
-          __threadfence();  // cumulative: the group's results are in my L2 before the flags
-          const int64_t t = (int64_t)f.own * ns + tl;
-          for (int q = 0; q < n; ++q) st_relaxed_sys(f.gflag[q] + t, f.epoch);
+          __threadfence();  // cumulative: the group's results are in my L2 before the counts
+          const int64_t t = (int64_t)f.own * ns + un / UPT;
+          for (int q = 0; q < n; ++q) red_add_relaxed_sys(f.gflag[q] + t, 1u);
           if (tra && ntr < f.trace_cap / 2)
             tra[ntr++] = make_uint4((1u << 28) | (uint32_t)t, t_claim, t_ready, (uint32_t)globaltimer_ns());
         }

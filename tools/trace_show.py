@@ -4,7 +4,7 @@ import sys
 import numpy as np
 
 tag = sys.argv[1]
-for r in (0, 1):
+for r in range(8):
     try:
         a = np.load(f"gpurun_out/{tag}/trace_r{r}.npy").astype(np.int64)
     except FileNotFoundError:
