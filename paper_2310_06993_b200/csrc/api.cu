@@ -948,10 +948,25 @@ int optr_rht_encode(const void* x, int dtype_in, int64_t L, float* y, int64_t di
   cudaStream_t st = (cudaStream_t)stream;
   uint32_t* signs = nullptr;
   size_t sbytes = (size_t)((dim + 31) / 32) * 4;
-  CK(cudaMallocAsync((void**)&signs, sbytes, st));
+  // OPTR_ENC_ORDER=strided: the fused multi-GPU path's order (strided pass
+  // first, transposed sign bytes) on one GPU, for profiling that pass alone
+  static int strided_first = -1;
+  if (strided_first < 0) {
+    const char* e = getenv("OPTR_ENC_ORDER");
+    strided_first = (e && e[0] == 's') ? 1 : 0;
+  }
+  PassGeom ps[3];
+  const int np = plan_passes(log2_exact(dim > 0 ? dim : 1), ps, true);
+  const bool sf = strided_first && np == 2 && ps[1].cb == 3;
+  CK(cudaMallocAsync((void**)&signs, sbytes * (sf ? 2 : 1) + 16, st));
   PrepArgs a;
   memset(&a, 0, sizeof(a));
   fill_sign_args(a, signs, dim, seed);
+  if (sf) {
+    a.signs_t = (uint8_t*)signs + sbytes;
+    a.t_lo = ps[1].lo;
+    a.t_ks = ps[1].ks;
+  }
   int rc = launch_prep(a, st);
   if (!rc) {
     SrcEncode src;
@@ -960,6 +975,7 @@ int optr_rht_encode(const void* x, int dtype_in, int64_t L, float* y, int64_t di
     src.dtype = dtype_in;
     src.L = L;
     src.signs = signs;
+    src.signs_t = a.signs_t;
     SrcBuf buf;
     memset(&buf, 0, sizeof(buf));
     buf.y[0] = y;
@@ -967,7 +983,15 @@ int optr_rht_encode(const void* x, int dtype_in, int64_t L, float* y, int64_t di
     memset(&snk, 0, sizeof(snk));
     snk.y[0] = y;
     snk.scale = (float)(1.0 / sqrt((double)dim));
-    rc = run_transform(log2_exact(dim), true, 0, 1, src, buf, snk, st, OPTR_K_ENC_FIRST);
+    if (sf) {
+      SnkBuf mid = snk;
+      mid.scale = 1.f;
+      const int nlog = log2_exact(dim);
+      rc = launch_pass(OPTR_K_ENC_FIRST, ps[1], nlog, 0, 1, src, mid, st);
+      if (!rc) rc = launch_pass(OPTR_K_ENC_LAST, ps[0], nlog, 0, 1, buf, snk, st);
+    } else {
+      rc = run_transform(log2_exact(dim), true, 0, 1, src, buf, snk, st, OPTR_K_ENC_FIRST);
+    }
   }
   cudaFreeAsync(signs, st);
   return rc;
@@ -1369,6 +1393,8 @@ struct optr_comm_s {
   unsigned int fepoch[2];      // fused-kernel tile-flag epochs of each parity
   cudaEvent_t fused_done[2];   // fused kernels of consecutive calls never overlap
   bool fused_recorded[2];
+  cudaEvent_t enc_done[2];     // fused path: the next call's prep starts after this strided encode
+  bool enc_recorded[2];
   unsigned long long epoch[3];
   cudaStream_t ws[2];       // per-parity work streams
   cudaEvent_t fork[2];
@@ -1437,13 +1463,18 @@ int optr_comm_create(optr_comm* out, int device, int rank, int n, int64_t max_le
   CK(cudaMemset(c->sym, 0, c->sym_bytes));
   CK(cudaMemset(c->local, 0, 2 * c->local_bytes));
   for (int p = 0; p < 2; ++p) c->chain_ctr[p] = (unsigned int*)(c->local + p * c->local_bytes + c->off_chain);
-  CK(cudaStreamCreateWithFlags(&c->pstream, cudaStreamNonBlocking));
+  // prep (ALU-heavy, off the critical path) at the lowest priority, the call
+  // streams at the highest: the block scheduler gives prep leftover SMs
+  int prio_lo = 0, prio_hi = 0;
+  CK(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+  CK(cudaStreamCreateWithPriority(&c->pstream, cudaStreamNonBlocking, prio_lo));
   for (int p = 0; p < 2; ++p) {
     CK(cudaEventCreateWithFlags(&c->prep_ready[p], cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&c->done[p], cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&c->fork[p], cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&c->fused_done[p], cudaEventDisableTiming));
-    CK(cudaStreamCreateWithFlags(&c->ws[p], cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&c->enc_done[p], cudaEventDisableTiming));
+    CK(cudaStreamCreateWithPriority(&c->ws[p], cudaStreamNonBlocking, prio_hi));
   }
   CK(cudaDeviceSynchronize());
   c->peer[rank] = c->sym;
@@ -1489,6 +1520,7 @@ int optr_comm_destroy(optr_comm c) {
     cudaEventDestroy(c->done[p]);
     cudaEventDestroy(c->fork[p]);
     cudaEventDestroy(c->fused_done[p]);
+    cudaEventDestroy(c->enc_done[p]);
     cudaStreamDestroy(c->ws[p]);
   }
   free(c);
@@ -1675,6 +1707,7 @@ static int tar_enqueue(optr_comm c, const void* x, void* out, int64_t L, int dty
   // per rank on their own, e.g. for unaligned x / out)
   const cudaStream_t ps = c->pstream;
   if (c->done_recorded[par]) CK(cudaStreamWaitEvent(ps, c->done[par], 0));
+
   CK(cudaMemsetAsync(counts, 0, (size_t)2 * n * 8, ps));
   PrepArgs pa;
   memset(&pa, 0, sizeof(pa));
@@ -1708,6 +1741,8 @@ static int tar_enqueue(optr_comm c, const void* x, void* out, int64_t L, int dty
       snk.y[me] = Yp[me];
       snk.scale = 1.f;
       if ((rc = launch_pass(OPTR_K_ENC_FIRST, fps[1], nlog, me, 1, src, snk, st))) return rc;
+      CK(cudaEventRecord(c->enc_done[par], st));
+      c->enc_recorded[par] = true;
     }
     TmaArgs ae, ad;
     memset(&ae, 0, sizeof(ae));

@@ -361,3 +361,32 @@ def test_chain_vs_oracle_d23(dev):
     for node in range(n):
         assert rel_err(outs[node], want[node]) < REL, node
         np.testing.assert_array_equal(got[node].astype(bool), tar[node][1])
+
+
+@pytest.mark.parametrize("logd,L,dtype", [(23, 5_000_001, "f32"), (25, 25_000_000, "bf16"), (24, 16_000_000, "f32")])
+def test_strided_first_encode_matches(dev, logd, L, dtype, tmp_path):
+    """The fused multi-GPU path's encode order (strided pass first, transposed
+    sign bytes, x read by TMA boxes) equals the default encode within the
+    float32 codec tolerance (subprocess: OPTR_ENC_ORDER is read once)."""
+    import os
+    import subprocess
+    import sys
+
+    code = (
+        "import sys, numpy as np, torch; sys.path.insert(0, %r);"
+        "import paper_2310_06993_b200 as P;"
+        "g = torch.Generator(device='cuda').manual_seed(5);"
+        "x = torch.randn(%d, device='cuda', generator=g).to(%s);"
+        "ctx = P.RhtContext.for_length(%d, 777);"
+        "np.save(%r, P.rht_encode(x, ctx).cpu().numpy())"
+    )
+    here = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    dt = "torch.float32" if dtype == "f32" else "torch.bfloat16"
+    outs = {}
+    for order in ("contig", "strided"):
+        path = str(tmp_path / f"{order}.npy")
+        env = dict(os.environ, OPTR_ENC_ORDER=order)
+        subprocess.run([sys.executable, "-c", code % (here, L, dt, L, path)], check=True, env=env, timeout=300)
+        outs[order] = np.load(path)
+    assert outs["contig"].shape == (1 << logd,)
+    assert rel_err(outs["strided"], outs["contig"]) < REL
