@@ -25,6 +25,7 @@ import argparse
 import json
 import math
 import os
+import re
 import statistics
 import subprocess
 import sys
@@ -168,13 +169,13 @@ def step_alg_bytes(buckets, n_workers, s_in, s_out, ht):
 
 # kernel classes -> kernel names in the one-GPU ncu capture (decode order there:
 # strided gather first, contiguous last)
-NCU_NAMES = {
-    "enc_first": "tma_pass_kernel<13, 2, 0, 1,",
-    "enc_last": "tma_pass_kernel<13, 2, 1, 0,",
-    "dec_first": "tma_pass_kernel<13, 2, 1, 2,",
-    "dec_last": "tma_pass_kernel<13, 2, 0, 0,",
-    "aggregate": "tma_agg_kernel",
-    "prep": "prep_kernel",
+NCU_NAMES = {  # regexes (stage count free: it depends on the tile shape)
+    "enc_first": r"tma_pass_kernel<\d+, \d, 0, 1,",
+    "enc_last": r"tma_pass_kernel<\d+, \d, 1, 0, SnkBuf",
+    "dec_first": r"tma_pass_kernel<\d+, \d, 1, 2,",
+    "dec_last": r"tma_pass_kernel<\d+, \d, 0, 0, SnkDecode",
+    "aggregate": r"tma_agg_kernel",
+    "prep": r"prep_kernel",
 }
 
 
@@ -191,7 +192,7 @@ def ncu_traffic(cls: str, multi: bool):
         with open(files[-1]) as fh:
             entries = json.load(fh)
         for e in entries:
-            if NCU_NAMES[cls] in e["kernel"]:
+            if re.search(NCU_NAMES[cls], e["kernel"]):
                 rd, wr = float(e["dram__bytes_read.sum"]), float(e["dram__bytes_write.sum"])
                 scale = 1e6 if rd + wr < 1e5 else 1.0  # the raw page reports MB
                 return {"bytes": int((rd + wr) * scale), "source": os.path.basename(files[-1]),

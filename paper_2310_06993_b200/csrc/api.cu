@@ -307,9 +307,10 @@ int launch_tma_pass_s(int cls, const TmaMaps& maps, const TmaMaps& dmaps, const 
                       1 << (T - 5), smem);
 }
 
-// ring depth of the TMA pass kernels: 2, strided T = 14 tiles 3 (D = 2^25:
+// ring depth of the TMA pass kernels: 2, strided T >= 13 tiles 3 (D = 2^25:
 // the strided pass waits on its 32-byte-row TMA boxes with one CTA per SM;
-// a third stage takes it from 90 to 60 us; contiguous is flat from 2 up).
+// a third stage takes it from 90 to 60 us; at D = 2^23 with the workers
+// batched, 2 CTAs x 3 stages beat 3 x 2 by ~2%; contiguous is flat from 2 up).
 // OPTR_TMA_STAGES (1..3) overrides both, OPTR_TMA_STAGES_C / _S one kind.
 int tma_stages(bool strided) {
   static int s[2] = {0, 0};
@@ -326,7 +327,7 @@ template <int T, bool STRIDED, int SK, class Snk, int CBW = 3>
 int launch_tma_pass(int cls, const TmaMaps& maps, const TmaMaps& dmaps, const TmaArgs& a, const Snk& snk,
                     int worker, int nworkers, cudaStream_t st) {
   int S = tma_stages(STRIDED);
-  if (S < 0) S = (STRIDED && T >= 14) ? 3 : 2;  // T = 13 strided keeps three CTAs per SM
+  if (S < 0) S = (STRIDED && T >= 13) ? 3 : 2;
   switch (S) {
     case 1: return launch_tma_pass_s<T, 1, STRIDED, SK, Snk, CBW>(cls, maps, dmaps, a, snk, worker, nworkers, st);
     case 3: return launch_tma_pass_s<T, 3, STRIDED, SK, Snk, CBW>(cls, maps, dmaps, a, snk, worker, nworkers, st);
