@@ -114,6 +114,15 @@ bool wide_rows() {
   return v == 1;
 }
 
+bool wide3_rows() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("OPTR_WIDE3");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
 int plan_passes(int n, PassGeom* out, bool encode_order) {
   // A contiguous pass on 2^c-entry tiles plus strided passes of <= 11 row
   // bits on 2^ks x 8 tiles (T = ks + 3 <= 14: one CTA's registers).  Encode
@@ -135,11 +144,16 @@ int plan_passes(int n, PassGeom* out, bool encode_order) {
     p[np++] = PassGeom{0, kContigBits + 1, 0, 0};
     p[np++] = PassGeom{kContigBits + 1, n - kContigBits - 1, kColBits, 0};
   } else {
+    // three passes (D >= 2^26): the strided passes take 32 columns (128-byte
+    // rows, full L2 lines) while T = ks + 5 <= 14; with 8 columns their tiles
+    // were 2^9..2^10 entries of 32-byte rows at multi-MB strides (~1.2-1.5
+    // TB/s).  OPTR_WIDE3=0 keeps 8 columns.
     int rest = n - kContigBits;
     int k1 = rest / 2;
+    const int cb = (wide3_rows() && rest - k1 + 5 <= 14) ? 5 : kColBits;
     p[np++] = PassGeom{0, kContigBits, 0, 0};
-    p[np++] = PassGeom{kContigBits, k1, kColBits, 0};
-    p[np++] = PassGeom{kContigBits + k1, rest - k1, kColBits, 0};
+    p[np++] = PassGeom{kContigBits, k1, cb, 0};
+    p[np++] = PassGeom{kContigBits + k1, rest - k1, cb, 0};
   }
   for (int i = 0; i < np; ++i) p[i].ntiles = (1LL << n) >> (p[i].cb + p[i].ks);
   for (int i = 0; i < np; ++i) out[i] = encode_order ? p[i] : p[np - 1 - i];
@@ -392,7 +406,7 @@ int try_tma(int cls, const PassGeom& pg, int nlog, int worker, int nworkers, con
         if (T == 13) return launch_tma_pass<13, true, SK>(cls, maps, dmaps, a, snk, worker, nworkers, st);
         return launch_tma_pass<14, true, SK>(cls, maps, dmaps, a, snk, worker, nworkers, st);
       } else {
-        if (T < 9 || T > 14 || (pg.cb == 5 && T != 14)) return -1;
+        if (T < 9 || T > 14 || (pg.cb == 5 && T < 11)) return -1;
         const uint32_t bw = 1u << pg.cb;
         const uint64_t d0 = 1ULL << pg.lo, d1 = 1ULL << pg.ks, d2 = 1ULL << (nlog - pg.lo - pg.ks);
         int box = (int)(d1 < 256 ? d1 : 256);
@@ -423,7 +437,18 @@ int try_tma(int cls, const PassGeom& pg, int nlog, int worker, int nworkers, con
           if (pg.cb == 3) a.signs_t = snk.signs_t;
         }
         a.box_rows = box;
-        if (pg.cb == 5) return launch_tma_pass<14, true, SK, Snk, 5>(cls, maps, dmaps, a, snk, worker, nworkers, st);
+        if (pg.cb == 5) {
+          if constexpr (kSnkBuf) {  // three-pass plans (32-column tiles)
+            switch (T) {
+              case 11: return launch_tma_pass<11, true, SK, Snk, 5>(cls, maps, dmaps, a, snk, worker, nworkers, st);
+              case 12: return launch_tma_pass<12, true, SK, Snk, 5>(cls, maps, dmaps, a, snk, worker, nworkers, st);
+              case 13: return launch_tma_pass<13, true, SK, Snk, 5>(cls, maps, dmaps, a, snk, worker, nworkers, st);
+              default: break;
+            }
+          }
+          if (T != 14) return -1;
+          return launch_tma_pass<14, true, SK, Snk, 5>(cls, maps, dmaps, a, snk, worker, nworkers, st);
+        }
         if constexpr (kSnkBuf) {  // small strided tiles (3-pass plans of D >= 2^26)
           switch (T) {
             case 9: return launch_tma_pass<9, true, SK>(cls, maps, dmaps, a, snk, worker, nworkers, st);

@@ -390,3 +390,33 @@ def test_strided_first_encode_matches(dev, logd, L, dtype, tmp_path):
         outs[order] = np.load(path)
     assert outs["contig"].shape == (1 << logd,)
     assert rel_err(outs["strided"], outs["contig"]) < REL
+
+
+def test_three_pass_wide_rows_match(dev, tmp_path):
+    """D = 2^26 (three-pass plan): 32-column strided tiles (default) against
+    the 8-column plan (OPTR_WIDE3=0), same masks: counts / received flags
+    bit-exact, results within the float32 codec tolerance; and the lossless
+    result is the exact mean."""
+    import os
+    import subprocess
+    import sys
+
+    here = os.path.dirname(os.path.abspath(__file__))
+    z = {}
+    for wide in ("1", "0"):
+        path = str(tmp_path / f"w{wide}.npz")
+        env = dict(os.environ, OPTR_WIDE3=wide)
+        env["PYTHONPATH"] = os.pathsep.join([os.path.dirname(here), here, env.get("PYTHONPATH", "")])
+        subprocess.run([sys.executable, os.path.join(here, "chain_case.py"), "2", "40000000", "f32", "2", path],
+                       check=True, env=env, timeout=600)
+        z[wide] = np.load(path)
+    np.testing.assert_array_equal(z["1"]["counts"], z["0"]["counts"])
+    np.testing.assert_array_equal(z["1"]["got"], z["0"]["got"])
+    assert rel_err(z["1"]["res"], z["0"]["res"]) < REL
+    n, L = 2, 40_000_000
+    g = torch.Generator(device=dev).manual_seed(3)
+    xs = [torch.randn(L, device=dev, generator=g) for _ in range(n)]
+    mean = (xs[0].double() + xs[1].double()) / 2
+    outs, _, _ = tar_allreduce_local(xs, rotation=0, ht=True, job_seed=1, generation=0, masks=MaskSpec.none())
+    for o in outs:
+        assert ((o.double() - mean).norm() / mean.norm()).item() < REL
