@@ -786,6 +786,18 @@ bool stage2_push() {
   return v == 1;
 }
 
+// One GPU: contiguous-first when the plan allows transposed decode signs and
+// the TMA decode epilogue (two passes, 8-column strided tiles of T >= 12),
+// else strided-first.
+bool decode_contig_first_local(bool two_pass) {
+  static int v = -2;
+  if (v == -2) {
+    const char* e = getenv("OPTR_DEC_ORDER");
+    v = !e ? -1 : (e[0] == 's' ? 0 : 1);
+  }
+  return v < 0 ? two_pass : v == 1;
+}
+
 bool decode_contig_first(bool multi_gpu) {
   static int v = -2;
   if (v == -2) {
@@ -1197,7 +1209,7 @@ extern "C" {
 
 // -------------------------------------------------- TAR, n workers, one GPU
 struct LocalLayout {
-  size_t y, a, signs, bitmap, counts, total;
+  size_t y, a, signs, signs_t, bitmap, counts, total;
   int64_t dim, smax, astride, pw;
 };
 
@@ -1215,6 +1227,8 @@ static LocalLayout local_layout(int n, int64_t L, int ht, int epp) {
   off = align_up(off + (size_t)n * (l.astride > 0 ? l.astride : 1) * 4, 256);
   l.signs = off;
   off = align_up(off + (size_t)((l.dim + 31) / 32 + 2) * 4, 256);
+  l.signs_t = off;  // transposed sign bytes for the strided decode pass
+  off = align_up(off + (size_t)(ht ? l.dim / 8 + 16 : 16), 256);
   l.bitmap = off;
   off = align_up(off + (size_t)2 * n * n * l.pw * 4, 256);
   l.counts = off;
@@ -1294,6 +1308,18 @@ int tar_local_impl(const void* const* x, void* const* out, int n, int64_t L, int
   PrepArgs pa;
   memset(&pa, 0, sizeof(pa));
   if (ht) fill_sign_args(pa, signs, dim, derive_seed(job_seed, bucket_id, generation));
+  // two-pass plans decode contiguous-first (the stage-2 gather on whole
+  // packets) and finish with the strided pass, whose signs come from the
+  // transposed sign bytes (coalesced, one bulk copy per tile)
+  PassGeom dps[3];
+  const int dnp = ht ? plan_passes(log2_exact(dim), dps, true) : 0;
+  const bool dec_cf = decode_contig_first_local(dnp == 2 && dps[1].cb == 3 && dps[1].ks + 3 >= 12);
+  uint8_t* const signs_t = (ht && dec_cf && dnp == 2 && dps[1].cb == 3) ? (uint8_t*)(ws + lay.signs_t) : nullptr;
+  if (signs_t) {
+    pa.signs_t = signs_t;
+    pa.t_lo = dps[1].lo;
+    pa.t_ks = dps[1].ks;
+  }
   const uint32_t* cbits = nullptr;
   if ((rc = setup_masks(pa, masks, dim, n, r, epp, bitmap, counts, 0, n, &cbits))) return rc;
   if ((rc = launch_prep(pa, st))) return rc;
@@ -1379,11 +1405,11 @@ int tar_local_impl(const void* const* x, void* const* out, int n, int64_t L, int
     snk.count_extra = counts + n;  // stage-2 row
     snk.count_stride = 1;
     snk.dim = (double)dim;
+    snk.signs_t = signs_t;
     rc = try_chain(OPTR_K_DEC_CHAIN, log2_exact(dim), 0, n, ga, buf, snk, chain_counters(set, st), st);
     if (rc < 0)
       rc = for_workers(dim, n, st, set, [&](int w0, int nw, cudaStream_t s2) {
-        return run_transform(log2_exact(dim), decode_contig_first(false), w0, nw, ga, buf, snk, s2,
-                             OPTR_K_DEC_FIRST);
+        return run_transform(log2_exact(dim), dec_cf, w0, nw, ga, buf, snk, s2, OPTR_K_DEC_FIRST);
       });
     if (rc) return rc;
   } else {
