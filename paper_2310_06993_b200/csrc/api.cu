@@ -1781,7 +1781,13 @@ static int tar_enqueue(optr_comm c, const void* x, void* out, int64_t L, int dty
   MaskView mv{cbits, pa.pw, n, epp, make_divider((uint32_t)epp)};
 
   if (fused) {
-    // fused kernels of consecutive calls never overlap (each spins on peers)
+    // Fused kernels of consecutive calls never overlap.  Letting the next one
+    // fill the previous one's tail deadlocked (watchdog, 2 GPUs): a rank's
+    // next fused kernel spins on SMs while a peer's next call still needs SM
+    // space for its prep / strided encode, held by that peer's previous
+    // fused kernel waiting on this rank -- a resource cycle outside the
+    // ticket order.  Serialised, every rank's fused(c) finishes before its
+    // fused(c+1) holds an SM.
     if (c->fused_recorded[par ^ 1]) CK(cudaStreamWaitEvent(st, c->fused_done[par ^ 1], 0));
     {  // strided encode pass: x -> Y (signs, pad, upcast fused)
       SrcEncode src;
