@@ -842,12 +842,20 @@ void fill_sign_args(PrepArgs& a, uint32_t* signs, int64_t dim, uint64_t seed) {
   a.sign_threads = (dim + kSignsPerThread - 1) / kSignsPerThread;
 }
 
-int launch_prep(const PrepArgs& a, cudaStream_t st) {
+// cap_per_sm > 0: at most that many CTAs per SM (grid-stride), for a prep
+// that runs in the background beside another call's kernels.
+int launch_prep(const PrepArgs& a, cudaStream_t st, int cap_per_sm = 0) {
   int64_t total = a.sign_threads + a.mask_threads;
   if (total == 0) return OPTR_OK;
   int rc = ensure_device_init();
   if (rc) return rc;
   int64_t blocks = (total + 255) / 256;
+  if (cap_per_sm > 0) {
+    int dev = 0, nsm = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    if (blocks > (int64_t)nsm * cap_per_sm) blocks = (int64_t)nsm * cap_per_sm;
+  }
   KScope ks(OPTR_K_PREP, st);
   prep_kernel<<<(unsigned)blocks, 256, 0, st>>>(a);
   CK(cudaGetLastError());
@@ -1490,8 +1498,8 @@ int optr_comm_create(optr_comm* out, int device, int rank, int n, int64_t max_le
     off = align_up(off + (size_t)smax * 4, 1024);
     c->off_g[p] = off;  // stage-2 receive vector, written by every owner's push
     off = align_up(off + (size_t)c->max_dim * 4, 1024);
-    c->off_ef[p] = off;  // fused kernel: per-tile encode / receive flags
-    off = align_up(off + (size_t)(c->max_dim >> 13 > 0 ? c->max_dim >> 13 : 1) * 4, 256);
+    c->off_ef[p] = off;  // fused kernel: per-tile encode flags [n][tiles], receive counts [tiles]
+    off = align_up(off + (size_t)n * (c->max_dim >> 13 > 0 ? c->max_dim >> 13 : 1) * 4, 256);
     c->off_gf[p] = off;
     off = align_up(off + (size_t)(c->max_dim >> 13 > 0 ? c->max_dim >> 13 : 1) * 4, 1024);
   }
@@ -1775,7 +1783,9 @@ static int tar_enqueue(optr_comm c, const void* x, void* out, int64_t L, int dty
   }
   const uint32_t* cbits = nullptr;
   if ((rc = setup_masks(pa, masks, dim, n, r, epp, bitmap, counts, me, me + 1, &cbits))) return rc;
-  if ((rc = launch_prep(pa, ps))) return rc;
+  // background prep: two CTAs per SM leave room for the previous call's
+  // strided passes (whose 512-thread CTAs waited behind a full-width prep)
+  if ((rc = launch_prep(pa, ps, 2))) return rc;
   CK(cudaEventRecord(c->prep_ready[par], ps));
   CK(cudaStreamWaitEvent(st, c->prep_ready[par], 0));
   MaskView mv{cbits, pa.pw, n, epp, make_divider((uint32_t)epp)};
@@ -1829,9 +1839,11 @@ static int tar_enqueue(optr_comm c, const void* x, void* out, int64_t L, int dty
     for (int i = 0; i < n; ++i) {
       f.Y[i] = Yp[i];
       f.A[i] = Ap[i];
-      f.eflag[i] = (unsigned int*)(c->peer[i] + c->off_ef[par]);
+      f.eflag_out[i] = (unsigned int*)(c->peer[i] + c->off_ef[par]) + (size_t)me * (c->max_dim >> 13);
       f.gflag[i] = (unsigned int*)(c->peer[i] + c->off_gf[par]);
     }
+    f.eflag_in = (const unsigned int*)(c->peer[me] + c->off_ef[par]);
+    f.estride = c->max_dim >> 13;
     f.ctr = c->chain_ctr[par];
     f.epoch = ++c->fepoch[par];
     f.n = n;

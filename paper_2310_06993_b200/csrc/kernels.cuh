@@ -211,8 +211,17 @@ __device__ __forceinline__ uint64_t coin_base(const PrepArgs& a, int stage, int 
   return base;
 }
 
+__device__ __forceinline__ void prep_item(const PrepArgs& a, int64_t t);
+
+// One work item per thread; a capped grid strides over the items (the
+// multi-GPU path runs prep as a thin background kernel on a side stream).
 __global__ void __launch_bounds__(256) prep_kernel(const __grid_constant__ PrepArgs a) {
-  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t total = a.sign_threads + a.mask_threads;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x)
+    prep_item(a, t);
+}
+
+__device__ __forceinline__ void prep_item(const PrepArgs& a, int64_t t) {
   if (t < a.sign_threads) {
     // signs 128c .. 128c+127 = outputs 64c .. 64c+63; Lemire bit of u32 halves.
     // Natural layout: chunk c = t.  With the transposed layout too, a warp

@@ -776,7 +776,7 @@ namespace optr {
 //   E/D group (2^(T-5) threads): all E tickets (row order, row k = tiles
 //     {j*ns + k}), then all D tickets (row order)
 //     E(t)  encode tile t of my wire vector Y in place (scale 1/sqrt(dim)),
-//           then eflag[t] = epoch in my memory (peers poll it over NVLink)
+//           then eflag[me][t] = epoch in every rank's memory
 //     D(t)  once my gflag[t] counts every unit of tile t: pull it from its owner's aggregate
 //           (one TMA bulk copy over NVLink, stage-2 masks applied as it is
 //           read) and decode it into my G
@@ -792,7 +792,12 @@ namespace optr {
 struct FusedArgs {
   const float* Y[kMaxW];       // every rank's wire vector (peer-mapped)
   float* A[kMaxW];             // every rank's owner-shard aggregate (peer-mapped)
-  unsigned int* eflag[kMaxW];  // every rank's encode-tile flags
+  // encode-tile flags: rank q keeps [n][tiles] in its own memory; my E job
+  // writes row `me` of every rank's copy (eflag_out[q]), my aggregate group
+  // polls its local copy (eflag_in + q*estride) -- no polling over NVLink
+  unsigned int* eflag_out[kMaxW];
+  const unsigned int* eflag_in;
+  int64_t estride;
   unsigned int* gflag[kMaxW];  // every rank's receive-tile flags
   unsigned int* ctr;           // local [0] E/D ticket, [1] CTAs done, [2] A ticket (reset by the last CTA)
   unsigned int epoch;
@@ -910,7 +915,7 @@ __global__ void __launch_bounds__((1 << (T - 5)) + kAggThreads)
     auto release_e = [&]() {
       if (pend_e >= 0) {
         __threadfence();  // cumulative over the group (its stores came before a group barrier)
-        st_relaxed_sys(f.eflag[me] + pend_e, f.epoch);
+        for (int q = 0; q < f.n; ++q) st_relaxed_sys(f.eflag_out[q] + pend_e, f.epoch);
         pend_e = -1;
       }
     };
@@ -976,7 +981,8 @@ __global__ void __launch_bounds__((1 << (T - 5)) + kAggThreads)
       if (f.exp && kind != FJ_NOP) {
         group_sync<1, NED>();
         if (tid == 0) {
-          if (kind == FJ_E) st_relaxed_sys(f.eflag[me] + t, f.epoch);
+          if (kind == FJ_E)
+            for (int q = 0; q < n; ++q) st_relaxed_sys(f.eflag_out[q] + t, f.epoch);
           claim_issue(s);
         }
       } else if (kind == FJ_E) {
@@ -1023,7 +1029,7 @@ __global__ void __launch_bounds__((1 << (T - 5)) + kAggThreads)
       const int64_t t = (int64_t)f.own * ns + u / UPT;
       unsigned int v[NW];
 #pragma unroll
-      for (int q = 0; q < n; ++q) v[q] = ld_relaxed_sys(f.eflag[q] + t);  // n loads in flight
+      for (int q = 0; q < n; ++q) v[q] = ld_relaxed_sys(f.eflag_in + q * f.estride + t);  // local, n in flight
       bool ok = true;
 #pragma unroll
       for (int q = 0; q < n; ++q) ok = ok && v[q] >= f.epoch;
@@ -1075,7 +1081,7 @@ __global__ void __launch_bounds__((1 << (T - 5)) + kAggThreads)
       const int s = k % SA;
       if (ta == 0 && s == pend_first) {
         const int64_t t = (int64_t)f.own * ns + cur / UPT;
-        for (int q = 0; q < n; ++q) spin_ge_sys(f.eflag[q] + t, f.epoch);
+        for (int q = 0; q < n; ++q) spin_ge_sys(f.eflag_in + q * f.estride + t, f.epoch);
         if (tra) t_ready = (uint32_t)globaltimer_ns();
         fence_proxy_async_global();
         const int first = pend_first, cnt = pend_count;
