@@ -1669,6 +1669,15 @@ bool fused_enabled() {
   return v == 1;
 }
 
+bool prep_after_enc() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("OPTR_PREP_AFTER_ENC");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
 template <int T, int NW>
 int launch_fused_t(const TmaArgs& ae, const TmaArgs& ad, const SnkBuf& se, const SnkBuf& sd, const FusedArgs& f,
                    cudaStream_t st) {
@@ -1770,6 +1779,10 @@ static int tar_enqueue(optr_comm c, const void* x, void* out, int64_t L, int dty
   // per rank on their own, e.g. for unaligned x / out)
   const cudaStream_t ps = c->pstream;
   if (c->done_recorded[par]) CK(cudaStreamWaitEvent(ps, c->done[par], 0));
+  // the host runs ahead: without this, this call's prep (ALU-heavy) would run
+  // beside the previous call's HBM-bound strided encode instead of beside its
+  // NVLink-bound fused kernel (OPTR_PREP_AFTER_ENC=0 disables)
+  if (fused && prep_after_enc() && c->enc_recorded[par ^ 1]) CK(cudaStreamWaitEvent(ps, c->enc_done[par ^ 1], 0));
 
   CK(cudaMemsetAsync(counts, 0, (size_t)2 * n * 8, ps));
   PrepArgs pa;

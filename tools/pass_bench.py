@@ -15,11 +15,13 @@ from paper_2310_06993_b200 import _lib
 ap = argparse.ArgumentParser()
 ap.add_argument("--logd", type=int, default=25)
 ap.add_argument("--iters", type=int, default=20)
+ap.add_argument("--L", type=int, default=0, help="bucket entries (default 2^logd)")
 args = ap.parse_args()
 dev = torch.device("cuda", 0)
 d = 1 << args.logd
-x = torch.randn(d, device=dev)
-ctx = P.RhtContext.for_length(d, 12345)
+L = args.L or d
+x = torch.randn(L, device=dev)
+ctx = P.RhtContext.for_length(L, 12345)
 y = P.rht_encode(x, ctx)
 for _ in range(3):
     P.rht_encode(x, ctx)
@@ -34,7 +36,7 @@ e1.record()
 torch.cuda.synchronize()
 t = _lib.timing_collect()
 ms = e0.elapsed_time(e1) / args.iters
-out = {"logd": args.logd, "encode_ms": round(ms, 4)}
+out = {"logd": args.logd, "L": L, "encode_ms": round(ms, 4)}
 for k, (tms, n, u) in t.items():
     if n:
         out[k] = {"us_per_launch": round(tms / n * 1e3, 2), "gbs": round(8 * d / (tms / n * 1e-3) / 1e9, 1)}
