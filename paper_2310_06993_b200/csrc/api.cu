@@ -1871,8 +1871,17 @@ static int tar_enqueue(optr_comm c, const void* x, void* out, int64_t L, int dty
     f.trace = (uint4*)g_fused_trace;
     f.trace_cap = g_fused_trace_cap;
     {
-      const char* e = getenv("OPTR_FUSED_EXP");
-      f.exp = (e && e[0] == '1') ? 1 : 0;
+      static const int exp = [] {
+        const char* e = getenv("OPTR_FUSED_EXP");
+        return (e && e[0] == '1') ? 1 : 0;
+      }();
+      static const uint64_t wd = [] {
+        const char* w = getenv("OPTR_WATCHDOG_S");
+        const double sec = (w && atof(w) > 0) ? atof(w) : 1800.0;
+        return (uint64_t)(sec * 1e9);
+      }();
+      f.exp = exp;
+      f.watchdog_ns = wd;
     }
     if ((rc = launch_fused(Tc, ae, ad, se, sd, f, st))) return rc < 0 ? OPTR_ECUDA : rc;
     CK(cudaEventRecord(c->fused_done[par], st));

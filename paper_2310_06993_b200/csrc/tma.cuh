@@ -808,6 +808,7 @@ struct FusedArgs {
   uint4* trace;   // debug (optr_debug_trace): per CTA [cap/2 E/D jobs | cap/2 A tiles]
   int trace_cap;
   int exp;        // experiment (OPTR_FUSED_EXP=1): E / D keep their flags and waits, skip the tiles
+  uint64_t watchdog_ns;
 };
 
 __device__ __forceinline__ unsigned int ld_acquire_sys(const unsigned int* p) {
@@ -840,14 +841,16 @@ __device__ __forceinline__ uint64_t globaltimer_ns() {
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
   return t;
 }
-// Spin until *p >= v (acquire, system scope).  A peer that never arrives is
-// a protocol bug: trap after 10 s instead of hanging the GPU.
-__device__ __noinline__ void spin_ge_sys(const unsigned int* p, unsigned int v) {
+// Spin until *p >= v.  A peer may legitimately be late (a straggler rank in
+// DDP); one that never arrives is a protocol bug or a dead rank: trap after
+// `limit_ns` (OPTR_WATCHDOG_S, default 1800 s like NCCL's default timeout)
+// instead of hanging the GPU.
+__device__ __noinline__ void spin_ge_sys(const unsigned int* p, unsigned int v, uint64_t limit_ns) {
   if (ld_relaxed_sys(p) >= v) return;
   const uint64_t t0 = globaltimer_ns();
   while (ld_relaxed_sys(p) < v) {
     __nanosleep(64);
-    if (globaltimer_ns() - t0 > 10000000000ull) {
+    if (globaltimer_ns() - t0 > limit_ns) {
       printf("optr: fused kernel wait timed out (flag %p, have %u, want %u)\n", p, ld_relaxed_sys(p), v);
       __trap();
     }
@@ -959,7 +962,7 @@ __global__ void __launch_bounds__((1 << (T - 5)) + kAggThreads)
       if (tid == 0 && (deferred >> s & 1u)) {
         release_e();  // never wait while holding an unreleased encode
         const int64_t t = slot_tile[s];
-        spin_ge_sys(f.gflag[me] + t, (unsigned)UPT);
+        spin_ge_sys(f.gflag[me] + t, (unsigned)UPT, f.watchdog_ns);
         fence_proxy_async_global();
         if (f.exp) mbar_arrive(&full[s]);
         else tile_issue_contig<T, TS_GATHER>(ad, me, t, sb, &full[s]);
@@ -1081,7 +1084,7 @@ __global__ void __launch_bounds__((1 << (T - 5)) + kAggThreads)
       const int s = k % SA;
       if (ta == 0 && s == pend_first) {
         const int64_t t = (int64_t)f.own * ns + cur / UPT;
-        for (int q = 0; q < n; ++q) spin_ge_sys(f.eflag_in + q * f.estride + t, f.epoch);
+        for (int q = 0; q < n; ++q) spin_ge_sys(f.eflag_in + q * f.estride + t, f.epoch, f.watchdog_ns);
         if (tra) t_ready = (uint32_t)globaltimer_ns();
         fence_proxy_async_global();
         const int first = pend_first, cnt = pend_count;

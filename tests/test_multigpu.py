@@ -32,9 +32,11 @@ def _dev(rank):
 
 def _init(rank, world, dev):
     """NCCL with one rank per GPU; gloo (host-side handle exchange only) when
-    ranks share GPUs, which NCCL refuses."""
+    ranks share GPUs, which NCCL refuses.  A protocol deadlock in the fused
+    kernel should fail the test in seconds, not hang it (watchdog)."""
     import torch.distributed as dist
 
+    os.environ.setdefault("OPTR_WATCHDOG_S", "30")
     if world > torch.cuda.device_count():
         dist.init_process_group("gloo", rank=rank, world_size=world)
     else:
