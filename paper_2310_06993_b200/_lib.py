@@ -11,7 +11,7 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "liboptr.so")
+LIB_PATH = os.environ.get("OPTR_LIB") or os.path.join(_HERE, "liboptr.so")
 
 OPTR_OK = 0
 OPTR_EINVAL = 1
