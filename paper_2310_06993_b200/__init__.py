@@ -13,6 +13,7 @@ from .collectives import (  # noqa: F401
     shard_lengths,
     shard_offsets,
     shard_owner,
+    tar_allreduce,
     tar_allreduce_local,
 )
 from .hadamard import (  # noqa: F401

@@ -280,6 +280,19 @@ def tar_allreduce_local(buckets: list, *, rotation: int = 0, ht: bool = False, j
     return out, counts, (got.bool() if got is not None else None)
 
 
+def tar_allreduce(entries: list, *, r: int = 0, masks: MaskSpec | None = None) -> list:
+    """The reference's ``tar_allreduce`` (collectives.py:97-150) for all n
+    nodes at once, on their already-encoded vectors (RHT is the runner's job,
+    runner.py:219-258): stage-1 masked fp64 mean at each shard owner, stage-2
+    assembly.  ``entries``: n equal-length CUDA float32 tensors.  Returns one
+    ``AllReduceResult(entries, received)`` per node, like the generator's
+    return value; the generator's channel protocol itself (SendShard /
+    OpenStage / AwaitStage) has no device counterpart -- ``masks`` replaces
+    the channel.  Bit-exact with the reference."""
+    outs, _counts, got = tar_allreduce_local(entries, rotation=r, ht=False, masks=masks, want_received=True)
+    return [AllReduceResult(entries=o, received=g) for o, g in zip(outs, got)]
+
+
 def expected_counts(dim: int, n: int, r: int) -> np.ndarray:
     """[2, n] expected entries per (stage, dst) (simdriver.py:245-248)."""
     lens = shard_lengths(dim, n)

@@ -420,3 +420,16 @@ def test_three_pass_wide_rows_match(dev, tmp_path):
     outs, _, _ = tar_allreduce_local(xs, rotation=0, ht=True, job_seed=1, generation=0, masks=MaskSpec.none())
     for o in outs:
         assert ((o.double() - mean).norm() / mean.norm()).item() < REL
+
+
+def test_tar_allreduce_reference_signature(dev):
+    """collectives.tar_allreduce (the reference's name and result type) is
+    bit-exact with the reference's masked TAR on encoded vectors."""
+    n, L, r = 5, 12_345, 3
+    bufs = O.make_buckets(4, n, L)
+    masks = O.datagram_masks(8, L, n, r, 0.05)
+    want = O.tar_masked(bufs, r, masks, 350)
+    res = P.collectives.tar_allreduce([cu(b, dev) for b in bufs], r=r, masks=MaskSpec.coin(8, 0.05))
+    for node in range(n):
+        np.testing.assert_array_equal(res[node].entries.cpu().numpy(), want[node][0])
+        np.testing.assert_array_equal(res[node].received.cpu().numpy(), want[node][1])
