@@ -173,11 +173,16 @@ def _ddp_worker(rank, world, port, outdir):
     dev = torch.device("cuda", _dev(rank))
     dist.init_process_group("nccl", rank=rank, world_size=world, device_id=dev)
     grads = {}
+    big = os.environ.get("OPTR_TEST_DDP_BIG") == "1"
     for mode in ("nccl", "overlap", "ordered"):
         torch.manual_seed(0)
-        model = nn.Sequential(nn.Linear(512, 1024), nn.ReLU(), nn.Linear(1024, 700), nn.ReLU(),
-                              nn.Linear(700, 10)).to(dev)
-        ddp = DDP(model, device_ids=[rank], bucket_cap_mb=1)
+        if big:  # one 6.55M-entry bucket (D = 2^23): the fused multi-GPU kernel
+            model = nn.Sequential(nn.Linear(512, 2560, bias=False), nn.ReLU(), nn.Linear(2560, 2560),
+                                  nn.ReLU(), nn.Linear(2560, 10)).to(dev)
+        else:
+            model = nn.Sequential(nn.Linear(512, 1024), nn.ReLU(), nn.Linear(1024, 700), nn.ReLU(),
+                                  nn.Linear(700, 10)).to(dev)
+        ddp = DDP(model, device_ids=[rank], bucket_cap_mb=25 if big else 1)
         if mode != "nccl":
             state = OptiReduceState(max_bucket_len=max_bucket_len_for(model, 1), ht=True, seed=3,
                                     overlap=(mode == "overlap"))
@@ -200,10 +205,14 @@ def _ddp_worker(rank, world, port, outdir):
 
 @pytest.mark.gpu
 @pytest.mark.multigpu
-def test_ddp_comm_hook_lossless_matches_mean():
+@pytest.mark.parametrize("big", [False, True])
+def test_ddp_comm_hook_lossless_matches_mean(big, monkeypatch):
     """Lossless TAR+RHT through the DDP hook == DDP's own mean all-reduce
-    within the float32 codec error."""
+    within the float32 codec error (small buckets: the barrier path; one
+    25 MB-class bucket: the fused kernel)."""
     import torch.multiprocessing as mp
+
+    monkeypatch.setenv("OPTR_TEST_DDP_BIG", "1" if big else "0")
 
     if not torch.cuda.is_available() or torch.cuda.device_count() < 2:
         pytest.skip("needs >= 2 GPUs")
