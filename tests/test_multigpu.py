@@ -116,6 +116,12 @@ def _gpu_worker(rank, world, port, outdir):
         torch.cuda.synchronize()
         np.save(os.path.join(outdir, f"c{ci}_r{rank}.npy"), out.cpu().numpy())
         np.save(os.path.join(outdir, f"c{ci}_r{rank}_rec.npy"), rec.cpu().numpy())
+        if dt == "bf16":  # bf16 out as well (DDP's bf16 buckets): the decode's bf16 TMA store
+            out16 = torch.empty(L, dtype=torch.bfloat16, device=dev)
+            comm.allreduce(x, out16, rotation=gen % world, ht=ht, job_seed=9, generation=gen,
+                           masks=MaskSpec.coin(700 + ci, p))
+            torch.cuda.synchronize()
+            np.save(os.path.join(outdir, f"c{ci}_r{rank}_bf16.npy"), out16.float().cpu().numpy())
     comm.close()
     dist.destroy_process_group()
 
@@ -151,6 +157,9 @@ def test_tar_rht_multi_gpu_vs_oracle():
                 continue
             want = O.run_generation(buckets, 9, gen, ht, masks=masks, r=r)
             for rank in range(world):
+                if dt == "bf16":
+                    o16 = np.load(os.path.join(d, f"c{ci}_r{rank}_bf16.npy")).astype(np.float64)
+                    assert np.linalg.norm(o16 - want[rank]) / np.linalg.norm(want[rank]) < 1e-2, (ci, rank)
                 out = np.load(os.path.join(d, f"c{ci}_r{rank}.npy"))
                 if ht:
                     rel = np.linalg.norm(out.astype(np.float64) - want[rank]) / np.linalg.norm(want[rank])
