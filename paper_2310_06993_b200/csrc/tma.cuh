@@ -1,21 +1,29 @@
-// TMA-pipelined FWHT passes (sm_100a).
+// TMA-pipelined FWHT passes and the persistent kernels built on them (sm_100a).
 //
 // A pass transforms index bits [lo, lo+ks) of a vector in tiles of 2^T
-// entries (see kernels.cuh PassGeom).  Tiles stream through a 3-stage
+// entries (see kernels.cuh PassGeom).  Tiles stream through a 2- or 3-stage
 // shared-memory ring per CTA, filled by one elected thread with TMA:
 //
 //   contiguous pass (lo = 0): one 1D bulk copy (cp.async.bulk) per tile;
-//   strided pass (cb = 3): 8 x box_rows tensor boxes (cp.async.bulk.tensor),
-//     because through the LSU each warp load of 32-byte row segments touches
-//     16 cache lines and the pass is L1-bound even on L2-resident data.
+//   strided pass (8 or 32 columns): box_rows-row tensor boxes
+//     (cp.async.bulk.tensor), because through the LSU each warp load of
+//     32-byte row segments touches 16 cache lines and the pass is L1-bound
+//     even on L2-resident data; sign bits for a strided tile come as one
+//     bulk copy of its column of transposed sign bytes (PrepArgs.signs_t).
 //
-// Each tile is transformed in place in its stage buffer: round A reads the
-// dense tile (float4), rounds B and C go through an XOR-swizzled copy of the
-// same buffer (conflict-free for every layout here), and the result leaves
-// either through vector STG (contiguous pass: each warp stores 512 bytes)
-// or through TMA tensor stores from the dense buffer (strided pass).  The
-// fused source transforms (encode pad/signs/bf16 upcast, TAR stage-2 gather
-// with masks) are applied when round A reads the tile.
+// Each tile is transformed in place in its stage buffer (tma_tile): round A
+// reads the dense tile (float4), rounds B and C go through a padded copy of
+// the same buffer (conflict-free for every layout here), and the result
+// leaves either through vector STG or through TMA tensor stores.  The fused
+// source transforms (encode pad/signs/bf16 upcast, TAR stage-2 gather with
+// masks) are applied when round A reads the tile, the decode epilogue
+// (count scale, signs, truncate, cast) when the last round writes it.
+//
+// Kernels: tma_pass_kernel (one pass, grid.y = worker), tma_chain_kernel
+// (opt-in: both passes of several workers, ticket queue), tma_agg_kernel
+// (TAR stage-1 mean, optional stage-2 push), tma_fused_kernel (multi-GPU:
+// contiguous encode + stage 1 + stage 2 + contiguous decode, per-tile flags
+// over NVLink).
 #pragma once
 #include <cuda.h>
 
