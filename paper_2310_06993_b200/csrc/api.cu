@@ -1680,11 +1680,11 @@ bool prep_after_enc() {
   return v == 1;
 }
 
-template <int T, int NW, int S>
+template <int T, int NW, int S, int NG>
 int launch_fused_t(const TmaArgs& ae, const TmaArgs& ad, const SnkBuf& se, const SnkBuf& sd, const FusedArgs& f,
                    cudaStream_t st) {
-  const size_t smem = tma_fused_smem_bytes<T, S>();
-  auto kern = tma_fused_kernel<T, S, NW>;
+  const size_t smem = tma_fused_smem_bytes<T, S, NG>();
+  auto kern = tma_fused_kernel<T, S, NW, NG>;
   int rc = set_smem_attr(kern, smem);
   if (rc) return rc;
   static int nsm = 0;
@@ -1695,7 +1695,7 @@ int launch_fused_t(const TmaArgs& ae, const TmaArgs& ad, const SnkBuf& se, const
     if (nsm <= 0) nsm = 148;
   }
   int per_sm = 0;
-  const int threads = (1 << (T - 5)) + kAggThreads;
+  const int threads = NG * (1 << (T - 5)) + kAggThreads;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem) != cudaSuccess || per_sm < 1)
     per_sm = 1;
   int grid = nsm * per_sm;
@@ -1712,13 +1712,16 @@ int launch_fused_t(const TmaArgs& ae, const TmaArgs& ad, const SnkBuf& se, const
 int launch_fused(int T, const TmaArgs& ae, const TmaArgs& ad, const SnkBuf& se, const SnkBuf& sd,
                  const FusedArgs& f, cudaStream_t st) {
   // (a 3-stage E/D ring for T = 13 measured slower: 0.504 vs 0.490 ms/step)
+  // (two E/D warp groups per CTA for T = 13 made the kernel 2% faster but the
+  // step slower, 0.507 vs 0.494 ms: the larger CTA crowds out the neighbour
+  // buckets' strided passes; the kernel keeps the NG parameter)
   switch (T * 100 + f.n) {
-    case 1302: return launch_fused_t<13, 2, 2>(ae, ad, se, sd, f, st);
-    case 1304: return launch_fused_t<13, 4, 2>(ae, ad, se, sd, f, st);
-    case 1308: return launch_fused_t<13, 8, 2>(ae, ad, se, sd, f, st);
-    case 1402: return launch_fused_t<14, 2, 2>(ae, ad, se, sd, f, st);
-    case 1404: return launch_fused_t<14, 4, 2>(ae, ad, se, sd, f, st);
-    case 1408: return launch_fused_t<14, 8, 2>(ae, ad, se, sd, f, st);
+    case 1302: return launch_fused_t<13, 2, 2, 1>(ae, ad, se, sd, f, st);
+    case 1304: return launch_fused_t<13, 4, 2, 1>(ae, ad, se, sd, f, st);
+    case 1308: return launch_fused_t<13, 8, 2, 1>(ae, ad, se, sd, f, st);
+    case 1402: return launch_fused_t<14, 2, 2, 1>(ae, ad, se, sd, f, st);
+    case 1404: return launch_fused_t<14, 4, 2, 1>(ae, ad, se, sd, f, st);
+    case 1408: return launch_fused_t<14, 8, 2, 1>(ae, ad, se, sd, f, st);
     default: return -1;
   }
 }

@@ -235,7 +235,7 @@ __device__ __forceinline__ void group_sync() {
 // the next load: for a contiguous tile right after the tile has been read
 // (the results then leave by STG), for a strided tile after its TMA store
 // group is committed (the refill policy decides which stage to wait for).
-template <int T, bool STRIDED, int SK, class Snk, int CBW, int BAR = 0, class Refill>
+template <int T, bool STRIDED, int SK, class Snk, int CBW, int BAR = 0, int TID_OFF = 0, class Refill>
 __device__ __forceinline__ void tma_tile(const TmaMaps* maps, const CUtensorMap* dst, const TmaArgs& a,
                                          const typename Snk::B& d, int worker, uint8_t* gotw, int64_t t,
                                          unsigned char* sb, Refill&& refill) {
@@ -248,7 +248,7 @@ __device__ __forceinline__ void tma_tile(const TmaMaps* maps, const CUtensorMap*
   static_assert(!STRIDED || !std::is_same<Snk, SnkDecode>::value || (P.pos[LR][0] == 0 && P.pos[LR][1] == 1),
                 "decode epilogue stores float4 groups");
   static_assert(sizeof(float) * pad(1 << T) <= tma_stage_bytes<T>(), "padded tile fits the stage");
-  const int tid = threadIdx.x;
+  const int tid = (int)threadIdx.x - TID_OFF;  // thread index inside its warp group
   const int b0 = thread_base<T>(P, 0, tid);
   const int b1 = thread_base<T>(P, 1, tid);
   const int b2 = thread_base<T>(P, LR, tid);  // last-round base
@@ -870,15 +870,15 @@ constexpr int kAggThreads = 256;
 __host__ __device__ constexpr int agg_chunk(int n) { return 4096 / n > 1024 ? 4096 / n : 1024; }
 constexpr int kAggBytes = 64 * 1024;  // A-group ring
 
-template <int T, int S>
+template <int T, int S, int NG>
 __host__ __device__ constexpr size_t tma_fused_smem_bytes() {
-  return S * tma_stage_bytes<T>() + kAggBytes + 256 + 1024;
+  return (size_t)NG * S * tma_stage_bytes<T>() + kAggBytes + 512 + 1024;
 }
 
 enum FusedJob { FJ_END = -1, FJ_E = 0, FJ_D = 2, FJ_NOP = 3 };
 
-template <int T, int kStages, int NW>
-__global__ void __launch_bounds__((1 << (T - 5)) + kAggThreads)
+template <int T, int kStages, int NW, int NG>
+__global__ void __launch_bounds__(NG * (1 << (T - 5)) + kAggThreads)
     tma_fused_kernel(const __grid_constant__ TmaArgs ae, const __grid_constant__ TmaArgs ad,
                      const __grid_constant__ SnkBuf se, const __grid_constant__ SnkBuf sd,
                      const __grid_constant__ FusedArgs f) {
@@ -894,19 +894,19 @@ __global__ void __launch_bounds__((1 << (T - 5)) + kAggThreads)
   static_assert(NW >= 2 && SA >= 2, "aggregate ring needs two stages");
   extern __shared__ __align__(16) unsigned char smraw[];
   unsigned char* const base = smraw + ((1024u - (smem_u32(smraw) & 1023u)) & 1023u);
-  float* const abuf = reinterpret_cast<float*>(base + kStages * SB);
-  uint64_t* const full = reinterpret_cast<uint64_t*>(base + kStages * SB + kAggBytes);
-  uint64_t* const abar = full + kStages;
-  int* const slot_kind = reinterpret_cast<int*>(abar + SA);
-  int64_t* const slot_tile = reinterpret_cast<int64_t*>(slot_kind + 4);
-  int* const aslot = reinterpret_cast<int*>(slot_tile + 4);  // A ring: (tile << 8 | chunk), -1 end
+  float* const abuf = reinterpret_cast<float*>(base + (size_t)NG * kStages * SB);
+  uint64_t* const full = reinterpret_cast<uint64_t*>(base + (size_t)NG * kStages * SB + kAggBytes);
+  uint64_t* const abar = full + NG * kStages;
+  int* const slot_kind = reinterpret_cast<int*>(abar + SA);                // [NG][4]
+  int64_t* const slot_tile = reinterpret_cast<int64_t*>(slot_kind + NG * 4);  // [NG][4]
+  int* const aslot = reinterpret_cast<int*>(slot_tile + NG * 4);  // A ring: (unit << 8 | chunk), -1 end
   const int tid = threadIdx.x;
   constexpr int n = NW;
   const int me = f.me;
   const int64_t ns = f.ns;
 
   if (tid == 0) {
-    for (int s = 0; s < kStages; ++s) mbar_init(&full[s], 1);
+    for (int s = 0; s < NG * kStages; ++s) mbar_init(&full[s], 1);
     for (int s = 0; s < SA; ++s) mbar_init(&abar[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -914,7 +914,16 @@ __global__ void __launch_bounds__((1 << (T - 5)) + kAggThreads)
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   asm volatile("griddepcontrol.wait;" ::: "memory");
 
-  if (tid < NED) {
+  // E/D warp group G (NG groups per CTA, independent rings / barriers / ticket
+  // order positions; all claim from the same counter)
+  auto ed_loop = [&](auto gc) {
+    constexpr int G = decltype(gc)::value;
+    constexpr int BARID = 1 + 2 * G;
+    const int ltid = tid - G * NED;
+    unsigned char* const gbase = base + (size_t)G * kStages * SB;
+    uint64_t* const gfull = full + G * kStages;
+    int* const gkind = slot_kind + G * 4;
+    int64_t* const gtile = slot_tile + G * 4;
     // ------------------------------------------------ E/D warp group
     // tickets [0, n*ns): E in row order; [n*ns, 2*n*ns): D in row order (E
     // never queues behind a D; the D rows drain as the owners publish)
@@ -944,84 +953,90 @@ __global__ void __launch_bounds__((1 << (T - 5)) + kAggThreads)
           t = (int64_t)u * ns + row;
         }
       }
-      slot_kind[s] = kind;
-      slot_tile[s] = t;
+      gkind[s] = kind;
+      gtile[s] = t;
       if (kind == FJ_E && !f.exp) {
-        tile_issue_contig<T, TS_BUF>(ae, me, t, base + s * SB, &full[s]);
+        tile_issue_contig<T, TS_BUF>(ae, me, t, gbase + s * SB, &gfull[s]);
       } else if (kind == FJ_D) {
         if (ld_relaxed_sys(f.gflag[me] + t) >= (unsigned)UPT) {
           fence_proxy_async_global();
-          if (f.exp) mbar_arrive(&full[s]);
-          else tile_issue_contig<T, TS_GATHER>(ad, me, t, base + s * SB, &full[s]);
+          if (f.exp) mbar_arrive(&gfull[s]);
+          else tile_issue_contig<T, TS_GATHER>(ad, me, t, gbase + s * SB, &gfull[s]);
         } else {
           deferred |= 1u << s;
         }
       } else {
-        mbar_arrive(&full[s]);  // no-op / end: nothing through the ring
+        mbar_arrive(&gfull[s]);  // no-op / end: nothing through the ring
       }
     };
-    if (tid == 0)
+    if (ltid == 0)
       for (int s = 0; s < kStages; ++s) claim_issue(s);
-    uint4* const tr = f.trace ? f.trace + (size_t)blockIdx.x * f.trace_cap : nullptr;
+    uint4* const tr = (f.trace && G == 0) ? f.trace + (size_t)blockIdx.x * f.trace_cap : nullptr;
     for (int k = 0;; ++k) {
       const int s = k % kStages;
-      unsigned char* const sb = base + s * SB;
-      const uint32_t tb = tr && tid == 0 ? (uint32_t)globaltimer_ns() : 0u;
-      if (tid == 0 && (deferred >> s & 1u)) {
+      unsigned char* const sb = gbase + s * SB;
+      const uint32_t tb = tr && ltid == 0 ? (uint32_t)globaltimer_ns() : 0u;
+      if (ltid == 0 && (deferred >> s & 1u)) {
         release_e();  // never wait while holding an unreleased encode
-        const int64_t t = slot_tile[s];
+        const int64_t t = gtile[s];
         spin_ge_sys(f.gflag[me] + t, (unsigned)UPT, f.watchdog_ns);
         fence_proxy_async_global();
-        if (f.exp) mbar_arrive(&full[s]);
-        else tile_issue_contig<T, TS_GATHER>(ad, me, t, sb, &full[s]);
+        if (f.exp) mbar_arrive(&gfull[s]);
+        else tile_issue_contig<T, TS_GATHER>(ad, me, t, sb, &gfull[s]);
         deferred &= ~(1u << s);
       }
-      mbar_wait(&full[s], (uint32_t)((k / kStages) & 1));
-      const int kind = slot_kind[s];
-      const int64_t t = slot_tile[s];
+      mbar_wait(&gfull[s], (uint32_t)((k / kStages) & 1));
+      const int kind = gkind[s];
+      const int64_t t = gtile[s];
       if (kind == FJ_END) {
-        if (tid == 0) release_e();
+        if (ltid == 0) release_e();
         break;
       }
-      if (tid == 0 && kind != FJ_E) release_e();
+      if (ltid == 0 && kind != FJ_E) release_e();
       // a D tile's data has landed: re-arm its counter for the next call on
       // this parity (the owner adds to it again only after seeing my next
       // encode flag, which is released after this store)
-      if (tid == 0 && kind == FJ_D) st_relaxed_sys(f.gflag[me] + t, 0u);
-      const uint32_t trd = tr && tid == 0 ? (uint32_t)globaltimer_ns() : 0u;
+      if (ltid == 0 && kind == FJ_D) st_relaxed_sys(f.gflag[me] + t, 0u);
+      const uint32_t trd = tr && ltid == 0 ? (uint32_t)globaltimer_ns() : 0u;
       if (f.exp && kind != FJ_NOP) {
-        group_sync<1, NED>();
-        if (tid == 0) {
+        group_sync<BARID, NED>();
+        if (ltid == 0) {
           if (kind == FJ_E)
             for (int q = 0; q < n; ++q) st_relaxed_sys(f.eflag_out[q] + t, f.epoch);
           claim_issue(s);
         }
       } else if (kind == FJ_E) {
-        tma_tile<T, false, TS_BUF, SnkBuf, 3, 1>(nullptr, nullptr, ae, se.bind(me), me, nullptr, t, sb,
+        tma_tile<T, false, TS_BUF, SnkBuf, 3, BARID, G * NED>(nullptr, nullptr, ae, se.bind(me), me, nullptr, t, sb,
                                                  [&]() { claim_issue(s); });
         // released after the group's next job (or before any wait / exit), so
         // the fence finds the tile's stores drained instead of stalling on them
-        group_sync<1, NED>();
-        if (tid == 0) {
+        group_sync<BARID, NED>();
+        if (ltid == 0) {
           release_e();
           pend_e = t;
         }
       } else if (kind == FJ_D) {
-        tma_tile<T, false, TS_GATHER, SnkBuf, 3, 1>(nullptr, nullptr, ad, sd.bind(me), me, nullptr, t, sb,
+        tma_tile<T, false, TS_GATHER, SnkBuf, 3, BARID, G * NED>(nullptr, nullptr, ad, sd.bind(me), me, nullptr, t, sb,
                                                     [&]() { claim_issue(s); });
       } else {
         // no-op ticket: every thread has read the slot (it is only rewritten
         // after this barrier)
-        group_sync<1, NED>();
-        if (tid == 0) claim_issue(s);
+        group_sync<BARID, NED>();
+        if (ltid == 0) claim_issue(s);
       }
-      if (tr && tid == 0 && k < f.trace_cap / 2)
+      if (tr && ltid == 0 && k < f.trace_cap / 2)
         tr[k] = make_uint4(((uint32_t)kind << 28) | (uint32_t)t, tb, trd, (uint32_t)globaltimer_ns());
     }
+  };
+
+  if (tid < NED) {
+    ed_loop(std::integral_constant<int, 0>{});
+  } else if (NG > 1 && tid < NG * NED) {
+    ed_loop(std::integral_constant<int, (NG > 1 ? 1 : 0)>{});
   } else {
     // ------------------------------------------------ A warp group
     // TAR stage 1 + stage-2 push (collectives.py:113-137) of my shard's tiles
-    const int ta = tid - NED;
+    const int ta = tid - NG * NED;
     const int64_t nunits = ns * UPT;
     const int64_t soff = (int64_t)f.own * f.shard_len;
     // producer state (ta == 0).  A new unit whose encodes are not all in is

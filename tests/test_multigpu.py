@@ -44,11 +44,21 @@ def _init(rank, world, dev):
 
 
 def _free_port():
-    s = socket.socket()
-    s.bind(("127.0.0.1", 0))
-    p = s.getsockname()[1]
-    s.close()
-    return p
+    """A bindable port outside the ephemeral range (bind-to-0 ports can be
+    taken again by the previous spawn's lingering NCCL / gloo sockets)."""
+    import random
+
+    for _ in range(200):
+        p = random.randint(20000, 29999)
+        s = socket.socket()
+        try:
+            s.bind(("127.0.0.1", p))
+            return p
+        except OSError:
+            continue
+        finally:
+            s.close()
+    raise RuntimeError("no free port")
 
 
 # ------------------------------------------------------------ CPU / gloo
