@@ -1,5 +1,5 @@
 """Summaries of a profile_round.sh capture for profiles/:
-  python tools/ncu_summary.py gpurun_out/<tag> profiles/<name>.json
+  python tools/ncu_summary.py gpurun_out/<tag> profiles/<name>.json [report.ncu-rep]
 writes the json (per captured kernel: duration, DRAM bytes and
 %, L2 %, active vs elapsed cycles, instructions, issue %, warps active,
 registers, grid, top stalls) and prints the launch-list share table of
@@ -19,8 +19,10 @@ KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "smsp__inst_executed.sum", "smsp__issue_active.avg.pct_of_peak_sustained_active",
         "sm__warps_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread", "launch__grid_size",
         "launch__block_size"]
-raw = subprocess.run(["ncu", "-i", f"{tag}/prof.ncu-rep", "--page", "raw", "--csv"], capture_output=True,
-                     text=True).stdout
+import os
+
+rep = sys.argv[3] if len(sys.argv) > 3 else f"{tag}/prof.ncu-rep"
+raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(raw)))
 h = rows[0]
 out = []
@@ -43,6 +45,8 @@ json.dump(out, open(prefix, "w"), indent=1)
 print(f"wrote {prefix} ({len(out)} kernels)")
 
 # launch-list shares
+if not os.path.exists(f"{tag}/launches.csv"):
+    sys.exit(0)
 tot = defaultdict(lambda: [0, 0.0, 0.0, 0.0])
 with open(f"{tag}/launches.csv") as fh:
     lines = [l for l in fh if l.startswith('"')]
