@@ -661,11 +661,21 @@ int launch_tma_aggregate(const AggArgs& ag, int nowners, int64_t smax, cudaStrea
   a.r = ag.r;
   a.owner_base = ag.owner_base;
   a.m = ag.m;
-  const size_t smem = tma_agg_smem_bytes<kAggChunk>(ag.n);
-  auto kern = ag.n == 2 ? tma_agg_kernel<kAggChunk, 2>
-            : ag.n == 4 ? tma_agg_kernel<kAggChunk, 4>
-            : ag.n == 8 ? tma_agg_kernel<kAggChunk, 8>
-                        : tma_agg_kernel<kAggChunk, 0>;
+  // chunk ring depth: OPTR_AGG_STAGES=4 (default 2; 4 measured slower on one
+  // GPU, 1.013 vs 0.988 ms/step: more CTAs per SM beat a deeper ring here)
+  static const int agg_s = [] {
+    const char* e = getenv("OPTR_AGG_STAGES");
+    return (e && e[0] == '4') ? 4 : 2;
+  }();
+  const size_t smem = agg_s == 4 ? tma_agg_smem_bytes<kAggChunk, 4>(ag.n) : tma_agg_smem_bytes<kAggChunk, 2>(ag.n);
+  auto kern = agg_s == 4 ? (ag.n == 2 ? tma_agg_kernel<kAggChunk, 2, 4>
+                            : ag.n == 4 ? tma_agg_kernel<kAggChunk, 4, 4>
+                            : ag.n == 8 ? tma_agg_kernel<kAggChunk, 8, 4>
+                                        : tma_agg_kernel<kAggChunk, 0, 4>)
+                         : (ag.n == 2 ? tma_agg_kernel<kAggChunk, 2, 2>
+                            : ag.n == 4 ? tma_agg_kernel<kAggChunk, 4, 2>
+                            : ag.n == 8 ? tma_agg_kernel<kAggChunk, 8, 2>
+                                        : tma_agg_kernel<kAggChunk, 0, 2>);
   int rc = set_smem_attr(kern, smem);
   if (rc) return rc;
   static int nsm = 0;

@@ -681,17 +681,17 @@ struct TmaAggArgs {
   MaskView m;
 };
 
-template <int CH>
+template <int CH, int S = 2>
 __host__ __device__ constexpr size_t tma_agg_smem_bytes(int n) {
-  return (size_t)2 * n * CH * sizeof(float) + 64 + 1024;
+  return (size_t)S * n * CH * sizeof(float) + 64 + 1024;
 }
 
-template <int CH, int NW>
+template <int CH, int NW, int S = 2>
 __global__ void __launch_bounds__(CH / 4) tma_agg_kernel(const __grid_constant__ TmaAggArgs a) {
   extern __shared__ __align__(16) unsigned char smraw[];
   unsigned char* const base = smraw + ((1024u - (smem_u32(smraw) & 1023u)) & 1023u);
-  float* const buf = reinterpret_cast<float*>(base);  // [2][n][CH]
-  uint64_t* const full = reinterpret_cast<uint64_t*>(base + (size_t)2 * a.n * CH * sizeof(float));
+  float* const buf = reinterpret_cast<float*>(base);  // [S][n][CH]
+  uint64_t* const full = reinterpret_cast<uint64_t*>(base + (size_t)S * a.n * CH * sizeof(float));
   const int tid = threadIdx.x;
   const int n = NW > 0 ? NW : a.n;  // compile-time worker count for the common n
   const int o = a.owner_base + blockIdx.y;
@@ -700,8 +700,7 @@ __global__ void __launch_bounds__(CH / 4) tma_agg_kernel(const __grid_constant__
   const int64_t nchunks = (len + CH - 1) / CH;
   float* const A = a.A[o];
   if (tid == 0) {
-    mbar_init(&full[0], 1);
-    mbar_init(&full[1], 1);
+    for (int s = 0; s < S; ++s) mbar_init(&full[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
@@ -720,13 +719,12 @@ __global__ void __launch_bounds__(CH / 4) tma_agg_kernel(const __grid_constant__
   };
   const int64_t stride = gridDim.x;
   int64_t c = blockIdx.x;
-  if (tid == 0) {
-    if (c < nchunks) issue(c, 0);
-    if (c + stride < nchunks) issue(c + stride, 1);
-  }
+  if (tid == 0)
+    for (int s = 0; s < S; ++s)
+      if (c + s * stride < nchunks) issue(c + s * stride, s);
   for (int k = 0; c < nchunks; ++k, c += stride) {
-    const int s = k & 1;
-    mbar_wait(&full[s], (uint32_t)((k >> 1) & 1));
+    const int s = k % S;
+    mbar_wait(&full[s], (uint32_t)((k / S) & 1));
     const int64_t e = c * CH + tid * 4;
     float4 res = make_float4(0.f, 0.f, 0.f, 0.f);
     if (e < len) {
@@ -752,7 +750,7 @@ __global__ void __launch_bounds__(CH / 4) tma_agg_kernel(const __grid_constant__
                         mean_of(acc[2], (double)c4[2]), mean_of(acc[3], (double)c4[3]));
     }
     __syncthreads();  // stage s has been read
-    if (tid == 0 && c + 2 * stride < nchunks) issue(c + 2 * stride, s);
+    if (tid == 0 && c + S * stride < nchunks) issue(c + S * stride, s);
     if (e + 4 <= len) {
       if (a.push) {
         // stage 2 (collectives.py:133-137): the owner's mean goes to every rank
