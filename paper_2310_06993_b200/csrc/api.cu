@@ -667,8 +667,9 @@ int launch_tma_aggregate(const AggArgs& ag, int nowners, int64_t smax, cudaStrea
     const char* e = getenv("OPTR_AGG_STAGES");
     return (e && e[0] == '4') ? 4 : 2;
   }();
-  const size_t smem = agg_s == 4 ? tma_agg_smem_bytes<kAggChunk, 4>(ag.n) : tma_agg_smem_bytes<kAggChunk, 2>(ag.n);
-  auto kern = agg_s == 4 ? (ag.n == 2 ? tma_agg_kernel<kAggChunk, 2, 4>
+  const bool s4 = agg_s == 4 && ag.n <= 8;  // 4 x n x 4 KB must fit in shared memory
+  const size_t smem = s4 ? tma_agg_smem_bytes<kAggChunk, 4>(ag.n) : tma_agg_smem_bytes<kAggChunk, 2>(ag.n);
+  auto kern = s4 ? (ag.n == 2 ? tma_agg_kernel<kAggChunk, 2, 4>
                             : ag.n == 4 ? tma_agg_kernel<kAggChunk, 4, 4>
                             : ag.n == 8 ? tma_agg_kernel<kAggChunk, 8, 4>
                                         : tma_agg_kernel<kAggChunk, 0, 4>)
