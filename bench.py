@@ -13,7 +13,8 @@ at ``--gpus N>1`` there is one worker per GPU (torchrun, NVLink peer pulls).
 ``value``: whole-job gradient GB/s reduced = workers * bytes(gradient) / step
 time (device time, CUDA events, max over ranks).  ``e2e``: the same through
 the public API with pinned host buffers copied in and results copied out
-inside the timed region.  ``roofline``: the dominant kernel's algorithmic
+inside the timed region, pipelined per bucket (bucket b's D2H overlaps bucket
+b+1's H2D).  ``roofline``: the dominant kernel's algorithmic
 bytes / its live CUDA-event duration against MEASURED_PEAKS.json.
 ``cpu_baseline``: the reference algorithm (oracle port of ubar, numpy, the
 same masks) timed on this host on one bucket.
@@ -262,17 +263,20 @@ def run_ours(args):
     state = {"gen": 0}
     overlap = os.environ.get("OPTR_BENCH_SYNC", "0") != "1"  # A/B switch: buckets in order
 
+    def call_bucket(b, gen, src, dst, async_op):
+        masks = MaskSpec.coin(1000003 * gen + b, drop) if drop > 0 else MaskSpec.none()
+        r = gen % n_workers
+        if multi:
+            comm.allreduce(src[b], dst[b], rotation=r, ht=ht, job_seed=7,
+                           generation=gen, bucket_id=b, masks=masks, async_op=async_op)
+        else:
+            tar_allreduce_local(src[b], rotation=r, ht=ht, job_seed=7, generation=gen,
+                                bucket_id=b, masks=masks, out=dst[b], async_op=async_op)
+
     def one_step(src=None, dst=None):
         gen = state["gen"]
-        for b, L in enumerate(buckets):
-            masks = MaskSpec.coin(1000003 * gen + b, drop) if drop > 0 else MaskSpec.none()
-            r = gen % n_workers
-            if multi:
-                comm.allreduce((src or grads)[b], (dst or outs)[b], rotation=r, ht=ht, job_seed=7,
-                               generation=gen, bucket_id=b, masks=masks, async_op=overlap)
-            else:
-                tar_allreduce_local((src or grads)[b], rotation=r, ht=ht, job_seed=7, generation=gen,
-                                    bucket_id=b, masks=masks, out=(dst or outs)[b], async_op=overlap)
+        for b in range(len(buckets)):
+            call_bucket(b, gen, src or grads, dst or outs, overlap)
         if multi:
             comm.join()
         else:
@@ -340,20 +344,48 @@ def run_ours(args):
         host_in = [[x.cpu().pin_memory() for x in ws] for ws in grads]
         host_out = [[torch.empty_like(h).pin_memory() for h in ws] for ws in host_in]
 
+    # Bucket pipeline (what a DDP comm hook sees): bucket b's H2D on one copy
+    # stream, its TAR call on the compute stream once it has landed, its D2H
+    # on a second copy stream as soon as it is done -- so bucket b's D2H
+    # overlaps bucket b+1's H2D (the two PCIe directions run concurrently).
+    h2d_st = torch.cuda.Stream(dev)
+    d2h_st = torch.cuda.Stream(dev)
+    if multi:
+        dev_in = [torch.empty_like(x) for x in grads]
+        dev_out = [torch.empty_like(x) for x in grads]
+    else:
+        dev_in = [[torch.empty_like(x) for x in ws] for ws in grads]
+        dev_out = [[torch.empty_like(x) for x in ws] for ws in grads]
+
     def e2e_step():
-        if multi:
-            dsrc = [h.to(dev, non_blocking=True) for h in host_in]
-            ddst = [torch.empty_like(x) for x in dsrc]
-            one_step(dsrc, ddst)
-            for h, d in zip(host_out, ddst):
-                h.copy_(d, non_blocking=True)
-        else:
-            dsrc = [[h.to(dev, non_blocking=True) for h in ws] for ws in host_in]
-            ddst = [[torch.empty_like(x) for x in ws] for ws in dsrc]
-            one_step(dsrc, ddst)
-            for hs, ds in zip(host_out, ddst):
-                for h, d in zip(hs, ds):
-                    h.copy_(d, non_blocking=True)
+        gen = state["gen"]
+        h2d_st.wait_stream(stream)
+        d2h_st.wait_stream(stream)
+        landed = []
+        with torch.cuda.stream(h2d_st):
+            for b in range(len(buckets)):
+                if multi:
+                    dev_in[b].copy_(host_in[b], non_blocking=True)
+                else:
+                    for d, h in zip(dev_in[b], host_in[b]):
+                        d.copy_(h, non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(h2d_st)
+                landed.append(ev)
+        for b in range(len(buckets)):
+            stream.wait_event(landed[b])
+            call_bucket(b, gen, dev_in, dev_out, False)
+            done = torch.cuda.Event()
+            done.record(stream)
+            d2h_st.wait_event(done)
+            with torch.cuda.stream(d2h_st):
+                if multi:
+                    host_out[b].copy_(dev_out[b], non_blocking=True)
+                else:
+                    for h, d in zip(host_out[b], dev_out[b]):
+                        h.copy_(d, non_blocking=True)
+        stream.wait_stream(d2h_st)
+        state["gen"] += 1
 
     e2e_step()
     barrier()
@@ -367,7 +399,8 @@ def run_ours(args):
     per_rank_workers = 1 if multi else n_workers
     io_bytes = per_rank_workers * grad_bytes
     e2e = {"value": round(n_workers * grad_bytes / (e2e_ms * 1e-3) / 1e9, 3), "unit": "GB/s",
-           "ms_per_step": round(e2e_ms, 3), "h2d_bytes_per_step": io_bytes, "d2h_bytes_per_step": io_bytes}
+           "ms_per_step": round(e2e_ms, 3), "h2d_bytes_per_step": io_bytes, "d2h_bytes_per_step": io_bytes,
+           "pipeline": "per bucket: H2D stream -> TAR call -> D2H stream (D2H of b overlaps H2D of b+1)"}
 
     # ---- roofline of the dominant kernel class (live CUDA-event durations)
     peaks = load_peaks()
