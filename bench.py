@@ -173,20 +173,22 @@ def step_alg_bytes(buckets, n_workers, s_in, s_out, ht):
 NCU_NAMES = {  # regexes (stage count free: it depends on the tile shape)
     "enc_first": r"tma_pass_kernel<\d+, \d, 0, 1,",
     "enc_last": r"tma_pass_kernel<\d+, \d, 1, 0, SnkBuf",
-    "dec_first": r"tma_pass_kernel<\d+, \d, 1, 2,",
-    "dec_last": r"tma_pass_kernel<\d+, \d, 0, 0, SnkDecode",
+    "dec_first": r"tma_pass_kernel<\d+, \d, [01], 2,",
+    "dec_last": r"tma_pass_kernel<\d+, \d, [01], 0, SnkDecode",
     "aggregate": r"tma_agg_kernel",
     "prep": r"prep_kernel",
 }
 
 
 def ncu_traffic(cls: str, multi: bool):
-    """dram read+write bytes per launch of `cls` from profiles/, or None."""
+    """(dram read+write bytes per launch of `cls`, source file) from profiles/, or None."""
     if multi:
         return None
     import glob
 
+    # the newest capture of the current kernels first (``*_head``), else the latest round's
     files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_ncu_full_1gpu_resnet50.json")))
+    files += sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_ncu_full_1gpu_resnet50_head.json")))
     if not files or cls not in NCU_NAMES:
         return None
     try:
@@ -196,8 +198,7 @@ def ncu_traffic(cls: str, multi: bool):
             if re.search(NCU_NAMES[cls], e["kernel"]):
                 rd, wr = float(e["dram__bytes_read.sum"]), float(e["dram__bytes_write.sum"])
                 scale = 1e6 if rd + wr < 1e5 else 1.0  # the raw page reports MB
-                return {"bytes": int((rd + wr) * scale), "source": os.path.basename(files[-1]),
-                        "note": "cold-cache ncu replay; the live run reuses L2"}
+                return int((rd + wr) * scale), os.path.basename(files[-1])
     except Exception:
         return None
     return None
@@ -438,7 +439,9 @@ def run_ours(args):
                 "traffic": None}
     # DRAM traffic of the dominant kernel from the committed ncu --set full capture
     # (profiles/r01_ncu_full_*.json; per launch = per worker-pass on one GPU)
-    roof["traffic"] = ncu_traffic(dom, multi)
+    tr = ncu_traffic(dom, multi)
+    if tr is not None:
+        roof["traffic"], roof["traffic_src"] = tr[0], tr[1] + " (cold-cache ncu replay; the live run reuses L2)"
     kernels = {k: {"ms_per_step": round(v[0] / args.steps, 4), "launches_per_step": v[1] / args.steps,
                    "avg_launch_us": round(v[0] / v[1] * 1e3, 2),
                    "hbm_gbs": round(class_bytes(k) / (v[0] * 1e-3) / 1e9, 1)}
