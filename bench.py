@@ -142,10 +142,9 @@ def kernel_bytes(cls: str, dim: int, L: int, n: int, s_in: int, s_out: int) -> i
         "dec_last": Y + s_out * L,     # read scratch, write output
         "assemble": Y + s_out * L,
         "prep": dim // 8,
-        # persistent two-pass chains: the intermediate between the passes is
-        # not counted (it is meant to stay in L2), so these are the minimum
-        "enc_chain": s_in * L + Y,     # read x, write the wire
-        "dec_chain": Y + s_out * L,    # gather the aggregates, write the output
+        # one GPU: last encode pass of every worker + stage-1 mean, per
+        # worker: read its first-pass vector, write 1/n of the aggregate
+        "enc_mean": Y + S,
         # multi-GPU fused kernel: contiguous encode pass in place (2Y), owner
         # shard in from n wire vectors + mean out to n receive vectors (local
         # side only: S in, S out), contiguous decode pass in place (2Y)

@@ -187,11 +187,11 @@ int optr_comm_barrier(optr_comm c, void* stream);
 #define OPTR_K_ASSEMBLE 8   /* stage-2 gather without RHT                   */
 #define OPTR_K_BARRIER 9
 #define OPTR_K_OTHER 10
-#define OPTR_K_ENC_CHAIN 11 /* both encode passes, all workers, one launch  */
-#define OPTR_K_DEC_CHAIN 12 /* gather + both decode passes, one launch      */
-#define OPTR_K_FUSED 13     /* multi-GPU: contiguous encode + stage 1 + stage 2
+#define OPTR_K_ENC_MEAN 11  /* one GPU: last encode pass of every worker fused
+                               with the stage-1 mean (wire never written)   */
+#define OPTR_K_FUSED 12     /* multi-GPU: contiguous encode + stage 1 + stage 2
                                + contiguous decode, one persistent launch  */
-#define OPTR_K_CLASSES 14
+#define OPTR_K_CLASSES 13
 /* Enable (1) / disable (0) CUDA-event timing of every kernel launch. */
 int optr_timing_enable(int on);
 /* Debug: event trace of the fused multi-GPU kernel into a device buffer of

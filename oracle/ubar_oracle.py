@@ -300,7 +300,7 @@ def tar_masked(wire: list, r: int, masks: dict, epp: int) -> list:
 def run_generation(buckets: list, job_seed: int, generation: int, ht: bool,
                    masks: dict | None = None, r: int | None = None,
                    epp: int = MAX_PAYLOAD // ENTRY_BYTES, threads: int = 1,
-                   return_wire: bool = False):
+                   return_wire: bool = False, bucket_id: int | None = None):
     """runner.py:211-276 hot-path composition with the channel replaced by
     ``masks``: ht -> RhtContext(derive_seed(seed, g%65536, g)) (:217-222),
     encode every node and cast float32 (:223-225), TAR (:230-246), decode
@@ -308,7 +308,8 @@ def run_generation(buckets: list, job_seed: int, generation: int, ht: bool,
     zeros (:248-258).  rotation r = generation % n unless given (:274-275).
 
     ``threads`` > 1 runs the per-node encode/decode in a thread pool (numpy
-    releases the GIL), used only for the CPU-baseline timing.
+    releases the GIL).  ``bucket_id`` replaces the runner's ``g % 65536`` in
+    the seed derivation (a DDP hook keys the codec by its bucket index).
     """
     n = len(buckets)
     length = len(buckets[0])
@@ -319,7 +320,8 @@ def run_generation(buckets: list, job_seed: int, generation: int, ht: bool,
     try:
         if ht:
             dim = next_pow2(length)
-            signs = rht_signs(dim, derive_seed(job_seed, generation % 65536, generation))
+            bid = generation % 65536 if bucket_id is None else bucket_id
+            signs = rht_signs(dim, derive_seed(job_seed, bid, generation))
             wire = list(pmap(lambda b: rht_encode(b, dim, signs).astype(np.float32), buckets))
         else:
             dim = length

@@ -179,16 +179,20 @@ class AllReduceResult:
 # -------------------------------------------------------- n workers, 1 GPU
 _WS: dict = {}
 _SLOT: dict = {}
+_RETIRED: list = []  # grown-out async workspaces, kept alive until local_join()
 
 
-def _workspace(n: int, L: int, ht: bool, epp: int, device, slot: int = -1):
-    """Cached workspace per device (and per async slot)."""
+def _workspace(n: int, L: int, ht: bool, epp: int, device, key):
+    """Cached workspace per (device, caller stream) for synchronous calls and
+    per (device, slot) for async calls, so calls on different streams never
+    share one."""
     import torch
 
     need = int(lib().optr_tar_local_workspace(n, L, int(ht), epp))
-    key = (str(device), slot)
     ws = _WS.get(key)
     if ws is None or ws.numel() < need:
+        if ws is not None and key[1] == "slot":
+            _RETIRED.append(ws)  # a queued async call may still use it
         ws = torch.empty(max(need, 1), dtype=torch.uint8, device=device)
         _WS[key] = ws
     return ws, need
@@ -201,6 +205,9 @@ def local_join(stream=None):
 
     st = stream if stream is not None else torch.cuda.current_stream()
     check(lib().optr_local_join(st.cuda_stream), "local_join")
+    # workspaces replaced while async calls were queued: the caller's stream
+    # now waits for those calls, so the blocks may return to the allocator
+    _RETIRED.clear()
 
 
 def _dtype_code(t) -> int:
@@ -227,9 +234,9 @@ def tar_allreduce_local(buckets: list, *, rotation: int = 0, ht: bool = False, j
     ``want_received``) the ``[n, dim]`` bool AllReduceResult.received.
     Everything is enqueued on ``stream`` (default: current); no host sync.
     ``async_op=True``: the call runs on one of two library streams (two
-    buckets in flight); ``out`` (and ``counts``/``got`` when requested) are
-    ready only after ``local_join()``; keep every tensor passed in alive and
-    untouched until then.
+    buckets in flight); ``out`` and ``counts`` are ready only after
+    ``local_join()``; keep every tensor passed in or returned alive and
+    untouched until then (``want_received`` needs a synchronous call).
     ``bucket_id`` defaults to ``generation % 65536`` like the runner
     (runner.py:219-222); the RHT seed is derive_seed(job_seed, bucket_id,
     generation).
@@ -246,19 +253,21 @@ def tar_allreduce_local(buckets: list, *, rotation: int = 0, ht: bool = False, j
     for b in buckets:
         if len(b) != L or b.device != dev or b.dtype != buckets[0].dtype or not b.is_contiguous():
             raise ValueError("buckets must be contiguous, same length, dtype and device")
+    if async_op and want_received:
+        raise ValueError("want_received needs a synchronous call (the flags are converted on the stream)")
     masks = masks or MaskSpec.none()
     out_dtype = out_dtype or buckets[0].dtype
-    if out is None:
-        out = [torch.empty(L, dtype=out_dtype, device=dev) for _ in range(n)]
+    st = stream if stream is not None else torch.cuda.current_stream(dev)
     dim = (1 << max(0, (L - 1).bit_length())) if ht else L
-    # async calls run on a library stream the caching allocator does not know
-    # about, so they only write caller-owned tensors: no counts unless asked
-    counts = torch.zeros((2, n), dtype=torch.int64, device=dev) if (not async_op or want_received) else None
-    got = torch.empty((n, dim), dtype=torch.uint8, device=dev) if want_received else None
+    # outputs are allocated on the stream the library call is ordered after
+    with torch.cuda.stream(st):
+        if out is None:
+            out = [torch.empty(L, dtype=out_dtype, device=dev) for _ in range(n)]
+        counts = torch.zeros((2, n), dtype=torch.int64, device=dev)
+        got = torch.empty((n, dim), dtype=torch.uint8, device=dev) if want_received else None
     xs = (ctypes.c_void_p * n)(*[b.data_ptr() for b in buckets])
     os_ = (ctypes.c_void_p * n)(*[o.data_ptr() for o in out])
     spec = masks.to_c()
-    st = stream if stream is not None else torch.cuda.current_stream(dev)
     args = (xs, os_, n, L, _dtype_code(buckets[0]), _dtype_code(out[0]), int(job_seed),
             int(generation % 65536 if bucket_id is None else bucket_id), int(generation), int(rotation),
             int(bool(ht)), ctypes.byref(spec))
@@ -267,17 +276,18 @@ def tar_allreduce_local(buckets: list, *, rotation: int = 0, ht: bool = False, j
         key = str(dev)
         slot = _SLOT.get(key, 0)
         _SLOT[key] = slot ^ 1
-        ws, need = _workspace(n, L, ht, masks.epp, dev, slot)
-        check(lib().optr_tar_local_async(*args, ws.data_ptr(), need,
-                                         counts.data_ptr() if counts is not None else None,
-                                         got.data_ptr() if got is not None else None, slot, st.cuda_stream),
+        ws, need = _workspace(n, L, ht, masks.epp, dev, (key, "slot", slot))
+        check(lib().optr_tar_local_async(*args, ws.data_ptr(), need, counts.data_ptr(), None, slot, st.cuda_stream),
               "tar_allreduce_local")
     else:
-        ws, need = _workspace(n, L, ht, masks.epp, dev)
+        ws, need = _workspace(n, L, ht, masks.epp, dev, (str(dev), "stream", st.cuda_stream))
         check(lib().optr_tar_local(*args, ws.data_ptr(), need, counts.data_ptr(),
                                    got.data_ptr() if got is not None else None, st.cuda_stream),
               "tar_allreduce_local")
-    return out, counts, (got.bool() if got is not None else None)
+        if got is not None:
+            with torch.cuda.stream(st):
+                got = got.bool()
+    return out, counts, got
 
 
 def tar_allreduce(entries: list, *, r: int = 0, masks: MaskSpec | None = None) -> list:

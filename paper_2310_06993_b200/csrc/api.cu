@@ -102,27 +102,6 @@ int bind_device(void* stream) {
 constexpr int kContigBits = 13;
 constexpr int kColBits = 3;
 
-// OPTR_WIDE=1 uses a 14+9 split with 128-byte strided rows at D = 2^23
-// (fewer TMA requests, but 16K-entry tiles fit one CTA per SM: measured
-// slower than the default 13+10 split with three CTAs per SM).
-bool wide_rows() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("OPTR_WIDE");
-    v = (e && e[0] == '1') ? 1 : 0;
-  }
-  return v == 1;
-}
-
-bool wide3_rows() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("OPTR_WIDE3");
-    v = (e && e[0] == '0') ? 0 : 1;
-  }
-  return v == 1;
-}
-
 int plan_passes(int n, PassGeom* out, bool encode_order) {
   // A contiguous pass on 2^c-entry tiles plus strided passes of <= 11 row
   // bits on 2^ks x 8 tiles (T = ks + 3 <= 14: one CTA's registers).  Encode
@@ -133,10 +112,6 @@ int plan_passes(int n, PassGeom* out, bool encode_order) {
   int np = 0;
   if (n <= kContigBits) {
     p[np++] = PassGeom{0, n, 0, 1};
-  } else if (n == 23 && wide_rows()) {
-    // 16K-entry contiguous tiles + 512 x 32 strided tiles: 128-byte rows
-    p[np++] = PassGeom{0, 14, 0, 0};
-    p[np++] = PassGeom{14, 9, 5, 0};
   } else if (n <= kContigBits + 11) {
     p[np++] = PassGeom{0, kContigBits, 0, 0};
     p[np++] = PassGeom{kContigBits, n - kContigBits, kColBits, 0};
@@ -150,7 +125,7 @@ int plan_passes(int n, PassGeom* out, bool encode_order) {
     // TB/s).  OPTR_WIDE3=0 keeps 8 columns.
     int rest = n - kContigBits;
     int k1 = rest / 2;
-    const int cb = (wide3_rows() && rest - k1 + 5 <= 14) ? 5 : kColBits;
+    const int cb = rest - k1 + 5 <= 14 ? 5 : kColBits;
     p[np++] = PassGeom{0, kContigBits, 0, 0};
     p[np++] = PassGeom{kContigBits, k1, cb, 0};
     p[np++] = PassGeom{kContigBits + k1, rest - k1, cb, 0};
@@ -236,16 +211,8 @@ int launch_smem(int cls, const PassGeom& pg, int worker_base, int nworkers, cons
 
 // Launch with programmatic stream serialization (PDL) so the kernel is
 // scheduled while its predecessor drains; the kernels call
-// griddepcontrol.wait before touching dependent memory.  OPTR_PDL=0 disables.
-bool pdl_enabled() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("OPTR_PDL");
-    v = (e && e[0] == '0') ? 0 : 1;
-  }
-  return v == 1;
-}
-
+// griddepcontrol.wait before touching dependent memory.  Off while timing
+// (the per-launch events would serialise anyway).
 template <class K, class... Args>
 cudaError_t launch_ex(K kernel, dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {
   cudaLaunchConfig_t cfg;
@@ -258,7 +225,7 @@ cudaError_t launch_ex(K kernel, dim3 grid, dim3 block, size_t smem, cudaStream_t
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = pdl_enabled() && !g_timing ? 1 : 0;
+  cfg.numAttrs = g_timing ? 0 : 1;
   return cudaLaunchKernelEx(&cfg, kernel, args...);
 }
 
@@ -266,11 +233,11 @@ cudaError_t launch_ex(K kernel, dim3 grid, dim3 block, size_t smem, cudaStream_t
 PFN_cuTensorMapEncodeTiled_v12000 g_encode_tiled = nullptr;
 int g_tma_mode = -1;  // -1 unknown, 0 off, 1 on
 
+// TMA tensor maps need the driver's cuTensorMapEncodeTiled
 bool tma_enabled() {
   if (g_tma_mode < 0) {
-    const char* e = getenv("OPTR_TMA");
-    g_tma_mode = (e && e[0] == '0') ? 0 : 1;
-    if (g_tma_mode) {
+    g_tma_mode = 1;
+    {
       cudaDriverEntryPointQueryResult q;
       if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void**)&g_encode_tiled, cudaEnableDefault, &q) !=
               cudaSuccess ||
@@ -324,29 +291,15 @@ int launch_tma_pass_s(int cls, const TmaMaps& maps, const TmaMaps& dmaps, const 
 // ring depth of the TMA pass kernels: 2, strided T >= 13 tiles 3 (D = 2^25:
 // the strided pass waits on its 32-byte-row TMA boxes with one CTA per SM;
 // a third stage takes it from 90 to 60 us; at D = 2^23 with the workers
-// batched, 2 CTAs x 3 stages beat 3 x 2 by ~2%; contiguous is flat from 2 up).
-// OPTR_TMA_STAGES (1..3) overrides both, OPTR_TMA_STAGES_C / _S one kind.
-int tma_stages(bool strided) {
-  static int s[2] = {0, 0};
-  int& v = s[strided ? 1 : 0];
-  if (!v) {
-    const char* e = getenv(strided ? "OPTR_TMA_STAGES_S" : "OPTR_TMA_STAGES_C");
-    if (!e) e = getenv("OPTR_TMA_STAGES");
-    v = (e && e[0] >= '1' && e[0] <= '3') ? e[0] - '0' : -1;  // -1: per-shape default
-  }
-  return v;
-}
-
+// batched, 2 CTAs x 3 stages beat 3 x 2 by ~2%; contiguous is flat from 2 up;
+// profiles/r01_stage_sweep.jsonl).
 template <int T, bool STRIDED, int SK, class Snk, int CBW = 3>
 int launch_tma_pass(int cls, const TmaMaps& maps, const TmaMaps& dmaps, const TmaArgs& a, const Snk& snk,
                     int worker, int nworkers, cudaStream_t st) {
-  int S = tma_stages(STRIDED);
-  if (S < 0) S = (STRIDED && T >= 13) ? 3 : 2;
-  switch (S) {
-    case 1: return launch_tma_pass_s<T, 1, STRIDED, SK, Snk, CBW>(cls, maps, dmaps, a, snk, worker, nworkers, st);
-    case 3: return launch_tma_pass_s<T, 3, STRIDED, SK, Snk, CBW>(cls, maps, dmaps, a, snk, worker, nworkers, st);
-    default: return launch_tma_pass_s<T, 2, STRIDED, SK, Snk, CBW>(cls, maps, dmaps, a, snk, worker, nworkers, st);
-  }
+  if constexpr (STRIDED && T >= 13)
+    return launch_tma_pass_s<T, 3, STRIDED, SK, Snk, CBW>(cls, maps, dmaps, a, snk, worker, nworkers, st);
+  else
+    return launch_tma_pass_s<T, 2, STRIDED, SK, Snk, CBW>(cls, maps, dmaps, a, snk, worker, nworkers, st);
 }
 
 // A pass through the TMA ring kernel when the shapes allow it; -1 when the
@@ -488,163 +441,6 @@ int try_tma(int cls, const PassGeom& pg, int nlog, int worker, int nworkers, con
   }
 }
 
-// ---------------------------------------------- persistent two-pass chain
-// OPTR_CHAIN=1 opts in (measured slower than the separate pass launches on
-// the default workloads: the per-tile pipeline, not launch ramps, limits).
-bool chain_enabled() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("OPTR_CHAIN");
-    v = (e && e[0] == '1') ? 1 : 0;
-  }
-  return v == 1;
-}
-
-constexpr int kChainCtrWords = 2 + kMaxW;
-
-// Self-resetting ticket/dependency counters of the chain kernel, one block
-// per stream that launches chains (zeroed once, on that stream).
-unsigned int* chain_counters(int key, cudaStream_t st) {
-  static unsigned int* pool[64][8] = {};
-  int dev = 0;
-  cudaGetDevice(&dev);
-  std::lock_guard<std::mutex> lk(g_attr_mu);
-  unsigned int*& p = pool[dev & 63][key & 7];
-  if (!p) {
-    if (cudaMalloc(&p, kChainCtrWords * sizeof(unsigned int)) != cudaSuccess) {
-      p = nullptr;
-      return nullptr;
-    }
-    if (cudaMemsetAsync(p, 0, kChainCtrWords * sizeof(unsigned int), st) != cudaSuccess) return nullptr;
-  }
-  return p;
-}
-
-template <int T, int S, int SK0, class Snk1>
-int launch_chain_s(int cls, const TmaMaps& maps1, const TmaMaps& dmaps1, const TmaArgs& a0, const TmaArgs& a1,
-                   const SnkBuf& snk0, const Snk1& snk1, const ChainSched& cs, int nworkers, cudaStream_t st) {
-  const size_t smem = tma_chain_smem_bytes<T, S>();
-  auto kern = tma_chain_kernel<T, S, SK0, Snk1, 3>;
-  int rc = set_smem_attr(kern, smem);
-  if (rc) return rc;
-  static int nsm = 0;
-  if (!nsm) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    if (nsm <= 0) nsm = 148;
-  }
-  int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 1 << (T - 5), smem) != cudaSuccess ||
-      per_sm < 1)
-    per_sm = 1;
-  int64_t gx = (int64_t)nsm * per_sm;
-  const int64_t total = cs.jstart[cs.njobs];
-  if (gx > total) gx = total;
-  KScope ks(cls, st, nworkers);
-  launch_ex(kern, dim3((unsigned)gx), dim3(1 << (T - 5)), smem, st, maps1, dmaps1, a0, a1, snk0, snk1, cs);
-  return launch_check(kern, "tma_chain", T, 3, (int)gx, 1, 1 << (T - 5), smem);
-}
-
-// Both passes of a two-pass transform for workers [wb, wb+nw) in one
-// persistent launch (contiguous pass first, fused source; strided pass
-// second, fused sink).  -1 when the plan or the buffers do not fit it.
-template <class Src, class Snk>
-int try_chain(int cls, int nlog, int wb, int nw, const Src& src, const SrcBuf& buf, const Snk& snk,
-              unsigned int* ctr, cudaStream_t st) {
-  constexpr bool kBuf = std::is_same<Src, SrcBuf>::value;
-  constexpr bool kEnc = std::is_same<Src, SrcEncode>::value;
-  constexpr bool kGather = std::is_same<Src, SrcGather>::value;
-  constexpr bool kSnkBuf = std::is_same<Snk, SnkBuf>::value;
-  constexpr bool kSnkDec = std::is_same<Snk, SnkDecode>::value;
-  if constexpr (!(kBuf || kEnc || kGather) || !(kSnkBuf || kSnkDec)) {
-    return -1;
-  } else {
-    if (!ctr || !chain_enabled() || !tma_enabled()) return -1;
-    PassGeom ps[3];
-    if (plan_passes(nlog, ps, true) != 2) return -1;
-    const int T = ps[0].ks;
-    if (ps[0].cb != 0 || ps[0].lo != 0 || (T != 13 && T != 14)) return -1;
-    if (ps[1].cb != 3 || ps[1].lo != T || ps[1].ks + 3 != T) return -1;
-    TmaArgs a0, a1;
-    memset(&a0, 0, sizeof(a0));
-    memset(&a1, 0, sizeof(a1));
-    TmaMaps maps1, dmaps1;
-    memset(&maps1, 0, sizeof(maps1));
-    memset(&dmaps1, 0, sizeof(dmaps1));
-    a0.ntiles = ps[0].ntiles;
-    for (int w = wb; w < wb + nw; ++w) {
-      if constexpr (kBuf) a0.xw[w] = src.y[w];
-      if constexpr (kEnc) {
-        a0.xw[w] = src.x[w];
-        if (((uintptr_t)a0.xw[w] & 15) || ((uintptr_t)src.signs & 15)) return -1;
-      }
-    }
-    if constexpr (kEnc) {
-      a0.dtype = src.dtype;
-      a0.L = src.L;
-      a0.signs = src.signs;
-    }
-    if constexpr (kGather) {
-      if (src.pow2_shift < T) return -1;
-      for (int o = 0; o < src.n; ++o) a0.A[o] = src.A[o];
-      a0.n = src.n;
-      a0.r = src.r;
-      a0.shard_shift = src.pow2_shift;
-      a0.m = src.m;
-      a0.got = src.got;
-      a0.dim = src.dim;
-    }
-    const uint64_t d0 = 1ULL << T, d1 = 1ULL << ps[1].ks;
-    const int box = (int)(d1 < 256 ? d1 : 256);
-    for (int w = wb; w < wb + nw; ++w) {
-      if (!make_map3(&maps1.m[w], buf.y[w], d0, d1, 1, (uint32_t)box)) return -1;
-      if constexpr (kSnkBuf) {
-        if (!make_map3(&dmaps1.m[w], snk.y[w], d0, d1, 1, (uint32_t)box)) return -1;
-      } else {
-        const int64_t rows_full = snk.L >> T;
-        if (rows_full > 0 && !make_map3(&dmaps1.m[w], snk.out[w], d0, (uint64_t)rows_full, 1, (uint32_t)box,
-                                        snk.dtype))
-          return -1;
-        if (((uintptr_t)snk.out[w] & 15) || ((uintptr_t)snk.signs & 15)) return -1;
-      }
-    }
-    a1.ntiles = ps[1].ntiles;
-    a1.lo = T;
-    a1.box_rows = box;
-    if constexpr (kSnkBuf) a1.scale = snk.scale;
-    SnkBuf mid;
-    memset(&mid, 0, sizeof(mid));
-    for (int i = 0; i < kMaxW; ++i) mid.y[i] = buf.y[i];
-    mid.scale = 1.f;
-    ChainSched cs;
-    memset(&cs, 0, sizeof(cs));
-    cs.ctr = ctr;
-    cs.nw = kMaxW;
-    cs.nt0 = ps[0].ntiles;
-    cs.nt1 = ps[1].ntiles;
-    // w0.p0, w1.p0, w0.p1, w2.p0, w1.p1, ...: a worker's second pass follows
-    // one other worker's first pass
-    int64_t tk = 0;
-    auto add = [&](int pass, int w) {
-      cs.jpass[cs.njobs] = (int8_t)pass;
-      cs.jw[cs.njobs] = (int8_t)w;
-      cs.jstart[cs.njobs] = tk;
-      tk += pass == 0 ? cs.nt0 : cs.nt1;
-      ++cs.njobs;
-    };
-    for (int i = 0; i < nw; ++i) {
-      add(0, wb + i);
-      if (i > 0) add(1, wb + i - 1);
-    }
-    add(1, wb + nw - 1);
-    cs.jstart[cs.njobs] = tk;
-    constexpr int SK0 = kBuf ? TS_BUF : (kEnc ? TS_ENC : TS_GATHER);
-    if (T == 13) return launch_chain_s<13, 2, SK0>(cls, maps1, dmaps1, a0, a1, mid, snk, cs, nw, st);
-    return launch_chain_s<14, 2, SK0>(cls, maps1, dmaps1, a0, a1, mid, snk, cs, nw, st);
-  }
-}
-
 constexpr int kAggChunk = 1024;
 
 int launch_tma_aggregate(const AggArgs& ag, int nowners, int64_t smax, cudaStream_t st) {
@@ -661,22 +457,13 @@ int launch_tma_aggregate(const AggArgs& ag, int nowners, int64_t smax, cudaStrea
   a.r = ag.r;
   a.owner_base = ag.owner_base;
   a.m = ag.m;
-  // chunk ring depth: OPTR_AGG_STAGES=4 (default 2; 4 measured slower on one
-  // GPU, 1.013 vs 0.988 ms/step: more CTAs per SM beat a deeper ring here)
-  static const int agg_s = [] {
-    const char* e = getenv("OPTR_AGG_STAGES");
-    return (e && e[0] == '4') ? 4 : 2;
-  }();
-  const bool s4 = agg_s == 4 && ag.n <= 8;  // 4 x n x 4 KB must fit in shared memory
-  const size_t smem = s4 ? tma_agg_smem_bytes<kAggChunk, 4>(ag.n) : tma_agg_smem_bytes<kAggChunk, 2>(ag.n);
-  auto kern = s4 ? (ag.n == 2 ? tma_agg_kernel<kAggChunk, 2, 4>
-                            : ag.n == 4 ? tma_agg_kernel<kAggChunk, 4, 4>
-                            : ag.n == 8 ? tma_agg_kernel<kAggChunk, 8, 4>
-                                        : tma_agg_kernel<kAggChunk, 0, 4>)
-                         : (ag.n == 2 ? tma_agg_kernel<kAggChunk, 2, 2>
-                            : ag.n == 4 ? tma_agg_kernel<kAggChunk, 4, 2>
-                            : ag.n == 8 ? tma_agg_kernel<kAggChunk, 8, 2>
-                                        : tma_agg_kernel<kAggChunk, 0, 2>);
+  // chunk ring depth 2 (4 measured slower on one GPU, 1.013 vs 0.988 ms/step:
+  // more CTAs per SM beat a deeper ring here)
+  const size_t smem = tma_agg_smem_bytes<kAggChunk, 2>(ag.n);
+  auto kern = ag.n == 2 ? tma_agg_kernel<kAggChunk, 2, 2>
+              : ag.n == 4 ? tma_agg_kernel<kAggChunk, 4, 2>
+              : ag.n == 8 ? tma_agg_kernel<kAggChunk, 8, 2>
+                          : tma_agg_kernel<kAggChunk, 0, 2>;
   int rc = set_smem_attr(kern, smem);
   if (rc) return rc;
   static int nsm = 0;
@@ -782,66 +569,15 @@ int launch_aggregate(const AggArgs& ag, int nowners, int64_t smax, cudaStream_t 
 
 Pcg sign_pcg(uint64_t seed) { return pcg_from_u64s(&seed, 1); }
 
-// Decode pass order.  Multi-GPU: contiguous first, so the stage-2 receive
-// pulls whole owner chunks over NVLink (bulk copies) and the strided pass
-// finishes into `out` with the decode epilogue.  One GPU: strided first,
-// gathering from the L2-resident aggregates, contiguous last into `out`.
-// OPTR_DEC_ORDER=strided|contig overrides.
-// OPTR_STAGE2=pull keeps the stage-2 pull inside the decode pass.
-bool stage2_push() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("OPTR_STAGE2");
-    v = (e && e[0] == 'p' && e[1] == 'u' && e[2] == 'l') ? 0 : 1;
-  }
-  return v == 1;
-}
-
-// One GPU: contiguous-first when the plan allows transposed decode signs and
-// the TMA decode epilogue (two passes, 8-column strided tiles of T >= 12),
-// else strided-first.
-bool decode_contig_first_local(bool two_pass) {
-  static int v = -2;
-  if (v == -2) {
-    const char* e = getenv("OPTR_DEC_ORDER");
-    v = !e ? -1 : (e[0] == 's' ? 0 : 1);
-  }
-  return v < 0 ? two_pass : v == 1;
-}
-
-bool decode_contig_first(bool multi_gpu) {
-  static int v = -2;
-  if (v == -2) {
-    const char* e = getenv("OPTR_DEC_ORDER");
-    v = !e ? -1 : (e[0] == 's' ? 0 : 1);
-  }
-  return v < 0 ? multi_gpu : v == 1;
-}
-
-// Workers per transform launch: all of them (default; at D = 2^23 this
-// matches per-worker launches chained through L2 on helper streams in step
-// time, 1.01 vs 0.99 ms, with one launch per pass instead of four
-// concurrent ones).  OPTR_BATCH_WORKERS=0: batch only while the vectors fit
-// in half of L2, otherwise one worker at a time on the helper streams so each
-// worker's vector stays L2-resident between its passes.
-int workers_per_launch(int64_t dim, int n) {
-  static int l2 = 0;
-  if (!l2) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev) != cudaSuccess || l2 <= 0) l2 = 50 << 20;
-  }
-  static int batch = -1;
-  if (batch < 0) {
-    const char* e = getenv("OPTR_BATCH_WORKERS");
-    batch = (e && e[0] == '0') ? 0 : 1;
-  }
-  if (batch) return n;
-  int64_t bytes = dim * 4;
-  int k = (int)((int64_t)l2 / 2 / (bytes > 0 ? bytes : 1));
-  if (k < 1) k = 1;
-  if (k > n) k = n;
-  return k;
+// Decode pass order: contiguous first (the stage-2 receive then works on
+// whole packets per tile, and over NVLink pulls whole owner chunks with bulk
+// copies) whenever the strided pass can finish into `out` with the TMA decode
+// epilogue and transposed signs (two passes, 8-column strided tiles of
+// T >= 12); strided first otherwise.
+// Multi-GPU (unfused) always decodes contiguous-first.
+bool decode_contig_first(int nlog, bool multi_gpu) {
+  PassGeom ps[3];
+  return multi_gpu || (plan_passes(nlog, ps, true) == 2 && ps[1].cb == 3 && ps[1].ks + 3 >= 12);
 }
 
 void fill_sign_args(PrepArgs& a, uint32_t* signs, int64_t dim, uint64_t seed) {
@@ -1010,25 +746,10 @@ int optr_rht_encode(const void* x, int dtype_in, int64_t L, float* y, int64_t di
   cudaStream_t st = (cudaStream_t)stream;
   uint32_t* signs = nullptr;
   size_t sbytes = (size_t)((dim + 31) / 32) * 4;
-  // OPTR_ENC_ORDER=strided: the fused multi-GPU path's order (strided pass
-  // first, transposed sign bytes) on one GPU, for profiling that pass alone
-  static int strided_first = -1;
-  if (strided_first < 0) {
-    const char* e = getenv("OPTR_ENC_ORDER");
-    strided_first = (e && e[0] == 's') ? 1 : 0;
-  }
-  PassGeom ps[3];
-  const int np = plan_passes(log2_exact(dim > 0 ? dim : 1), ps, true);
-  const bool sf = strided_first && np == 2 && ps[1].cb == 3;
-  CK(cudaMallocAsync((void**)&signs, sbytes * (sf ? 2 : 1) + 16, st));
+  CK(cudaMallocAsync((void**)&signs, sbytes + 16, st));
   PrepArgs a;
   memset(&a, 0, sizeof(a));
   fill_sign_args(a, signs, dim, seed);
-  if (sf) {
-    a.signs_t = (uint8_t*)signs + sbytes;
-    a.t_lo = ps[1].lo;
-    a.t_ks = ps[1].ks;
-  }
   int rc = launch_prep(a, st);
   if (!rc) {
     SrcEncode src;
@@ -1037,7 +758,6 @@ int optr_rht_encode(const void* x, int dtype_in, int64_t L, float* y, int64_t di
     src.dtype = dtype_in;
     src.L = L;
     src.signs = signs;
-    src.signs_t = a.signs_t;
     SrcBuf buf;
     memset(&buf, 0, sizeof(buf));
     buf.y[0] = y;
@@ -1045,15 +765,7 @@ int optr_rht_encode(const void* x, int dtype_in, int64_t L, float* y, int64_t di
     memset(&snk, 0, sizeof(snk));
     snk.y[0] = y;
     snk.scale = (float)(1.0 / sqrt((double)dim));
-    if (sf) {
-      SnkBuf mid = snk;
-      mid.scale = 1.f;
-      const int nlog = log2_exact(dim);
-      rc = launch_pass(OPTR_K_ENC_FIRST, ps[1], nlog, 0, 1, src, mid, st);
-      if (!rc) rc = launch_pass(OPTR_K_ENC_LAST, ps[0], nlog, 0, 1, buf, snk, st);
-    } else {
-      rc = run_transform(log2_exact(dim), true, 0, 1, src, buf, snk, st, OPTR_K_ENC_FIRST);
-    }
+    rc = run_transform(log2_exact(dim), true, 0, 1, src, buf, snk, st, OPTR_K_ENC_FIRST);
   }
   cudaFreeAsync(signs, st);
   return rc;
@@ -1115,85 +827,8 @@ int optr_rht_decode(const float* y, const uint8_t* mask, int64_t dim, int64_t L,
 }  // extern "C"
 
 namespace {
-// ------------------------------------------------------- helper streams
-// Per-worker pass chains run on two helper streams forked from (and joined
-// back into) the caller's stream, so one worker's passes fill the ramp and
-// tail of the other's while both vectors stay L2-resident.
-constexpr int kHelpers = 2;
-struct Helpers {
-  bool init = false;
-  cudaStream_t s[kHelpers];
-  cudaEvent_t fork;
-  cudaEvent_t join[kHelpers];
-  std::mutex mu;
-};
-// set 0: synchronous calls; sets 1, 2: async calls of slot 0, 1
-Helpers g_help[64][3];
-
-Helpers* helpers(int set) {
-  int dev = 0;
-  cudaGetDevice(&dev);
-  Helpers* h = &g_help[dev & 63][set];
-  std::lock_guard<std::mutex> lk(g_attr_mu);
-  if (!h->init) {
-    for (int i = 0; i < kHelpers; ++i) {
-      if (cudaStreamCreateWithFlags(&h->s[i], cudaStreamNonBlocking) != cudaSuccess) return nullptr;
-      if (cudaEventCreateWithFlags(&h->join[i], cudaEventDisableTiming) != cudaSuccess) return nullptr;
-    }
-    if (cudaEventCreateWithFlags(&h->fork, cudaEventDisableTiming) != cudaSuccess) return nullptr;
-    h->init = true;
-  }
-  return h;
-}
-
-int fork_helpers(Helpers* h, cudaStream_t st) {
-  CK(cudaEventRecord(h->fork, st));
-  for (int i = 0; i < kHelpers; ++i) CK(cudaStreamWaitEvent(h->s[i], h->fork, 0));
-  return OPTR_OK;
-}
-
-int join_helpers(Helpers* h, cudaStream_t st) {
-  for (int i = 0; i < kHelpers; ++i) {
-    CK(cudaEventRecord(h->join[i], h->s[i]));
-    CK(cudaStreamWaitEvent(st, h->join[i], 0));
-  }
-  return OPTR_OK;
-}
-
-// Run `fn(worker_base, nworkers, stream)` over all n workers: batched while
-// they fit in L2 together, else one worker per launch on the helper streams.
-template <class F>
-int for_workers(int64_t dim, int n, cudaStream_t st, int set, F fn) {
-  const int k = workers_per_launch(dim, n);
-  if (k >= n) return fn(0, n, st);
-  Helpers* h = helpers(set);
-  if (!h) {
-    for (int w0 = 0; w0 < n; w0 += k) {
-      int rc = fn(w0, (n - w0 < k ? n - w0 : k), st);
-      if (rc) return rc;
-    }
-    return OPTR_OK;
-  }
-  static int chains = -1;
-  if (chains < 0) {
-    const char* e = getenv("OPTR_CHAINS");
-    chains = e ? atoi(e) : kHelpers;
-    if (chains < 1 || chains > kHelpers) chains = kHelpers;
-  }
-  std::lock_guard<std::mutex> lk(h->mu);
-  int rc = fork_helpers(h, st);
-  if (rc) return rc;
-  int i = 0;
-  for (int w0 = 0; w0 < n; w0 += k, ++i) {
-    rc = fn(w0, (n - w0 < k ? n - w0 : k), h->s[i % chains]);
-    if (rc) break;
-  }
-  int rc2 = join_helpers(h, st);
-  return rc ? rc : rc2;
-}
-
-// Async co-resident calls: two slots, each with its own work stream and
-// helper-stream set, so consecutive buckets overlap (one bucket's aggregate
+// Async co-resident calls: two slots, each with its own work stream, so
+// consecutive buckets overlap (one bucket's aggregate
 // and decode with the next one's encode).
 struct LocalAsync {
   bool init = false;
@@ -1304,10 +939,62 @@ int optr_local_join(void* stream) {
 }  // extern "C"
 
 namespace {
+// Fast one-GPU plan (RHT on, D = 2^23..2^25, equal power-of-two shards of
+// whole contiguous tiles): strided encode pass from x (signs, pad, cast) ->
+// contiguous encode pass of every worker fused with the stage-1 mean
+// (tma_mean_kernel: the wire vectors never reach memory) -> contiguous decode
+// pass with the stage-2 receive from the aggregate -> strided decode pass
+// into `out`.  Four launches per bucket; -1 when the shapes do not fit.
+struct FastPlan {
+  PassGeom contig, strided;
+  int nlog;
+};
+
+bool local_fast_plan(int64_t L, int64_t dim, int n, int ht, const void* const* x, void* const* out,
+                     FastPlan* fp) {
+  if (!ht || !tma_enabled() || !is_pow2(dim)) return false;
+  PassGeom ps[3];
+  const int nlog = log2_exact(dim);
+  if (plan_passes(nlog, ps, true) != 2) return false;
+  const int Tc = ps[0].ks, Ts = ps[1].ks + ps[1].cb;
+  if (ps[0].cb != 0 || (Tc != 13 && Tc != 14) || ps[1].cb != 3 || (Ts != 13 && Ts != 14)) return false;
+  const Shards sh = make_shards(dim, n);
+  if (sh.extra != 0 || !is_pow2(sh.base) || sh.base < (1LL << Tc)) return false;
+  if ((L >> ps[1].lo) < 1) return false;
+  for (int w = 0; w < n; ++w)
+    if (((uintptr_t)x[w] & 15) || ((uintptr_t)out[w] & 15)) return false;
+  fp->contig = ps[0];
+  fp->strided = ps[1];
+  fp->nlog = nlog;
+  return true;
+}
+
+template <int T>
+int launch_mean_t(const TmaArgs& a, const MeanArgs& m, cudaStream_t st) {
+  constexpr int S = 2;
+  const size_t smem = tma_smem_bytes<T, S>();
+  auto kern = tma_mean_kernel<T, S>;
+  int rc = set_smem_attr(kern, smem);
+  if (rc) return rc;
+  int dev = 0, nsm = 148, per_sm = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 1 << (T - 5), smem) != cudaSuccess || per_sm < 1)
+    per_sm = 1;
+  // equal tile counts per CTA (no tail of CTAs with one tile more)
+  const int64_t cap = (int64_t)nsm * per_sm;
+  const int64_t per_cta = (a.ntiles + cap - 1) / cap;
+  const int64_t gx = (a.ntiles + per_cta - 1) / per_cta;
+  KScope ks(OPTR_K_ENC_MEAN, st, m.n);
+  launch_ex(kern, dim3((unsigned)gx), dim3(1 << (T - 5)), smem, st, a, m);
+  return launch_check(kern, "tma_mean", T, 0, (int)gx, 1, 1 << (T - 5), smem);
+}
+
 int tar_local_impl(const void* const* x, void* const* out, int n, int64_t L, int dtype_in, int dtype_out,
                    uint64_t job_seed, uint64_t bucket_id, uint64_t generation, int rotation, int ht,
                    const optr_mask_spec* masks, void* workspace, size_t workspace_bytes,
                    uint64_t* received_out, uint8_t* got_out, cudaStream_t st, int set) {
+  (void)set;
   int rc = check_common(n, L, dtype_in, dtype_out, masks);
   if (rc) return rc;
   if (!x || !out || !workspace) return OPTR_EINVAL;
@@ -1323,19 +1010,23 @@ int tar_local_impl(const void* const* x, void* const* out, int n, int64_t L, int
   uint32_t* signs = (uint32_t*)(ws + lay.signs);
   uint32_t* bitmap = (uint32_t*)(ws + lay.bitmap);
   unsigned long long* counts = (unsigned long long*)(ws + lay.counts);
+  const Shards sh = make_shards(dim, n);
+  FastPlan fp;
+  const bool fast = local_fast_plan(L, dim, n, ht, x, out, &fp);
+  const int nlog = ht ? log2_exact(dim) : 0;
 
-  // 1. signs + masks + counts
+  // 1. signs (+ transposed sign bytes for the strided passes) + masks + counts
   CK(cudaMemsetAsync(counts, 0, (size_t)2 * n * 8, st));
   PrepArgs pa;
   memset(&pa, 0, sizeof(pa));
   if (ht) fill_sign_args(pa, signs, dim, derive_seed(job_seed, bucket_id, generation));
-  // two-pass plans decode contiguous-first (the stage-2 gather on whole
-  // packets) and finish with the strided pass, whose signs come from the
-  // transposed sign bytes (coalesced, one bulk copy per tile)
+  // general plan: two-pass plans decode contiguous-first and finish with the
+  // strided pass, whose signs come from the transposed sign bytes
   PassGeom dps[3];
-  const int dnp = ht ? plan_passes(log2_exact(dim), dps, true) : 0;
-  const bool dec_cf = decode_contig_first_local(dnp == 2 && dps[1].cb == 3 && dps[1].ks + 3 >= 12);
-  uint8_t* const signs_t = (ht && dec_cf && dnp == 2 && dps[1].cb == 3) ? (uint8_t*)(ws + lay.signs_t) : nullptr;
+  const int dnp = ht ? plan_passes(nlog, dps, true) : 0;
+  const bool dec_cf = ht && decode_contig_first(nlog, false);
+  uint8_t* const signs_t =
+      (ht && (fast || (dec_cf && dnp == 2 && dps[1].cb == 3))) ? (uint8_t*)(ws + lay.signs_t) : nullptr;
   if (signs_t) {
     pa.signs_t = signs_t;
     pa.t_lo = dps[1].lo;
@@ -1345,8 +1036,75 @@ int tar_local_impl(const void* const* x, void* const* out, int n, int64_t L, int
   if ((rc = setup_masks(pa, masks, dim, n, r, epp, bitmap, counts, 0, n, &cbits))) return rc;
   if ((rc = launch_prep(pa, st))) return rc;
   MaskView mv{cbits, pa.pw, n, epp, make_divider((uint32_t)epp)};
-  Shards sh = make_shards(dim, n);
 
+  // stage-2 receive source (collectives.py:140-150)
+  SrcGather ga;
+  memset(&ga, 0, sizeof(ga));
+  ga.sh = sh;
+  ga.n = n;
+  ga.r = r;
+  ga.m = mv;
+  ga.got = got_out;
+  ga.dim = dim;
+  ga.pow2_shift = (sh.extra == 0 && is_pow2(sh.base)) ? log2_exact(sh.base) : -1;
+  SnkDecode dec;
+  memset(&dec, 0, sizeof(dec));
+  for (int w = 0; w < n; ++w) {
+    dec.out[w] = out[w];
+    dec.count_base[w] = sh.len(owned_shard(w, r, n));
+  }
+  dec.dtype = dtype_out;
+  dec.L = L;
+  dec.signs = signs;
+  dec.signs_t = signs_t;
+  dec.count_extra = counts + n;  // stage-2 row
+  dec.count_stride = 1;
+  dec.dim = (double)dim;
+
+  if (fast) {
+    // 2. strided encode pass x -> Y (signs, pad, bf16 upcast fused)
+    SrcEncode src;
+    memset(&src, 0, sizeof(src));
+    src.dtype = dtype_in;
+    src.L = L;
+    src.signs = signs;
+    src.signs_t = signs_t;
+    SnkBuf mid;
+    memset(&mid, 0, sizeof(mid));
+    mid.scale = 1.f;
+    for (int w = 0; w < n; ++w) {
+      src.x[w] = x[w];
+      mid.y[w] = Y + (size_t)w * dim;
+    }
+    if ((rc = launch_pass(OPTR_K_ENC_FIRST, fp.strided, nlog, 0, n, src, mid, st))) return rc;
+    // 3. contiguous encode pass of every worker + stage-1 mean -> A (natural order)
+    TmaArgs ta;
+    memset(&ta, 0, sizeof(ta));
+    ta.ntiles = fp.contig.ntiles;
+    for (int w = 0; w < n; ++w) ta.xw[w] = Y + (size_t)w * dim;
+    MeanArgs ma;
+    memset(&ma, 0, sizeof(ma));
+    ma.agg = A;
+    ma.scale = (float)(1.0 / sqrt((double)dim));
+    ma.n = n;
+    ma.r = r;
+    ma.shard_shift = log2_exact(sh.base);
+    ma.m = mv;
+    rc = fp.contig.ks == 13 ? launch_mean_t<13>(ta, ma, st) : launch_mean_t<14>(ta, ma, st);
+    if (rc) return rc;
+    // 4. contiguous decode pass with the stage-2 receive, A -> Y
+    for (int o = 0; o < n; ++o) ga.A[o] = A + sh.off(owned_shard(o, r, n));
+    SrcBuf buf;
+    memset(&buf, 0, sizeof(buf));
+    for (int w = 0; w < n; ++w) buf.y[w] = mid.y[w];
+    if ((rc = launch_pass(OPTR_K_DEC_FIRST, fp.contig, nlog, 0, n, ga, mid, st))) return rc;
+    // 5. strided decode pass Y -> out (count scale, signs, truncate, cast)
+    if ((rc = launch_pass(OPTR_K_DEC_LAST, fp.strided, nlog, 0, n, buf, dec, st))) return rc;
+    if (received_out) CK(cudaMemcpyAsync(received_out, counts, (size_t)2 * n * 8, cudaMemcpyDeviceToDevice, st));
+    return OPTR_OK;
+  }
+
+  // ---- general plan (RHT off, other sizes and shard splits)
   // 2. wire vectors
   const float* Yw[kMaxW];
   if (ht) {
@@ -1365,12 +1123,7 @@ int tar_local_impl(const void* const* x, void* const* out, int n, int64_t L, int
       Yw[w] = Y + (size_t)w * dim;
     }
     snk.scale = (float)(1.0 / sqrt((double)dim));
-    rc = try_chain(OPTR_K_ENC_CHAIN, log2_exact(dim), 0, n, src, buf, snk, chain_counters(set, st), st);
-    if (rc < 0)
-      rc = for_workers(dim, n, st, set, [&](int w0, int nw, cudaStream_t s2) {
-        return run_transform(log2_exact(dim), true, w0, nw, src, buf, snk, s2, OPTR_K_ENC_FIRST);
-      });
-    if (rc) return rc;
+    if ((rc = run_transform(nlog, true, 0, n, src, buf, snk, st, OPTR_K_ENC_FIRST))) return rc;
   } else {
     for (int w = 0; w < n; ++w) {
       if (dtype_in == OPTR_F32) {
@@ -1400,39 +1153,12 @@ int tar_local_impl(const void* const* x, void* const* out, int n, int64_t L, int
   if ((rc = launch_aggregate(ag, n, lay.smax, st))) return rc;
 
   // 4. stage 2 receive (+ decode)
-  SrcGather ga;
-  memset(&ga, 0, sizeof(ga));
   for (int w = 0; w < n; ++w) ga.A[w] = ag.A[w];
-  ga.sh = sh;
-  ga.n = n;
-  ga.r = r;
-  ga.m = mv;
-  ga.got = got_out;
-  ga.dim = dim;
-  ga.pow2_shift = (sh.extra == 0 && is_pow2(sh.base)) ? log2_exact(sh.base) : -1;
   if (ht) {
     SrcBuf buf;
     memset(&buf, 0, sizeof(buf));
-    SnkDecode snk;
-    memset(&snk, 0, sizeof(snk));
-    for (int w = 0; w < n; ++w) {
-      buf.y[w] = Y + (size_t)w * dim;  // encoded vectors are dead after stage 1
-      snk.out[w] = out[w];
-      snk.count_base[w] = sh.len(owned_shard(w, r, n));
-    }
-    snk.dtype = dtype_out;
-    snk.L = L;
-    snk.signs = signs;
-    snk.count_extra = counts + n;  // stage-2 row
-    snk.count_stride = 1;
-    snk.dim = (double)dim;
-    snk.signs_t = signs_t;
-    rc = try_chain(OPTR_K_DEC_CHAIN, log2_exact(dim), 0, n, ga, buf, snk, chain_counters(set, st), st);
-    if (rc < 0)
-      rc = for_workers(dim, n, st, set, [&](int w0, int nw, cudaStream_t s2) {
-        return run_transform(log2_exact(dim), dec_cf, w0, nw, ga, buf, snk, s2, OPTR_K_DEC_FIRST);
-      });
-    if (rc) return rc;
+    for (int w = 0; w < n; ++w) buf.y[w] = Y + (size_t)w * dim;  // encoded vectors are dead after stage 1
+    if ((rc = run_transform(nlog, dec_cf, 0, n, ga, buf, dec, st, OPTR_K_DEC_FIRST))) return rc;
   } else {
     AsmArgs as;
     memset(&as, 0, sizeof(as));
@@ -1464,8 +1190,8 @@ struct optr_comm_s {
   char* peer[OPTR_MAX_WORKERS];
   bool opened[OPTR_MAX_WORKERS];
   char* local;  // two parities of signs | bitmap | counts
-  size_t off_signs, off_signs_t, off_bitmap, off_counts, off_chain, local_bytes;  // within one parity
-  unsigned int* chain_ctr[2];  // chain / fused kernel counters of each parity (self-resetting)
+  size_t off_signs, off_signs_t, off_bitmap, off_counts, off_ctr, local_bytes;  // within one parity
+  unsigned int* fused_ctr[2];  // chain / fused kernel counters of each parity (self-resetting)
   unsigned int fepoch[2];      // fused-kernel tile-flag epochs of each parity
   cudaEvent_t fused_done[2];   // fused kernels of consecutive calls never overlap
   bool fused_recorded[2];
@@ -1527,8 +1253,8 @@ int optr_comm_create(optr_comm* out, int device, int rank, int n, int64_t max_le
   off = align_up(off + (size_t)2 * n * n * pw * 4, 256);
   c->off_counts = off;
   off = align_up(off + (size_t)2 * n * 8, 256);
-  c->off_chain = off;
-  off = align_up(off + kChainCtrWords * sizeof(unsigned int), 256);
+  c->off_ctr = off;
+  off = align_up(off + 4 * sizeof(unsigned int), 256);
   c->local_bytes = off;
   if (cudaMalloc((void**)&c->sym, c->sym_bytes) != cudaSuccess ||
       cudaMalloc((void**)&c->local, 2 * c->local_bytes) != cudaSuccess) {
@@ -1538,7 +1264,7 @@ int optr_comm_create(optr_comm* out, int device, int rank, int n, int64_t max_le
   }
   CK(cudaMemset(c->sym, 0, c->sym_bytes));
   CK(cudaMemset(c->local, 0, 2 * c->local_bytes));
-  for (int p = 0; p < 2; ++p) c->chain_ctr[p] = (unsigned int*)(c->local + p * c->local_bytes + c->off_chain);
+  for (int p = 0; p < 2; ++p) c->fused_ctr[p] = (unsigned int*)(c->local + p * c->local_bytes + c->off_ctr);
   // prep (ALU-heavy, off the critical path) at the lowest priority, the call
   // streams at the highest: the block scheduler gives prep leftover SMs
   int prio_lo = 0, prio_hi = 0;
@@ -1673,19 +1399,21 @@ namespace {
 void* g_fused_trace = nullptr;  // optr_debug_trace
 int g_fused_trace_cap = 0;
 // OPTR_FUSED=0 keeps the barrier-separated encode / aggregate / decode path.
+// Fused-kernel watchdog: a peer that never arrives traps the kernel after
+// OPTR_WATCHDOG_S seconds (default 1800 s, NCCL's default timeout).
+uint64_t watchdog_ns() {
+  static const uint64_t wd = [] {
+    const char* w = getenv("OPTR_WATCHDOG_S");
+    const double sec = (w && atof(w) > 0) ? atof(w) : 1800.0;
+    return (uint64_t)(sec * 1e9);
+  }();
+  return wd;
+}
+
 bool fused_enabled() {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("OPTR_FUSED");
-    v = (e && e[0] == '0') ? 0 : 1;
-  }
-  return v == 1;
-}
-
-bool prep_after_enc() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("OPTR_PREP_AFTER_ENC");
     v = (e && e[0] == '0') ? 0 : 1;
   }
   return v == 1;
@@ -1786,7 +1514,7 @@ static int tar_enqueue(optr_comm c, const void* x, void* out, int64_t L, int dty
   const int nlog = ht ? log2_exact(dim) : 0;
   const int np = ht ? plan_passes(nlog, fps, true) : 0;
   const int Tc = np == 2 ? fps[0].ks : 0;
-  const bool fused = ht && fused_enabled() && tma_enabled() && stage2_push() && np == 2 && fps[0].cb == 0 &&
+  const bool fused = ht && fused_enabled() && tma_enabled() && np == 2 && fps[0].cb == 0 &&
                      (Tc == 13 || Tc == 14) && fps[1].cb == 3 && (fps[1].ks + 3 == 13 || fps[1].ks + 3 == 14) &&
                      (n == 2 || n == 4 || n == 8) && sh.extra == 0 && (sh.base >> Tc) >= 1 &&
                      ((sh.base >> Tc) << Tc) == sh.base && (L >> fps[1].lo) >= 1;
@@ -1797,8 +1525,8 @@ static int tar_enqueue(optr_comm c, const void* x, void* out, int64_t L, int dty
   if (c->done_recorded[par]) CK(cudaStreamWaitEvent(ps, c->done[par], 0));
   // the host runs ahead: without this, this call's prep (ALU-heavy) would run
   // beside the previous call's HBM-bound strided encode instead of beside its
-  // NVLink-bound fused kernel (OPTR_PREP_AFTER_ENC=0 disables)
-  if (fused && prep_after_enc() && c->enc_recorded[par ^ 1]) CK(cudaStreamWaitEvent(ps, c->enc_done[par ^ 1], 0));
+  // NVLink-bound fused kernel
+  if (fused && c->enc_recorded[par ^ 1]) CK(cudaStreamWaitEvent(ps, c->enc_done[par ^ 1], 0));
 
   CK(cudaMemsetAsync(counts, 0, (size_t)2 * n * 8, ps));
   PrepArgs pa;
@@ -1873,7 +1601,7 @@ static int tar_enqueue(optr_comm c, const void* x, void* out, int64_t L, int dty
     }
     f.eflag_in = (const unsigned int*)(c->peer[me] + c->off_ef[par]);
     f.estride = c->max_dim >> 13;
-    f.ctr = c->chain_ctr[par];
+    f.ctr = c->fused_ctr[par];
     f.epoch = ++c->fepoch[par];
     f.n = n;
     f.me = me;
@@ -1884,19 +1612,7 @@ static int tar_enqueue(optr_comm c, const void* x, void* out, int64_t L, int dty
     f.m = mv;
     f.trace = (uint4*)g_fused_trace;
     f.trace_cap = g_fused_trace_cap;
-    {
-      static const int exp = [] {
-        const char* e = getenv("OPTR_FUSED_EXP");
-        return (e && e[0] == '1') ? 1 : 0;
-      }();
-      static const uint64_t wd = [] {
-        const char* w = getenv("OPTR_WATCHDOG_S");
-        const double sec = (w && atof(w) > 0) ? atof(w) : 1800.0;
-        return (uint64_t)(sec * 1e9);
-      }();
-      f.exp = exp;
-      f.watchdog_ns = wd;
-    }
+    f.watchdog_ns = watchdog_ns();
     if ((rc = launch_fused(Tc, ae, ad, se, sd, f, st))) return rc < 0 ? OPTR_ECUDA : rc;
     CK(cudaEventRecord(c->fused_done[par], st));
     c->fused_recorded[par] = true;
@@ -1942,8 +1658,7 @@ static int tar_enqueue(optr_comm c, const void* x, void* out, int64_t L, int dty
     memset(&snk, 0, sizeof(snk));
     snk.y[me] = Yp[me];
     snk.scale = (float)(1.0 / sqrt((double)dim));
-    rc = try_chain(OPTR_K_ENC_CHAIN, log2_exact(dim), me, 1, src, buf, snk, c->chain_ctr[par], st);
-    if (rc < 0) rc = run_transform(log2_exact(dim), true, me, 1, src, buf, snk, st, OPTR_K_ENC_FIRST);
+    rc = run_transform(log2_exact(dim), true, me, 1, src, buf, snk, st, OPTR_K_ENC_FIRST);
     if (rc) return rc;
   } else {
     KScope ks(OPTR_K_OTHER, st);
@@ -1967,7 +1682,7 @@ static int tar_enqueue(optr_comm c, const void* x, void* out, int64_t L, int dty
   // Stage 2 fused into stage 1 (push): the owner writes its mean chunk into
   // every rank's receive vector G while it pulls the next chunk, so the
   // decode reads stage-2 data locally.  Needs the TMA aggregate.
-  const bool push = stage2_push() && agg_vec_ok(ag) && tma_enabled();
+  const bool push = agg_vec_ok(ag) && tma_enabled();
   if (push) {
     for (int i = 0; i < n; ++i) ag.G[i] = Gp[i];
     ag.push = 1;
@@ -2002,10 +1717,7 @@ static int tar_enqueue(optr_comm c, const void* x, void* out, int64_t L, int dty
     snk.count_extra = counts + n;
     snk.count_stride = 1;
     snk.dim = (double)dim;
-    rc = decode_contig_first(true)
-             ? try_chain(OPTR_K_DEC_CHAIN, log2_exact(dim), me, 1, ga, buf, snk, c->chain_ctr[par], st)
-             : -1;
-    if (rc < 0) rc = run_transform(log2_exact(dim), decode_contig_first(true), me, 1, ga, buf, snk, st, OPTR_K_DEC_FIRST);
+    rc = run_transform(log2_exact(dim), true, me, 1, ga, buf, snk, st, OPTR_K_DEC_FIRST);
     if (rc) return rc;
   } else {
     AsmArgs as;

@@ -120,6 +120,24 @@ __device__ __forceinline__ uint32_t keep4(const uint32_t* row, uint32_t e, const
   return k;
 }
 
+// True when every packet covering shard entries [e0, e0 + len) is delivered
+// (uniform per tile: the per-entry mask work is skipped).
+__device__ __forceinline__ bool packets_all_kept(const uint32_t* row, uint32_t e0, uint32_t len, const MaskView& m) {
+  const uint32_t p0 = m.dv.div(e0), p1 = m.dv.div(e0 + len - 1);
+  for (uint32_t w = p0 >> 5; w <= (p1 >> 5); ++w) {
+    uint32_t need = 0xffffffffu;
+    if (w == (p0 >> 5)) need &= 0xffffffffu << (p0 & 31);
+    if (w == (p1 >> 5)) need &= 0xffffffffu >> (31 - (p1 & 31));
+    if ((__ldg(row + w) & need) != need) return false;
+  }
+  return true;
+}
+
+// keep-flag nibble -> one count byte per entry (entries 0..3 of a float4)
+__device__ __forceinline__ uint32_t nibble_bytes(uint32_t kk) {
+  return (kk & 1u) | ((kk & 2u) << 7) | ((kk & 4u) << 14) | ((kk & 8u) << 21);
+}
+
 // packet index of entries e..e+3 of a shard (epp = entries per packet)
 struct Pkt4 {
   uint32_t p[4];

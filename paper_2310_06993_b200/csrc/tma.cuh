@@ -19,8 +19,8 @@
 // masks) are applied when round A reads the tile, the decode epilogue
 // (count scale, signs, truncate, cast) when the last round writes it.
 //
-// Kernels: tma_pass_kernel (one pass, grid.y = worker), tma_chain_kernel
-// (opt-in: both passes of several workers, ticket queue), tma_agg_kernel
+// Kernels: tma_pass_kernel (one pass, grid.y = worker), tma_mean_kernel
+// (one GPU: last encode pass of every worker + TAR stage-1 mean), tma_agg_kernel
 // (TAR stage-1 mean, optional stage-2 push), tma_fused_kernel (multi-GPU:
 // contiguous encode + stage 1 + stage 2 + contiguous decode, per-tile flags
 // over NVLink).
@@ -219,6 +219,17 @@ __device__ __forceinline__ float4 gather_mask4(const TmaArgs& a, int q, uint8_t*
   return make_float4(k0 ? v.x : 0.f, k1 ? v.y : 0.f, k2 ? v.z : 0.f, k3 ? v.w : 0.f);
 }
 
+// Contiguous stage-2 tile t of receiver q lies in one shard: true when q owns
+// it or every packet of it arrived (no per-entry masks then).
+template <int T>
+__device__ __forceinline__ bool gather_tile_all_kept(const TmaArgs& a, int q, int64_t t) {
+  const int64_t g0 = t << T;
+  const int j = (int)(g0 >> a.shard_shift);
+  const int owner = shard_owner(j, a.r, a.n);
+  if (owner == q) return true;
+  return packets_all_kept(a.m.row(1, q, owner), (uint32_t)(g0 - ((int64_t)j << a.shard_shift)), 1u << T, a.m);
+}
+
 // CTA barrier (BAR = 0) or named barrier BAR over the first NT threads, for
 // kernels whose CTA holds several independent warp groups.
 template <int BAR, int NT>
@@ -235,10 +246,19 @@ __device__ __forceinline__ void group_sync() {
 // the next load: for a contiguous tile right after the tile has been read
 // (the results then leave by STG), for a strided tile after its TMA store
 // group is committed (the refill policy decides which stage to wait for).
-template <int T, bool STRIDED, int SK, class Snk, int CBW, int BAR = 0, int TID_OFF = 0, class Refill>
+// Contiguous passes hand their results to `epi(v, base)` when one is given
+// (v[4m..4m+3] are tile entries base + roff(make_rplan(T, 0), LR, 4m) + 0..3),
+// else store them through the sink.
+struct NoEpi {
+  __device__ __forceinline__ void operator()(const float (&)[32], int) const {}
+};
+
+template <int T, bool STRIDED, int SK, class Snk, int CBW, int BAR = 0, int TID_OFF = 0, class Refill,
+          class Epi = NoEpi>
 __device__ __forceinline__ void tma_tile(const TmaMaps* maps, const CUtensorMap* dst, const TmaArgs& a,
                                          const typename Snk::B& d, int worker, uint8_t* gotw, int64_t t,
-                                         unsigned char* sb, Refill&& refill) {
+                                         unsigned char* sb, Refill&& refill, Epi&& epi = Epi{},
+                                         bool all_kept = false) {
   constexpr int CB = STRIDED ? CBW : 0;  // untransformed column bits (8 or 32 columns)
   constexpr int CM = (1 << CB) - 1;
   constexpr RPlan P = make_rplan(T, CB);
@@ -318,7 +338,10 @@ __device__ __forceinline__ void tma_tile(const TmaMaps* maps, const CUtensorMap*
                        __int_as_float(__float_as_int(q4.w) ^ ((~sw & 8u) << 28)));
     } else {
       q4 = *reinterpret_cast<const float4*>(tile + i);
-      if constexpr (SK == TS_GATHER) q4 = gather_mask4(a, worker, gotw, g, q4);
+      if constexpr (SK == TS_GATHER) {
+        if (!all_kept) q4 = gather_mask4(a, worker, gotw, g, q4);
+        else if (gotw) *reinterpret_cast<uchar4*>(gotw + g) = make_uchar4(1, 1, 1, 1);
+      }
     }
     v[4 * m] = q4.x;
     v[4 * m + 1] = q4.y;
@@ -356,7 +379,10 @@ __device__ __forceinline__ void tma_tile(const TmaMaps* maps, const CUtensorMap*
     bfly32<P.xm[2]>(v);
   }
   group_sync<BAR, (1 << (T - 5))>();  // the padded tile has been read: the stage is free
-  if constexpr (!STRIDED) {
+  if constexpr (!STRIDED && !std::is_same<std::decay_t<Epi>, NoEpi>::value) {
+    if (tid == 0) refill();
+    epi(v, b2);
+  } else if constexpr (!STRIDED) {
     if (tid == 0) refill();
     if constexpr (P.pos[LR][0] == 0 && P.pos[LR][1] == 1) {
 #pragma unroll
@@ -480,6 +506,8 @@ __global__ void __launch_bounds__(1 << (T - 5)) tma_pass_kernel(const __grid_con
     const int s = k % kStages;
     unsigned char* const sb = base + s * SB;
     mbar_wait(&full[s], (uint32_t)((k / kStages) & 1));
+    bool all_kept = false;
+    if constexpr (SK == TS_GATHER && !STRIDED) all_kept = gather_tile_all_kept<T>(a, worker, t);
     tma_tile<T, STRIDED, SK, Snk, CBW>(&maps, &dst, a, d, worker, gotw, t, sb, [&]() {
       if constexpr (!STRIDED) {
         // contiguous: the stage was read; refill it while the results leave by STG
@@ -501,63 +529,39 @@ __global__ void __launch_bounds__(1 << (T - 5)) tma_pass_kernel(const __grid_con
   }
 }
 
-// ------------------------------------------------ persistent two-pass chain
-// Both passes of a two-pass transform (contiguous bits [0,T), then strided
-// bits [T,n) on 2^(T-CB) x 2^CB tiles: the same tile size) for several
-// workers in ONE persistent launch.  Tiles are handed out by a global ticket
-// counter in job order w0.p0, w1.p0, w0.p1, w2.p0, w1.p1, ..., so each
-// worker's intermediate is still L2-resident when its second pass reads it,
-// and no pass pays a launch ramp or a tail.  A pass-1 tile of worker w
-// depends on every pass-0 tile of w (per-worker completion counter).
-//
-// Thread 0 claims tickets in processing order (slot k % S holds position k;
-// a strided slot is refilled one tile late, once its store has read it).  A
-// pass-1 tile whose dependency is not met at claim time is deferred: its load
-// is issued when the CTA reaches it, after all of the CTA's earlier tiles
-// are finished and signalled, so waiting never blocks a tile it depends on.
-template <int T, int S>
-__host__ __device__ constexpr size_t tma_chain_smem_bytes() {
-  return S * tma_stage_bytes<T>() + 128 + 1024;  // ring, barriers + slot records, alignment
-}
-
-struct ChainSched {
-  unsigned int* ctr;  // [0] ticket, [1] CTAs done, [2 + w] pass-0 tiles done; zero on entry, reset by the last CTA
-  int nw;
-  int64_t nt0, nt1;  // tiles per worker of pass 0 / pass 1
-  int njobs;
-  int8_t jpass[2 * kMaxW];
-  int8_t jw[2 * kMaxW];
-  int64_t jstart[2 * kMaxW + 1];  // first ticket of each job; jstart[njobs] = total
+// ------------------------- last encode pass + TAR stage-1 mean (one GPU)
+// The contiguous (last) encode pass of every co-resident worker fused with
+// TAR stage 1 (collectives.py:113-125, _mean_received :77-94): a CTA takes
+// contiguous tile t of worker 0, 1, ..., n-1 in turn through its TMA ring,
+// transforms each and scales it by 1/sqrt(dim) in fp32 (the wire value,
+// runner.py:224), and accumulates it in fp64 in ascending worker order under
+// the stage-1 masks of the tile's owner (own tile always counted, misses
+// add 0.0).  After the last worker it writes the owner's mean of the tile
+// into the natural-order aggregate vector, so the n wire vectors are never
+// written to memory.  A tile lies in one shard (equal power-of-two shards of
+// >= 2^T entries); a peer whose packets over the tile all arrived skips the
+// per-entry masks.
+struct MeanArgs {
+  float* agg;   // [dim]: shard j's mean at j's natural offset
+  float scale;  // 1/sqrt(dim)
+  int n, r, shard_shift;
+  MaskView m;   // stage-1 rows (stage 0 of the bitmap layout)
 };
 
-__device__ __forceinline__ unsigned int ld_acquire_gpu(const unsigned int* p) {
-  unsigned int v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void fence_proxy_async_global() {
-  asm volatile("fence.proxy.async.global;" ::: "memory");
-}
-
-template <int T, int kStages, int SK0, class Snk1, int CBW>
-__global__ void __launch_bounds__(1 << (T - 5)) tma_chain_kernel(const __grid_constant__ TmaMaps maps1,
-                                                               const __grid_constant__ TmaMaps dmaps1,
-                                                               const __grid_constant__ TmaArgs a0,
-                                                               const __grid_constant__ TmaArgs a1,
-                                                               const __grid_constant__ SnkBuf snk0,
-                                                               const __grid_constant__ Snk1 snk1,
-                                                               const __grid_constant__ ChainSched cs) {
+template <int T, int kStages>
+__global__ void __launch_bounds__(1 << (T - 5)) tma_mean_kernel(const __grid_constant__ TmaArgs a,
+                                                              const __grid_constant__ MeanArgs ma) {
   constexpr size_t SB = tma_stage_bytes<T>();
+  constexpr RPlan P = make_rplan(T, 0);
+  constexpr int LR = P.nr - 1;
+  static_assert(P.pos[LR][0] == 0, "vector groups in the last round");
+  // the last round holds tile bits 0,1 (float4 groups, T = 13) or bit 0 (pairs, T = 14)
+  constexpr int VW = P.pos[LR][1] == 1 ? 4 : 2;
   extern __shared__ __align__(16) unsigned char smraw[];
   unsigned char* const base = smraw + ((1024u - (smem_u32(smraw) & 1023u)) & 1023u);
   uint64_t* const full = reinterpret_cast<uint64_t*>(base + kStages * SB);
-  int* const slot_job = reinterpret_cast<int*>(full + kStages);          // job of each slot, -1 = end
-  int64_t* const slot_tile = reinterpret_cast<int64_t*>(slot_job + 4);   // tile within the job
   const int tid = threadIdx.x;
-  unsigned int* const ticket = cs.ctr;
-  unsigned int* const done = cs.ctr + 2;
-  const int64_t total = cs.jstart[cs.njobs];
-
+  const int n = ma.n;
   if (tid == 0) {
     for (int s = 0; s < kStages; ++s) mbar_init(&full[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -565,99 +569,79 @@ __global__ void __launch_bounds__(1 << (T - 5)) tma_chain_kernel(const __grid_co
   __syncthreads();
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   asm volatile("griddepcontrol.wait;" ::: "memory");
-
-  // thread-0 state
-  bool ended = false;
-  int lag = -1;                  // strided slot whose refill is pending
-  unsigned deferred = 0;         // slots claimed but not yet issued (bit s)
-  auto do_issue = [&](int s) {
-    const int j = slot_job[s];
-    const int w = cs.jw[j];
-    const int64_t t = slot_tile[s];
-    if (cs.jpass[j] == 0) {
-      tile_issue<T, false, SK0, CBW>(maps1, a0, w, t, base + s * SB, &full[s]);
-    } else {
-      fence_proxy_async_global();  // pass-0 results (generic stores) before these TMA reads
-      tile_issue<T, true, TS_BUF, CBW>(maps1, a1, w, t, base + s * SB, &full[s]);
-    }
-  };
-  auto claim_issue = [&](int s) {
-    int j = -1;
-    int64_t t = 0;
-    if (!ended) {
-      const int64_t tk = atomicAdd(ticket, 1u);
-      if (tk >= total) {
-        ended = true;
-      } else {
-        j = 0;
-        while (tk >= cs.jstart[j + 1]) ++j;
-        t = tk - cs.jstart[j];
-      }
-    }
-    slot_job[s] = j;
-    slot_tile[s] = t;
-    if (j < 0) {
-      mbar_arrive(&full[s]);  // end marker: completes the phase with no data
-    } else if (cs.jpass[j] == 1 && ld_acquire_gpu(done + cs.jw[j]) < (unsigned)cs.nt0) {
-      deferred |= 1u << s;
-    } else {
-      do_issue(s);
-    }
+  const int64_t stride = gridDim.x;
+  // job k = (tile blockIdx.x + (k / n) * stride, worker k % n)
+  auto issue = [&](int64_t k, int s) {
+    const int64_t t = blockIdx.x + (k / n) * stride;
+    if (t < a.ntiles) tile_issue_contig<T, TS_BUF>(a, (int)(k % n), t, base + (size_t)s * SB, &full[s]);
   };
   if (tid == 0)
-    for (int s = 0; s < kStages; ++s) claim_issue(s);
-
-  for (int k = 0;; ++k) {
-    const int s = k % kStages;
-    unsigned char* const sb = base + s * SB;
-    if (tid == 0 && (deferred >> s & 1u)) {
-      const unsigned int* dw = done + cs.jw[slot_job[s]];
-      while (ld_acquire_gpu(dw) < (unsigned)cs.nt0) __nanosleep(64);
-      do_issue(s);
-      deferred &= ~(1u << s);
+    for (int s = 0; s < kStages; ++s) issue(s, s);
+  double acc[32];
+  uint32_t cnt[8];
+  uint32_t slow = 0;  // bit w: worker w's tile needs per-entry masks
+  int owner = 0;
+  uint32_t e0 = 0;    // tile offset inside its shard
+  const SnkBuf::B nosnk{nullptr, 1.f};
+  for (int64_t k = 0;; ++k) {
+    const int64_t t = blockIdx.x + (k / n) * stride;
+    if (t >= a.ntiles) break;
+    const int w = (int)(k % n);
+    const int s = (int)(k % kStages);
+    if (w == 0) {
+      const int64_t g0 = t << T;
+      const int j = (int)(g0 >> ma.shard_shift);
+      owner = shard_owner(j, ma.r, n);
+      e0 = (uint32_t)(g0 - ((int64_t)j << ma.shard_shift));
+      slow = 0;
+      for (int i = 0; i < n; ++i)
+        if (i != owner && !packets_all_kept(ma.m.row(0, owner, i), e0, 1u << T, ma.m)) slow |= 1u << i;
     }
     mbar_wait(&full[s], (uint32_t)((k / kStages) & 1));
-    const int j = slot_job[s];
-    if (j < 0) break;
-    const int w = cs.jw[j];
-    const int64_t t = slot_tile[s];  // read before tma_tile's first barrier; refills come after it
-    if (cs.jpass[j] == 0) {
-      uint8_t* const gotw = (SK0 == TS_GATHER && a0.got) ? a0.got + (int64_t)w * a0.dim : nullptr;
-      tma_tile<T, false, SK0, SnkBuf, CBW>(&maps1, &dmaps1.m[w], a0, snk0.bind(w), w, gotw, t, sb, [&]() {
-        if (lag >= 0) {
-          bulk_wait_read0();
-          claim_issue(lag);
-          lag = -1;
-        }
-        claim_issue(s);
-      });
-      __syncthreads();  // all results of the tile are stored
-      if (tid == 0) {
-        __threadfence();
-        fence_proxy_async_global();
-        atomicAdd(done + w, 1u);
-      }
-    } else {
-      tma_tile<T, true, TS_BUF, Snk1, CBW>(&maps1, &dmaps1.m[w], a1, snk1.bind(w), w, nullptr, t, sb, [&]() {
-        if (lag >= 0) {
-          bulk_wait_read1();  // the previous strided store has left its slot
-          claim_issue(lag);
-        }
-        lag = s;
-      });
-    }
+    tma_tile<T, false, TS_BUF, SnkBuf, 3>(
+        nullptr, nullptr, a, nosnk, w, nullptr, t, base + (size_t)s * SB, [&]() { issue(k + kStages, s); },
+        [&](const float (&v)[32], int b2) {
+          const bool masked = (slow >> w) & 1u;
+          // entry j = VW*q + c of this thread: count byte j%4 of cnt[j/4]
+#pragma unroll
+          for (int q = 0; q < 32 / VW; ++q) {
+            const uint32_t i = (uint32_t)(b2 + roff(P, LR, VW * q));
+            uint32_t kk = (1u << VW) - 1u;
+            if (masked) {
+              const uint32_t e = e0 + i;
+              kk = (keep4(ma.m.row(0, owner, w), e & ~3u, ma.m) >> (e & 3u)) & ((1u << VW) - 1u);
+            }
+#pragma unroll
+            for (int c = 0; c < VW; ++c) {
+              const double x = ((kk >> c) & 1u) ? (double)(v[VW * q + c] * ma.scale) : 0.0;
+              acc[VW * q + c] = (w == 0 ? 0.0 : acc[VW * q + c]) + x;
+            }
+            const int cw = (VW * q) / 4, sh = 8 * ((VW * q) % 4);
+            cnt[cw] = ((w == 0 && sh == 0) ? 0u : cnt[cw]) + (nibble_bytes(kk) << sh);
+          }
+          if (w == n - 1) {
+            float* const out = ma.agg + (t << T);
+#pragma unroll
+            for (int q = 0; q < 32 / VW; ++q) {
+              const int i = b2 + roff(P, LR, VW * q);
+              float r[VW];
+#pragma unroll
+              for (int c = 0; c < VW; ++c) {
+                const int j = VW * q + c;
+                r[c] = mean_of(acc[j], (double)((cnt[j / 4] >> (8 * (j % 4))) & 0xffu));
+              }
+              if constexpr (VW == 4)
+                st4(out + i, make_float4(r[0], r[1], r[2], r[3]));
+              else
+                *reinterpret_cast<float2*>(out + i) = make_float2(r[0], r[1]);
+            }
+          }
+        });
   }
-  if (tid == 0) {
-    bulk_wait0();
-    __threadfence();
-    const unsigned int prev = atomicAdd(cs.ctr + 1, 1u);
-    if (prev == gridDim.x - 1) {  // last CTA out: reset the counters for the next launch
-      cs.ctr[0] = 0;
-      cs.ctr[1] = 0;
-      for (int w = 0; w < cs.nw; ++w) done[w] = 0;
-      __threadfence();
-    }
-  }
+}
+
+__device__ __forceinline__ void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 
 }  // namespace optr
@@ -813,7 +797,6 @@ struct FusedArgs {
   MaskView m;
   uint4* trace;   // debug (optr_debug_trace): per CTA [cap/2 E/D jobs | cap/2 A tiles]
   int trace_cap;
-  int exp;        // experiment (OPTR_FUSED_EXP=1): E / D keep their flags and waits, skip the tiles
   uint64_t watchdog_ns;
 };
 
@@ -825,12 +808,14 @@ __device__ __forceinline__ unsigned int ld_acquire_sys(const unsigned int* p) {
 __device__ __forceinline__ void st_release_sys(unsigned int* p, unsigned int v) {
   asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
-// Flags of the fused kernel.  Every reader reaches the flagged data through
-// the writer GPU's L2 (its own HBM or NVLink peer requests), so a writer
-// needs its data visible at GPU scope (__threadfence after a group barrier,
-// cumulative) before a relaxed system-scope flag store; a reader polls with
-// relaxed loads and issues its (TMA) reads only after seeing the flag.
-// System-scope releases / fences here cost microseconds each under NVLink load.
+// Flags of the fused kernel (PTX memory model, fence-based synchronisation
+// at system scope, since writer and reader sit on different GPUs):
+//   writer: data stores by the group -> group barrier -> one thread:
+//           fence.acq_rel.sys (release, cumulative over the barrier) ->
+//           relaxed system-scope flag store / reduction;
+//   reader: relaxed system-scope polls -> fence.acq_rel.sys (acquire) ->
+//           fence.proxy.async -> TMA reads of the flagged data.
+__device__ __forceinline__ void fence_acq_rel_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
 __device__ __forceinline__ unsigned int ld_relaxed_sys(const unsigned int* p) {
   unsigned int v;
   asm volatile("ld.relaxed.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -932,7 +917,7 @@ __global__ void __launch_bounds__(NG * (1 << (T - 5)) + kAggThreads)
     int64_t pend_e = -1;  // thread 0: encoded tile whose eflag is not yet released
     auto release_e = [&]() {
       if (pend_e >= 0) {
-        __threadfence();  // cumulative over the group (its stores came before a group barrier)
+        fence_acq_rel_sys();  // release, cumulative over the group (its stores came before a group barrier)
         for (int q = 0; q < f.n; ++q) st_relaxed_sys(f.eflag_out[q] + pend_e, f.epoch);
         pend_e = -1;
       }
@@ -953,13 +938,13 @@ __global__ void __launch_bounds__(NG * (1 << (T - 5)) + kAggThreads)
       }
       gkind[s] = kind;
       gtile[s] = t;
-      if (kind == FJ_E && !f.exp) {
+      if (kind == FJ_E) {
         tile_issue_contig<T, TS_BUF>(ae, me, t, gbase + s * SB, &gfull[s]);
       } else if (kind == FJ_D) {
         if (ld_relaxed_sys(f.gflag[me] + t) >= (unsigned)UPT) {
+          fence_acq_rel_sys();  // acquire
           fence_proxy_async_global();
-          if (f.exp) mbar_arrive(&gfull[s]);
-          else tile_issue_contig<T, TS_GATHER>(ad, me, t, gbase + s * SB, &gfull[s]);
+          tile_issue_contig<T, TS_GATHER>(ad, me, t, gbase + s * SB, &gfull[s]);
         } else {
           deferred |= 1u << s;
         }
@@ -978,9 +963,9 @@ __global__ void __launch_bounds__(NG * (1 << (T - 5)) + kAggThreads)
         release_e();  // never wait while holding an unreleased encode
         const int64_t t = gtile[s];
         spin_ge_sys(f.gflag[me] + t, (unsigned)UPT, f.watchdog_ns);
+        fence_acq_rel_sys();  // acquire
         fence_proxy_async_global();
-        if (f.exp) mbar_arrive(&gfull[s]);
-        else tile_issue_contig<T, TS_GATHER>(ad, me, t, sb, &gfull[s]);
+        tile_issue_contig<T, TS_GATHER>(ad, me, t, sb, &gfull[s]);
         deferred &= ~(1u << s);
       }
       mbar_wait(&gfull[s], (uint32_t)((k / kStages) & 1));
@@ -996,14 +981,7 @@ __global__ void __launch_bounds__(NG * (1 << (T - 5)) + kAggThreads)
       // encode flag, which is released after this store)
       if (ltid == 0 && kind == FJ_D) st_relaxed_sys(f.gflag[me] + t, 0u);
       const uint32_t trd = tr && ltid == 0 ? (uint32_t)globaltimer_ns() : 0u;
-      if (f.exp && kind != FJ_NOP) {
-        group_sync<BARID, NED>();
-        if (ltid == 0) {
-          if (kind == FJ_E)
-            for (int q = 0; q < n; ++q) st_relaxed_sys(f.eflag_out[q] + t, f.epoch);
-          claim_issue(s);
-        }
-      } else if (kind == FJ_E) {
+      if (kind == FJ_E) {
         tma_tile<T, false, TS_BUF, SnkBuf, 3, BARID, G * NED>(nullptr, nullptr, ae, se.bind(me), me, nullptr, t, sb,
                                                  [&]() { claim_issue(s); });
         // released after the group's next job (or before any wait / exit), so
@@ -1015,7 +993,8 @@ __global__ void __launch_bounds__(NG * (1 << (T - 5)) + kAggThreads)
         }
       } else if (kind == FJ_D) {
         tma_tile<T, false, TS_GATHER, SnkBuf, 3, BARID, G * NED>(nullptr, nullptr, ad, sd.bind(me), me, nullptr, t, sb,
-                                                    [&]() { claim_issue(s); });
+                                                    [&]() { claim_issue(s); }, NoEpi{},
+                                                    gather_tile_all_kept<T>(ad, me, t));
       } else {
         // no-op ticket: every thread has read the slot (it is only rewritten
         // after this barrier)
@@ -1087,6 +1066,7 @@ __global__ void __launch_bounds__(NG * (1 << (T - 5)) + kAggThreads)
             return;
           }
           if (tra) t_ready = (uint32_t)globaltimer_ns();
+          fence_acq_rel_sys();  // acquire
           fence_proxy_async_global();
         }
       }
@@ -1107,6 +1087,7 @@ __global__ void __launch_bounds__(NG * (1 << (T - 5)) + kAggThreads)
         const int64_t t = (int64_t)f.own * ns + cur / UPT;
         for (int q = 0; q < n; ++q) spin_ge_sys(f.eflag_in + q * f.estride + t, f.epoch, f.watchdog_ns);
         if (tra) t_ready = (uint32_t)globaltimer_ns();
+        fence_acq_rel_sys();  // acquire
         fence_proxy_async_global();
         const int first = pend_first, cnt = pend_count;
         pend_first = -1;
@@ -1146,7 +1127,7 @@ __global__ void __launch_bounds__(NG * (1 << (T - 5)) + kAggThreads)
       group_sync<2, kAggThreads>();  // stage s consumed (and the unit's results stored, when last)
       if (ta == 0) {
         if (last) {
-          __threadfence();  // cumulative: the group's results are in my L2 before the counts
+          fence_acq_rel_sys();  // release: the group's results before the counts
           const int64_t t = (int64_t)f.own * ns + un / UPT;
           for (int q = 0; q < n; ++q) red_add_relaxed_sys(f.gflag[q] + t, 1u);
           if (tra && ntr < f.trace_cap / 2)

@@ -13,9 +13,12 @@ calls ``TarCommunicator.allreduce`` with its own bucket:
 * stage 2, fused into the same kernel: the owner pushes its aggregate into
   every peer's symmetric gather buffer over NVLink (collectives.py:127-150);
 * device barrier; masked decode from the local gather buffer
-  (runner.py:248-256).  (``OPTR_STAGE2=pull`` selects the older variant:
-  a second barrier, then every rank pulls the owners' aggregates inside the
-  first decode pass.)
+  (runner.py:248-256).
+
+That is the barrier path (other sizes).  For D = 2^23..2^25 and n in
+{2, 4, 8} the encode's contiguous pass, both stages and the decode's
+contiguous pass run in one persistent kernel with per-tile flags over NVLink
+(DESIGN.md §5).
 
 torch.distributed (NCCL) only carries the one-time IPC handle exchange and
 host barriers; the data path is peer loads inside the kernels.
@@ -115,15 +118,27 @@ class TarCommunicator:
         check(lib().optr_comm_join(self._h, st.cuda_stream), "comm_join")
 
     def close(self):
+        """Collective: every rank must call it.  No rank unmaps or frees its
+        symmetric buffer while a peer's kernels may still read it or store
+        flags into it (local drain, then an all-rank barrier)."""
         if self._h is not None:
             import torch
+            import torch.distributed as dist
 
             torch.cuda.synchronize(self.device)
+            if dist.is_initialized():
+                dist.barrier(self.group)
             lib().optr_comm_destroy(self._h)
             self._h = None
 
     def __del__(self):
+        # no collective barrier from a finaliser: only drain locally
         try:
-            self.close()
+            if self._h is not None:
+                import torch
+
+                torch.cuda.synchronize(self.device)
+                lib().optr_comm_destroy(self._h)
+                self._h = None
         except Exception:
             pass

@@ -21,6 +21,11 @@ reference itself produces on fixed seeds:
                       captured at consumption time (SURVEY finding 2/5) and
                       stored per packet, next to the reference results
                       (runner.py:211-276).
+* ``sim_gpt2xl.npz`` -- the same capture at the GPT-2 XL bucket shape
+                      (BASELINE configs[3]: n=8, 13,107,200 entries, bf16-valued
+                      inputs, 5% drops, adaptive timeouts): packed packet masks
+                      plus per-node checksums and sampled entries of the
+                      reference's results (the full outputs are 420 MB).
 
 Nothing here runs on the GPU box; the .npz files travel instead.
 """
@@ -302,8 +307,55 @@ def gen_sim():
                         gens=np.array([c[6] for c in configs]), **rec)
 
 
+def bf16_round(x: np.ndarray) -> np.ndarray:
+    """float32 -> nearest bfloat16 (ties to even), kept as float32 (torch's
+    .to(torch.bfloat16) on finite values)."""
+    u = np.ascontiguousarray(x, dtype=np.float32).view(np.uint32).astype(np.uint64)
+    u = (u + 0x7FFF + ((u >> 16) & 1)) & 0xFFFF0000
+    return u.astype(np.uint32).view(np.float32)
+
+
+def gen_sim_large():
+    n, L, p, ratio, dist, seed = 8, 13_107_200, 0.05, 3.0, "lognormal", 5
+    cfg = ExperimentConfig(n=n, bucket_len=L, ht="on", drop_prob=p, p99_over_p50=ratio,
+                           latency_distribution=dist, seed=seed, calibration_iterations=3)
+    session = build_session(cfg)
+    brng = _bucket_rng(cfg)
+    epp = cfg.max_payload // 4
+    buckets = [bf16_round(brng.standard_normal(L).astype(np.float32)) for _ in range(n)]
+    log, orig = _capture_stage1()
+    try:
+        r = session.rotation
+        gen_idx = session.generation
+        report = session.run_generation(buckets)
+    finally:
+        ucoll._mean_received = orig
+    dim = len(report.stats[0].result.entries)
+    offs = shard_offsets(dim, n)
+    log = log[-n:]
+    rec = {}
+    for rank, masks in log:
+        for src, m in masks.items():
+            rec[f"m1_{rank}_{src}"] = np.packbits(_to_packets(m, epp), bitorder="little")
+    for dst, st in enumerate(report.stats):
+        got = np.asarray(st.result.received)
+        for src in range(n):
+            if src != dst:
+                j = owned_shard(src, r, n)
+                rec[f"m2_{dst}_{src}"] = np.packbits(_to_packets(got[offs[j]:offs[j + 1]], epp), bitorder="little")
+    outs = np.stack([np.asarray(x, dtype=np.float32) for x in report.results])
+    idx = np.random.default_rng(0).choice(L, 4096, replace=False)
+    rec["sample_idx"] = idx
+    rec["sample_out"] = outs[:, idx]
+    rec["out_sum"] = outs.astype(np.float64).sum(axis=1)
+    rec["out_norm"] = np.linalg.norm(outs.astype(np.float64), axis=1)
+    rec["meta"] = np.array([n, L, int(report.ht_used), r, gen_idx, seed, epp, dim])
+    rec["loss"] = np.array([s.loss_rate for s in report.stats])
+    np.savez_compressed(OUT / "sim_gpt2xl.npz", **rec)
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["rng", "codec", "lossless", "datagram", "sim"]
+    which = sys.argv[1:] or ["rng", "codec", "lossless", "datagram", "sim", "sim_large"]
     for w in which:
         globals()[f"gen_{w}"]()
         print("wrote", w)

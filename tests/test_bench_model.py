@@ -30,12 +30,12 @@ def test_step_alg_bytes_rht_off_and_bf16():
 
 def test_kernel_bytes_classes():
     dim, L, n = 1 << 23, 6_553_600, 4
-    for cls in ("enc_first", "enc_last", "aggregate", "dec_first", "dec_last", "enc_chain", "dec_chain", "fused",
-                "prep"):
+    for cls in ("enc_first", "enc_last", "enc_mean", "aggregate", "dec_first", "dec_last", "fused", "prep"):
         assert bench.kernel_bytes(cls, dim, L, n, 4, 4) > 0
-    # the chains count the minimum (no intermediate round trip)
-    assert bench.kernel_bytes("enc_chain", dim, L, n, 4, 4) < (bench.kernel_bytes("enc_first", dim, L, n, 4, 4)
-                                                                + bench.kernel_bytes("enc_last", dim, L, n, 4, 4))
+    # the fused last-pass + stage-1 mean reads the wire once and writes one
+    # shard's mean per worker: less than the last pass plus the aggregate
+    assert bench.kernel_bytes("enc_mean", dim, L, n, 4, 4) < (bench.kernel_bytes("enc_last", dim, L, n, 4, 4)
+                                                               + bench.kernel_bytes("aggregate", dim, L, n, 4, 4))
 
 
 def test_ddp_hook_host_logic():

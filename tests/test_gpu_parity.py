@@ -315,41 +315,11 @@ def test_async_local_two_in_flight_matches_sync(dev):
             assert torch.equal(outs[g][w], want[g][w])
 
 
-# ------------------------------------------------ persistent chain kernel
-@pytest.mark.parametrize("n,L,dtype", [(4, 5_000_000, "f32"), (3, 4_500_000, "f32"), (2, 25_000_000, "bf16"),
-                                       (8, 7_000_000, "f32")])
-def test_chain_matches_pass_launches(dev, n, L, dtype, tmp_path):
-    """The two-pass chain kernel (one persistent launch for both passes of
-    every worker, D = 2^23 / 2^25) is bit-identical to the separate pass
-    launches in the same order (subprocess, OPTR_CHAIN=0 and contiguous-first
-    decode), masks and received flags included."""
-    import os
-    import subprocess
-    import sys
-
-    import chain_case
-
-    here = os.path.dirname(os.path.abspath(__file__))
-    z = {}
-    for chain in ("1", "0"):
-        path = str(tmp_path / f"c{chain}.npz")
-        env = dict(os.environ, OPTR_CHAIN=chain, OPTR_DEC_ORDER="contig")
-        env["PYTHONPATH"] = os.pathsep.join([os.path.dirname(here), here, env.get("PYTHONPATH", "")])
-        subprocess.run([sys.executable, os.path.join(here, "chain_case.py"), str(n), str(L), dtype, "1", path],
-                       check=True, env=env, timeout=600)
-        z[chain] = np.load(path)
-    for k in ("counts", "got", "res"):
-        np.testing.assert_array_equal(z["1"][k], z["0"][k])
-    # and the default path (strided-first local decode) agrees within the codec error
-    res, counts, got, _ = chain_case.run(n, L, dtype, seed=1)
-    np.testing.assert_array_equal(counts, z["1"]["counts"])
-    np.testing.assert_array_equal(got, z["1"]["got"])
-    assert rel_err(res, z["1"]["res"]) < (REL if dtype == "f32" else 1e-2)  # bf16 output rounding
-
-
-def test_chain_vs_oracle_d23(dev):
-    """Default pass path (n=4, D=2^23, datagram coin) against the oracle; the
-    chain kernel is pinned to it bit-exactly by the test above."""
+# ------------------------------------------------ one-GPU fast plan
+def test_fast_plan_vs_oracle_d23(dev):
+    """One-GPU fast plan (strided encode, encode+stage-1 mean kernel, gather
+    decode, strided decode; n=4, D=2^23, datagram coin) against the oracle,
+    received flags bit-exact."""
     n, L, p, gen = 4, 4_500_001, 0.01, 3
     seed, coin_seed = 21, 555
     r = gen % n
@@ -361,65 +331,6 @@ def test_chain_vs_oracle_d23(dev):
     for node in range(n):
         assert rel_err(outs[node], want[node]) < REL, node
         np.testing.assert_array_equal(got[node].astype(bool), tar[node][1])
-
-
-@pytest.mark.parametrize("logd,L,dtype", [(23, 5_000_001, "f32"), (25, 25_000_000, "bf16"), (24, 16_000_000, "f32")])
-def test_strided_first_encode_matches(dev, logd, L, dtype, tmp_path):
-    """The fused multi-GPU path's encode order (strided pass first, transposed
-    sign bytes, x read by TMA boxes) equals the default encode within the
-    float32 codec tolerance (subprocess: OPTR_ENC_ORDER is read once)."""
-    import os
-    import subprocess
-    import sys
-
-    code = (
-        "import sys, numpy as np, torch; sys.path.insert(0, %r);"
-        "import paper_2310_06993_b200 as P;"
-        "g = torch.Generator(device='cuda').manual_seed(5);"
-        "x = torch.randn(%d, device='cuda', generator=g).to(%s);"
-        "ctx = P.RhtContext.for_length(%d, 777);"
-        "np.save(%r, P.rht_encode(x, ctx).cpu().numpy())"
-    )
-    here = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    dt = "torch.float32" if dtype == "f32" else "torch.bfloat16"
-    outs = {}
-    for order in ("contig", "strided"):
-        path = str(tmp_path / f"{order}.npy")
-        env = dict(os.environ, OPTR_ENC_ORDER=order)
-        subprocess.run([sys.executable, "-c", code % (here, L, dt, L, path)], check=True, env=env, timeout=300)
-        outs[order] = np.load(path)
-    assert outs["contig"].shape == (1 << logd,)
-    assert rel_err(outs["strided"], outs["contig"]) < REL
-
-
-def test_three_pass_wide_rows_match(dev, tmp_path):
-    """D = 2^26 (three-pass plan): 32-column strided tiles (default) against
-    the 8-column plan (OPTR_WIDE3=0), same masks: counts / received flags
-    bit-exact, results within the float32 codec tolerance; and the lossless
-    result is the exact mean."""
-    import os
-    import subprocess
-    import sys
-
-    here = os.path.dirname(os.path.abspath(__file__))
-    z = {}
-    for wide in ("1", "0"):
-        path = str(tmp_path / f"w{wide}.npz")
-        env = dict(os.environ, OPTR_WIDE3=wide)
-        env["PYTHONPATH"] = os.pathsep.join([os.path.dirname(here), here, env.get("PYTHONPATH", "")])
-        subprocess.run([sys.executable, os.path.join(here, "chain_case.py"), "2", "40000000", "f32", "2", path],
-                       check=True, env=env, timeout=600)
-        z[wide] = np.load(path)
-    np.testing.assert_array_equal(z["1"]["counts"], z["0"]["counts"])
-    np.testing.assert_array_equal(z["1"]["got"], z["0"]["got"])
-    assert rel_err(z["1"]["res"], z["0"]["res"]) < REL
-    n, L = 2, 40_000_000
-    g = torch.Generator(device=dev).manual_seed(3)
-    xs = [torch.randn(L, device=dev, generator=g) for _ in range(n)]
-    mean = (xs[0].double() + xs[1].double()) / 2
-    outs, _, _ = tar_allreduce_local(xs, rotation=0, ht=True, job_seed=1, generation=0, masks=MaskSpec.none())
-    for o in outs:
-        assert ((o.double() - mean).norm() / mean.norm()).item() < REL
 
 
 def test_tar_allreduce_reference_signature(dev):

@@ -18,12 +18,23 @@ import oracle as O
 torch = pytest.importorskip("torch")
 
 
-def _world():
-    """Ranks for the multi-GPU tests: one per GPU (<= 8), or OPTR_TEST_WORLD
-    ranks round-robin over the GPUs (e.g. 8 ranks on 4 GPUs, with
-    OPTR_FUSED_GRID capping each persistent grid so two fit on a GPU)."""
+def _worlds():
+    """Rank counts for the multi-process tests.  One rank per GPU when the box
+    has >= 2 GPUs; on a one-GPU box the ranks are oversubscribed onto GPU 0
+    (n = 2 and n = 4 processes, each with its own context: the GPU time-slices
+    them, gloo carries the one-time handle exchange), so the driver's
+    one-GPU test run still executes the multi-GPU kernels -- the fused
+    per-tile-flag kernel included -- instead of skipping them.
+    OPTR_TEST_WORLD overrides (e.g. 8 ranks on 4 GPUs)."""
     env = os.environ.get("OPTR_TEST_WORLD")
-    return int(env) if env else min(torch.cuda.device_count(), 8)
+    if env:
+        return [int(env)]
+    nd = torch.cuda.device_count()
+    return [min(nd, 8)] if nd >= 2 else [2, 4]
+
+
+def _world():
+    return _worlds()[0]
 
 
 def _dev(rank):
@@ -33,14 +44,21 @@ def _dev(rank):
 def _init(rank, world, dev):
     """NCCL with one rank per GPU; gloo (host-side handle exchange only) when
     ranks share GPUs, which NCCL refuses.  A protocol deadlock in the fused
-    kernel should fail the test in seconds, not hang it (watchdog)."""
+    kernel should fail the test in seconds, not hang it (watchdog; longer
+    when the ranks time-slice one GPU)."""
     import torch.distributed as dist
 
-    os.environ.setdefault("OPTR_WATCHDOG_S", "30")
-    if world > torch.cuda.device_count():
+    shared = world > torch.cuda.device_count()
+    os.environ.setdefault("OPTR_WATCHDOG_S", "120" if shared else "30")
+    if shared:
         dist.init_process_group("gloo", rank=rank, world_size=world)
     else:
         dist.init_process_group("nccl", rank=rank, world_size=world, device_id=dev)
+
+
+def _need_gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
 
 
 def _free_port():
@@ -89,17 +107,21 @@ def test_handle_exchange_gloo_world2():
 
 # ------------------------------------------------------------ multi-GPU
 CASES = [
-    # L, p, gen, ht, dtype
-    (1 << 16, 0.05, 3, True, "f32"),
-    (100_000, 0.01, 5, True, "f32"),
-    (25_000_000, 0.01, 1, True, "f32"),
-    (12_345, 0.05, 2, False, "f32"),
-    (1 << 20, 0.02, 4, True, "bf16"),
-    # fused multi-GPU kernel (D = 2^23, 2^25): against the oracle / exact mean
-    (5_000_000, 0.02, 6, True, "f32"),
-    (4_200_000, 0.01, 7, True, "bf16"),
-    (25_000_000, 0.0, 2, True, "f32"),
+    # L, p, gen, ht, dtype, max world (the oracle's cost bounds the big cases)
+    (1 << 16, 0.05, 3, True, "f32", 8),
+    (1_048_576, 0.01, 2, True, "f32", 8),     # BASELINE configs[0] shape (1M entries, 1%)
+    (12_345, 0.05, 2, False, "f32", 8),       # RHT off: bit-exact
+    (1 << 20, 0.02, 4, True, "bf16", 8),
+    (5_000_000, 0.02, 6, True, "f32", 8),     # fused kernel, D = 2^23
+    (4_200_000, 0.01, 7, True, "bf16", 8),    # fused kernel, bf16 in
+    (25_000_000, 0.01, 1, True, "f32", 4),    # north-star headline bucket, 1% drops
+    (25_000_000, 0.0, 2, True, "f32", 8),     # headline, lossless
+    (40_000_000, 0.01, 3, True, "f32", 2),    # D = 2^26 (three-pass plan), 1% drops
 ]
+
+
+def _cases(world):
+    return [(ci, c) for ci, c in enumerate(CASES) if world <= c[5]]
 
 
 def _gpu_worker(rank, world, port, outdir):
@@ -113,10 +135,12 @@ def _gpu_worker(rank, world, port, outdir):
     torch.cuda.set_device(_dev(rank))
     dev = torch.device("cuda", _dev(rank))
     _init(rank, world, dev)
-    comm = TarCommunicator(max_len=max(c[0] for c in CASES))
-    for ci, (L, p, gen, ht, dt) in enumerate(CASES):
+    cases = _cases(world)
+    comm = TarCommunicator(max_len=max(c[0] for _, c in cases))
+    for ci, (L, p, gen, ht, dt, _mw) in cases:
         buckets = O.make_buckets(100 + ci, world, L)
         x = torch.from_numpy(buckets[rank]).to(dev)
+        del buckets
         if dt == "bf16":
             x = x.to(torch.bfloat16)
         out = torch.empty(L, dtype=torch.float32, device=dev)
@@ -132,54 +156,51 @@ def _gpu_worker(rank, world, port, outdir):
                            masks=MaskSpec.coin(700 + ci, p))
             torch.cuda.synchronize()
             np.save(os.path.join(outdir, f"c{ci}_r{rank}_bf16.npy"), out16.float().cpu().numpy())
+        del x, out
     comm.close()
     dist.destroy_process_group()
 
 
 @pytest.mark.gpu
-@pytest.mark.multigpu
-def test_tar_rht_multi_gpu_vs_oracle():
+@pytest.mark.parametrize("world", _worlds() if torch.cuda.is_available() else [2])
+def test_tar_rht_multi_rank_vs_oracle(world):
+    """One worker per rank (TarCommunicator: fused per-tile-flag kernel for
+    D = 2^23..2^25, barrier path otherwise) against the oracle's n-worker
+    generation under the same coin masks, per element: RHT on within 1e-5
+    relative L2 per node (the 25M-entry headline with 1% drops included),
+    RHT off bit-exact, received counts bit-exact."""
     import torch.multiprocessing as mp
 
-    if not torch.cuda.is_available() or torch.cuda.device_count() < 2:
-        pytest.skip("needs >= 2 GPUs")
-    world = _world()
+    _need_gpu()
     with tempfile.TemporaryDirectory() as d:
         mp.spawn(_gpu_worker, args=(world, _free_port(), d), nprocs=world, join=True)
-        for ci, (L, p, gen, ht, dt) in enumerate(CASES):
+        for ci, (L, p, gen, ht, dt, _mw) in _cases(world):
             buckets = O.make_buckets(100 + ci, world, L)
             if dt == "bf16":
                 buckets = [torch.from_numpy(b).to(torch.bfloat16).float().numpy() for b in buckets]
             r = gen % world
             dim = O.next_pow2(L) if ht else L
             masks = O.datagram_masks(700 + ci, dim, world, r, p)
-            if L > 5_000_000:
-                # size-independent checks at the headline size: counts bit-exact,
-                # lossless-ish agreement with the exact mean bounded by the loss
-                mean = O.oracle_allreduce(buckets)
-                sc = O.stage_counts(masks, dim, world, r, 350)
-                for rank in range(world):
-                    out = np.load(os.path.join(d, f"c{ci}_r{rank}.npy")).astype(np.float64)
-                    rec = np.load(os.path.join(d, f"c{ci}_r{rank}_rec.npy"))
-                    assert rec[0] == sc[(1, rank)][0] and rec[1] == sc[(2, rank)][0]
-                    rel = np.linalg.norm(out - mean) / np.linalg.norm(mean)
-                    assert rel < (1e-5 if p == 0 else 0.3), (ci, rank, rel)
-                continue
-            want = O.run_generation(buckets, 9, gen, ht, masks=masks, r=r)
+            sc = O.stage_counts(masks, dim, world, r, 350)
+            want = O.run_generation(buckets, 9, gen, ht, masks=masks, r=r, threads=world)
+            del buckets
             for rank in range(world):
+                rec = np.load(os.path.join(d, f"c{ci}_r{rank}_rec.npy"))
+                assert rec[0] == sc[(1, rank)][0] and rec[1] == sc[(2, rank)][0], (ci, rank)
+                out = np.load(os.path.join(d, f"c{ci}_r{rank}.npy"))
                 if dt == "bf16":
                     o16 = np.load(os.path.join(d, f"c{ci}_r{rank}_bf16.npy")).astype(np.float64)
                     assert np.linalg.norm(o16 - want[rank]) / np.linalg.norm(want[rank]) < 1e-2, (ci, rank)
-                out = np.load(os.path.join(d, f"c{ci}_r{rank}.npy"))
                 if ht:
                     rel = np.linalg.norm(out.astype(np.float64) - want[rank]) / np.linalg.norm(want[rank])
                     assert rel < 1e-5, (ci, rank, rel)
                 else:
                     np.testing.assert_array_equal(out, want[rank])
+            del want
 
 
 # ------------------------------------------------------------ DDP hook
-def _ddp_worker(rank, world, port, outdir):
+def _ddp_worker(rank, world, port, outdir, big):
     import torch.distributed as dist
     import torch.nn as nn
     from torch.nn.parallel import DistributedDataParallel as DDP
@@ -190,10 +211,10 @@ def _ddp_worker(rank, world, port, outdir):
     os.environ["MASTER_PORT"] = str(port)
     torch.cuda.set_device(_dev(rank))
     dev = torch.device("cuda", _dev(rank))
-    dist.init_process_group("nccl", rank=rank, world_size=world, device_id=dev)
+    _init(rank, world, dev)
     grads = {}
-    big = os.environ.get("OPTR_TEST_DDP_BIG") == "1"
-    for mode in ("nccl", "overlap", "ordered"):
+    captured = []  # lossy mode: (generation, bucket index, input, output) per hook call
+    for mode in ("default", "overlap", "ordered", "lossy"):
         torch.manual_seed(0)
         if big:  # one 6.55M-entry bucket (D = 2^23): the fused multi-GPU kernel
             model = nn.Sequential(nn.Linear(512, 2560, bias=False), nn.ReLU(), nn.Linear(2560, 2560),
@@ -201,11 +222,19 @@ def _ddp_worker(rank, world, port, outdir):
         else:
             model = nn.Sequential(nn.Linear(512, 1024), nn.ReLU(), nn.Linear(1024, 700), nn.ReLU(),
                                   nn.Linear(700, 10)).to(dev)
-        ddp = DDP(model, device_ids=[rank], bucket_cap_mb=25 if big else 1)
-        if mode != "nccl":
+        ddp = DDP(model, device_ids=[dev.index], bucket_cap_mb=25 if big else 1)
+        if mode != "default":
             state = OptiReduceState(max_bucket_len=max_bucket_len_for(model, 1), ht=True, seed=3,
-                                    overlap=(mode == "overlap"))
-            ddp.register_comm_hook(state, optireduce_hook)
+                                    overlap=(mode != "ordered"), drop_prob=0.02 if mode == "lossy" else 0.0)
+            if mode == "lossy":
+                def hook(st, bucket):
+                    g, inp = st.generation, bucket.buffer().clone()
+                    fut = optireduce_hook(st, bucket)
+                    captured.append((g, bucket.index(), inp, fut.value()))
+                    return fut
+                ddp.register_comm_hook(state, hook)
+            else:
+                ddp.register_comm_hook(state, optireduce_hook)
         g = torch.Generator(device=dev).manual_seed(100 + rank)
         for _step in range(2):  # second pass reuses the buffers at the next generation
             model.zero_grad(set_to_none=True)
@@ -214,43 +243,73 @@ def _ddp_worker(rank, world, port, outdir):
             loss.backward()
         torch.cuda.synchronize()
         grads[mode] = torch.cat([p.grad.flatten() for p in model.parameters()]).cpu().numpy()
-        if mode != "nccl":
+        if mode != "default":
             assert state.generation == 2
-            assert len(state.received) >= 2 and not state._pending
+            assert len(state.received) >= 1 and not state._pending
             state.comm.close()
-    np.save(os.path.join(outdir, f"ddp_r{rank}.npy"), np.stack([grads["nccl"], grads["overlap"], grads["ordered"]]))
+    np.save(os.path.join(outdir, f"ddp_r{rank}.npy"), np.stack([grads[m] for m in ("default", "overlap", "ordered")]))
+    for k, (gen, b, inp, out) in enumerate(captured):
+        np.save(os.path.join(outdir, f"lossy_r{rank}_{k}.npy"),
+                np.stack([inp.float().cpu().numpy(), out.float().cpu().numpy()]))
+        np.save(os.path.join(outdir, f"lossy_r{rank}_{k}_meta.npy"), np.array([gen, b]))
     dist.destroy_process_group()
 
 
 @pytest.mark.gpu
-@pytest.mark.multigpu
 @pytest.mark.parametrize("big", [False, True])
-def test_ddp_comm_hook_lossless_matches_mean(big, monkeypatch):
-    """Lossless TAR+RHT through the DDP hook == DDP's own mean all-reduce
-    within the float32 codec error (small buckets: the barrier path; one
-    25 MB-class bucket: the fused kernel)."""
+def test_ddp_comm_hook_vs_mean_and_oracle(big):
+    """Through DDP's register_comm_hook: lossless TAR+RHT == DDP's own mean
+    all-reduce within the float32 codec error (overlapped and ordered buckets
+    bit-identical); with 2% seeded coin drops every bucket of every rank
+    equals the oracle's lossy generation on the ranks' captured buckets
+    (codec seed derive_seed(seed, bucket index, generation), rotation
+    generation % n) within 1e-5.  Small buckets take the barrier path, one
+    25 MB-class bucket the fused kernel."""
     import torch.multiprocessing as mp
 
-    monkeypatch.setenv("OPTR_TEST_DDP_BIG", "1" if big else "0")
+    from paper_2310_06993_b200.ddp_hook import _COIN_TAG
 
-    if not torch.cuda.is_available() or torch.cuda.device_count() < 2:
-        pytest.skip("needs >= 2 GPUs")
+    _need_gpu()
     world = _world()
-    if world > torch.cuda.device_count():
-        pytest.skip("DDP over NCCL needs one rank per GPU")
     with tempfile.TemporaryDirectory() as d:
-        mp.spawn(_ddp_worker, args=(world, _free_port(), d), nprocs=world, join=True)
+        mp.spawn(_ddp_worker, args=(world, _free_port(), d, big), nprocs=world, join=True)
         for r in range(world):
             ref, ovl, ordered = np.load(os.path.join(d, f"ddp_r{r}.npy"))
             for got in (ovl, ordered):
                 rel = np.linalg.norm(got.astype(np.float64) - ref) / np.linalg.norm(ref)
                 assert rel < 1e-5, rel
             np.testing.assert_array_equal(ovl, ordered)  # same kernels, same order of arithmetic
+        k = 0
+        while os.path.exists(os.path.join(d, f"lossy_r0_{k}.npy")):
+            gen, b = (int(v) for v in np.load(os.path.join(d, f"lossy_r0_{k}_meta.npy")))
+            io = [np.load(os.path.join(d, f"lossy_r{r}_{k}.npy")) for r in range(world)]
+            L = io[0].shape[1]
+            dim = O.next_pow2(L)
+            p = 0.02
+            masks = O.datagram_masks(O.derive_seed(3 ^ _COIN_TAG, b, gen), dim, world, gen % world, p)
+            want = O.run_generation([x[0] for x in io], 3, gen, True, masks=masks, r=gen % world,
+                                    bucket_id=b, threads=world)
+            for r in range(world):
+                rel = np.linalg.norm(io[r][1].astype(np.float64) - want[r]) / np.linalg.norm(want[r])
+                assert rel < 1e-5, (k, r, rel)
+            k += 1
+        assert k >= 2  # two backward passes, >= 1 bucket each
 
 
-# ------------------------------------------- fused kernel vs barrier path
-def _seq_worker(rank, world, port, outdir, fused):
-    os.environ["OPTR_FUSED"] = "1" if fused else "0"
+# ------------------------------------------- fused kernel protocol stress
+LENS = [5_000_000, 8_388_608, 3_000_000, 16_000_000, 5_000_000]
+
+
+def _checksum(t):
+    """Position-weighted sum of the fp32 bit patterns (detects any changed,
+    moved or stale element)."""
+    v = t.view(torch.int32).to(torch.int64)
+    w = torch.arange(v.numel(), device=t.device, dtype=torch.int64) % 1009 + 1
+    return (v * w).sum()
+
+
+def _seq_worker(rank, world, port, outdir, mode, reps):
+    os.environ["OPTR_FUSED"] = "0" if mode == "barrier" else "1"
     import torch.distributed as dist
 
     from paper_2310_06993_b200.collectives import MaskSpec
@@ -261,44 +320,59 @@ def _seq_worker(rank, world, port, outdir, fused):
     torch.cuda.set_device(_dev(rank))
     dev = torch.device("cuda", _dev(rank))
     _init(rank, world, dev)
-    lens = [5_000_000, 8_388_608, 3_000_000, 16_000_000, 5_000_000]
-    comm = TarCommunicator(max_len=max(lens))
+    comm = TarCommunicator(max_len=max(LENS))
     g = torch.Generator(device=dev).manual_seed(50 + rank)
-    xs = [torch.randn(L, device=dev, generator=g) for L in lens]
+    xs = [torch.randn(L, device=dev, generator=g) for L in LENS]
     outs = [torch.empty_like(x) for x in xs]
-    recs = [torch.zeros(2, dtype=torch.int64, device=dev) for _ in lens]
-    for rep in range(2):  # second pass: both parities reused at the next epochs
-        for b, L in enumerate(lens):
-            gen = rep * len(lens) + b
+    recs = [torch.zeros(2, dtype=torch.int64, device=dev) for _ in LENS]
+    sums = torch.zeros((reps, len(LENS), 3), dtype=torch.int64, device=dev)
+    for rep in range(reps):
+        for b, L in enumerate(LENS):
+            gen = rep * len(LENS) + b
             comm.allreduce(xs[b], outs[b], rotation=gen % world, ht=True, job_seed=4, generation=gen,
-                           masks=MaskSpec.coin(300 + gen, 0.02), received=recs[b], async_op=True)
+                           masks=MaskSpec.coin(300 + gen, 0.02), received=recs[b], async_op=(mode != "sync"))
+            if mode == "sync":  # fully serialised: host sync + all-rank barrier between calls
+                torch.cuda.synchronize()
+                dist.barrier()
         comm.join()
+        for b in range(len(LENS)):
+            sums[rep, b, 0] = _checksum(outs[b])
+            sums[rep, b, 1:] = recs[b]
+        if rep == 0:
+            first = [o.clone() for o in outs]
     torch.cuda.synchronize()
-    for b in range(len(lens)):
-        np.save(os.path.join(outdir, f"f{int(fused)}_b{b}_r{rank}.npy"), outs[b].cpu().numpy())
-        np.save(os.path.join(outdir, f"f{int(fused)}_b{b}_r{rank}_rec.npy"), recs[b].cpu().numpy())
+    np.save(os.path.join(outdir, f"{mode}_r{rank}.npy"), sums.cpu().numpy())
+    for b in range(len(LENS)):  # the first repetition's results in full
+        np.save(os.path.join(outdir, f"{mode}_b{b}_r{rank}.npy"), first[b].cpu().numpy())
     comm.close()
     dist.destroy_process_group()
 
 
 @pytest.mark.gpu
-@pytest.mark.multigpu
-def test_fused_kernel_matches_barrier_path_async():
-    """Async back-to-back buckets through the fused per-tile-flag kernel give
-    the barrier-separated path's results (float32 codec tolerance; the pass
-    order differs) and identical received counts."""
+def test_fused_protocol_async_stress():
+    """The fused kernel's per-tile flags under back-to-back async calls (two
+    call parities in flight, epochs advancing) give bit-identical results and
+    received counts to the same calls fully serialised (host sync and an
+    all-rank barrier between calls), over reps x 5 buckets of D = 2^22..2^24;
+    and the barrier-separated unfused path agrees within the float32 codec
+    tolerance (its pass order differs).  OPTR_TEST_STRESS=reps scales it up
+    (profiles/: 2,000 reps = 10,000 calls per mode on 2 GPUs)."""
     import torch.multiprocessing as mp
 
-    if not torch.cuda.is_available() or torch.cuda.device_count() < 2:
-        pytest.skip("needs >= 2 GPUs")
+    _need_gpu()
     world = _world()
+    reps = int(os.environ.get("OPTR_TEST_STRESS", "3"))
     with tempfile.TemporaryDirectory() as d:
-        for fused in (True, False):
-            mp.spawn(_seq_worker, args=(world, _free_port(), d, fused), nprocs=world, join=True)
-        for b in range(5):
-            for r in range(world):
-                a = np.load(os.path.join(d, f"f1_b{b}_r{r}.npy")).astype(np.float64)
-                c = np.load(os.path.join(d, f"f0_b{b}_r{r}.npy")).astype(np.float64)
-                assert np.linalg.norm(a - c) / np.linalg.norm(c) < 1e-5, (b, r)
-                np.testing.assert_array_equal(np.load(os.path.join(d, f"f1_b{b}_r{r}_rec.npy")),
-                                              np.load(os.path.join(d, f"f0_b{b}_r{r}_rec.npy")))
+        for mode in ("async", "sync", "barrier"):
+            mp.spawn(_seq_worker, args=(world, _free_port(), d, mode, reps if mode != "barrier" else 1),
+                     nprocs=world, join=True)
+        for r in range(world):
+            a = np.load(os.path.join(d, f"async_r{r}.npy"))
+            s = np.load(os.path.join(d, f"sync_r{r}.npy"))
+            np.testing.assert_array_equal(a, s)
+            bar = np.load(os.path.join(d, f"barrier_r{r}.npy"))
+            np.testing.assert_array_equal(bar[0, :, 1:], a[0, :, 1:])  # received counts
+            for b in range(len(LENS)):
+                f = np.load(os.path.join(d, f"async_b{b}_r{r}.npy")).astype(np.float64)
+                c = np.load(os.path.join(d, f"barrier_b{b}_r{r}.npy")).astype(np.float64)
+                assert np.linalg.norm(f - c) / np.linalg.norm(c) < 1e-5, (b, r)

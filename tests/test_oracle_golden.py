@@ -10,7 +10,7 @@ import numpy as np
 import pytest
 
 import oracle as O
-from golden_util import GOLDEN
+from golden_util import GOLDEN, load
 
 
 def _load(name):
@@ -122,3 +122,35 @@ def test_fwht_dense_sylvester():
         np.testing.assert_allclose(O.fwht(x.copy()), h @ x, rtol=1e-10, atol=1e-10)
     with pytest.raises(ValueError):
         O.fwht(np.zeros(3))
+
+
+def _bf16(x):
+    """float32 -> bfloat16 (ties to even) as float32, like make_golden.bf16_round."""
+    u = np.ascontiguousarray(x, dtype=np.float32).view(np.uint32).astype(np.uint64)
+    u = (u + 0x7FFF + ((u >> 16) & 1)) & 0xFFFF0000
+    return u.astype(np.uint32).view(np.float32)
+
+
+def test_sim_capture_gpt2xl_shape_replays_reference():
+    """The reference's SimSession at the GPT-2 XL bucket shape (n=8,
+    13,107,200 bf16-valued entries, 5% drops, adaptive timeouts; masks
+    captured at consumption time) is reproduced exactly by the oracle:
+    sampled entries bit-equal, per-node sums equal."""
+    z = load("sim_gpt2xl.npz")
+    n, L, ht, r, gen_idx, seed, epp, dim = (int(v) for v in z["meta"])
+    npk = O.n_packets(dim // n, epp)
+    masks = {}
+    for dst in range(n):
+        for src in range(n):
+            if src != dst:
+                for stage in (1, 2):
+                    bits = np.unpackbits(z[f"m{stage}_{dst}_{src}"], bitorder="little")[:npk]
+                    masks[(stage, dst, src)] = bits.astype(bool)
+    lost = sum(int((~m).sum()) for m in masks.values()) / sum(len(m) for m in masks.values())
+    assert 0.0 < lost <= 0.06  # configs[3]: adaptive-timeout masks up to ~5%
+    want = O.run_generation([_bf16(b) for b in O.make_buckets(seed, n, L)], seed, gen_idx, bool(ht),
+                            masks=masks, r=r, epp=epp, threads=n)
+    idx = z["sample_idx"]
+    for node in range(n):
+        np.testing.assert_array_equal(want[node][idx], z["sample_out"][node])
+        assert want[node].astype(np.float64).sum() == z["out_sum"][node]
