@@ -15,7 +15,10 @@
  *   optr_fwht                 hadamard.py:76-90   fwht_in_place
  *   optr_rht_encode           hadamard.py:93-102  rht_encode
  *   optr_rht_decode           hadamard.py:105-123 rht_decode (+ EmptyReceptionError)
+ *   optr_*_f64                hadamard.py:76-123 in float64, bit-identical
  *   optr_masks_host           datagram.py:70-72,111-124 send-side coin, as packet bitmaps
+ *   optr_coin_packets         datagram.py:70-72,122 the coin of any sender's k-th packets
+ *   optr_mean_received        collectives.py:77-94 _mean_received
  *   optr_tar_local            runner.py:211-276 run_generation hot path (encode ->
  *                             collectives.py:97-150 tar_allreduce -> decode) for n
  *                             workers co-resident on one GPU (the SimSession shape)
@@ -67,6 +70,10 @@ typedef struct {
   uint64_t seed;         /* COIN: sender src draws from SeedSequence([seed,src]) */
   double drop_prob;      /* COIN: packet dropped iff random() < drop_prob      */
   const uint32_t* bitmap;/* BITMAP: device pointer in the layout above         */
+  /* COIN: host array of n draws each sender's stream made before this call
+   * (a DatagramEndpoint keeps one generator for every run(), datagram.py:70-72,
+   * so its k-th collective continues the stream); NULL = fresh streams.     */
+  const uint64_t* stream_offsets;
 } optr_mask_spec;
 
 /* ------------------------------------------------------------ host helpers */
@@ -79,6 +86,12 @@ int64_t optr_mask_words(int64_t dim, int n, int epp);
 /* host computation of the coin bitmaps (same layout; no GPU needed) */
 int optr_masks_host(uint32_t* bitmap_host, int64_t dim, int n, int rotation,
                     uint64_t seed, double drop_prob, int epp);
+/* keep[i] = 1 iff packet start+i of sender src's datagram coin stream is
+ * delivered (PCG64(SeedSequence([seed, src])).random() >= drop_prob,
+ * datagram.py:70-72,122), counter-indexed: any collective's per-packet
+ * drops in its own send order (host, no GPU needed). */
+int optr_coin_packets(uint64_t seed, int src, uint64_t start, int64_t count, double drop_prob,
+                      uint8_t* keep_host);
 /* library build/version string */
 const char* optr_version(void);
 
@@ -99,6 +112,25 @@ int optr_rht_encode(const void* x, int dtype_in, int64_t L, float* y, int64_t di
  * (hadamard.py:117-118).  out dtype OPTR_F32/BF16. */
 int optr_rht_decode(const float* y, const uint8_t* mask, int64_t dim, int64_t L,
                     uint64_t seed, void* out, int dtype_out, void* stream);
+
+/* Float64 codec in the reference's own arithmetic (numpy float64 callers):
+ * the same butterfly stages in the same order as hadamard.py:76-90, so the
+ * results are bit-identical to the reference's fwht_in_place / rht_encode /
+ * rht_decode (hadamard.py:76-123).  optr_rht_decode_f64 synchronises the
+ * stream to read the received count (OPTR_EEMPTY when it is 0). */
+int optr_fwht_f64(double* v, int64_t dim, void* stream);
+int optr_rht_encode_f64(const double* x, int64_t L, double* y, int64_t dim, uint64_t seed, void* stream);
+int optr_rht_decode_f64(const double* y, const uint8_t* mask, int64_t dim, int64_t L, uint64_t seed,
+                        double* out, void* stream);
+
+/* collectives.py:77-94 _mean_received on the GPU: out = float32(sum in
+ * ascending node order of own (i == rank) and peers[i] (as given, zero where
+ * missing) / sum of (1 for own, masks[i] for peers)), 0 where the count is 0,
+ * accumulated in float64 -- bit-identical to the reference.  peers, masks:
+ * HOST arrays of n device pointers; peers[i] NULL = no data from i (skipped),
+ * masks[i] NULL = every entry of peers[i] received (1 byte per entry). */
+int optr_mean_received(const float* own, const float* const* peers, const uint8_t* const* masks, int n,
+                       int rank, int64_t len, float* out, void* stream);
 
 /* ------------------------------------------- TAR+RHT, n workers on one GPU */
 /* Workspace bytes for optr_tar_local. */

@@ -40,6 +40,7 @@ class optr_mask_spec(ctypes.Structure):
         ("seed", ctypes.c_uint64),
         ("drop_prob", ctypes.c_double),
         ("bitmap", ctypes.c_void_p),
+        ("stream_offsets", ctypes.c_void_p),
     ]
 
 
@@ -55,10 +56,15 @@ SIGNATURES = {
     "optr_mask_words": (_i64, [_i64, _int, _int]),
     "optr_masks_host": (_int, [_vp, _i64, _int, _int, _u64, ctypes.c_double, _int]),
     "optr_version": (ctypes.c_char_p, []),
+    "optr_coin_packets": (_int, [_u64, _int, _u64, _i64, ctypes.c_double, _vp]),
+    "optr_mean_received": (_int, [_vp, _vp, _vp, _int, _int, _i64, _vp, _vp]),
     "optr_rht_signs": (_int, [_vp, _i64, _u64, _vp]),
     "optr_fwht": (_int, [_vp, _i64, _vp]),
     "optr_rht_encode": (_int, [_vp, _int, _i64, _vp, _i64, _u64, _vp]),
     "optr_rht_decode": (_int, [_vp, _vp, _i64, _i64, _u64, _vp, _int, _vp]),
+    "optr_fwht_f64": (_int, [_vp, _i64, _vp]),
+    "optr_rht_encode_f64": (_int, [_vp, _i64, _vp, _i64, _u64, _vp]),
+    "optr_rht_decode_f64": (_int, [_vp, _vp, _i64, _i64, _u64, _vp, _vp]),
     "optr_tar_local_workspace": (ctypes.c_size_t, [_int, _i64, _int, _int]),
     "optr_tar_local": (_int, [ctypes.POINTER(_vp), ctypes.POINTER(_vp), _int, _i64, _int, _int, _u64,
                               _u64, _u64, _int, _int, ctypes.POINTER(optr_mask_spec), _vp,

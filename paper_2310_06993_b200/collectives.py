@@ -108,6 +108,15 @@ def unpack_packet_masks(words: np.ndarray, dim: int, n: int, r: int, epp: int) -
     return out
 
 
+def coin_packets(seed: int, src: int, start: int, count: int, drop_prob: float) -> np.ndarray:
+    """Delivered flags of packets ``start .. start+count-1`` of sender ``src``'s
+    datagram coin stream (datagram.py:70-72,122), counter-indexed."""
+    keep = np.zeros(max(int(count), 0), dtype=np.uint8)
+    check(lib().optr_coin_packets(int(seed), int(src), int(start), int(count), float(drop_prob),
+                                  keep.ctypes.data if count > 0 else None), "coin_packets")
+    return keep.astype(bool)
+
+
 def coin_masks_host(dim: int, n: int, r: int, seed: int, drop_prob: float,
                     epp: int = MAX_PAYLOAD // ENTRY_BYTES) -> dict:
     """The datagram coin (datagram.py:70-72,117-124) computed by liboptr's host
@@ -136,16 +145,22 @@ class MaskSpec:
     seed: int = 0
     drop_prob: float = 0.0
     bitmap: object = None  # CUDA int32 tensor in the optr.h layout
+    # coin: draws each sender's stream made before this call (a reused
+    # DatagramEndpoint continues its generator, datagram.py:70-72); None = 0
+    stream_offsets: object = None
 
     @classmethod
     def none(cls, max_payload: int = MAX_PAYLOAD) -> "MaskSpec":
         return cls("none", epp=max_payload // ENTRY_BYTES)
 
     @classmethod
-    def coin(cls, seed: int, drop_prob: float, max_payload: int = MAX_PAYLOAD) -> "MaskSpec":
+    def coin(cls, seed: int, drop_prob: float, max_payload: int = MAX_PAYLOAD,
+             stream_offsets=None) -> "MaskSpec":
         if not 0.0 <= drop_prob <= 1.0:
             raise ValueError("drop_prob must be in [0,1]")
-        return cls("coin", epp=max_payload // ENTRY_BYTES, seed=int(seed), drop_prob=float(drop_prob))
+        offs = None if stream_offsets is None else [int(v) for v in stream_offsets]
+        return cls("coin", epp=max_payload // ENTRY_BYTES, seed=int(seed), drop_prob=float(drop_prob),
+                   stream_offsets=offs)
 
     @classmethod
     def from_packets(cls, packets: dict, dim: int, n: int, max_payload: int = MAX_PAYLOAD,
@@ -164,8 +179,12 @@ class MaskSpec:
             raise ValueError(f"unknown mask kind {self.kind!r}")
         if self.epp <= 0:
             raise ValueError("max_payload must hold at least one entry")
+        offs = None
+        if self.stream_offsets is not None:
+            self._offs_c = (ctypes.c_uint64 * _lib.MAX_WORKERS)(*self.stream_offsets)  # kept alive with the spec
+            offs = ctypes.addressof(self._offs_c)
         return _lib.optr_mask_spec(kinds[self.kind], int(self.epp), int(self.seed), float(self.drop_prob),
-                                   self.bitmap.data_ptr() if self.bitmap is not None else None)
+                                   self.bitmap.data_ptr() if self.bitmap is not None else None, offs)
 
 
 @dataclass

@@ -13,6 +13,7 @@
 #include "../../include/optr.h"
 #include "kernels.cuh"
 #include "tma.cuh"
+#include "internal.h"
 
 #include <cudaTypedefs.h>
 
@@ -639,7 +640,8 @@ int setup_masks(PrepArgs& a, const optr_mask_spec* ms, int64_t dim, int n, int r
     for (int s = 0; s < n; ++s) {
       uint64_t ent[2] = {ms->seed, (uint64_t)s};
       Pcg p = pcg_from_u64s(ent, 2);
-      a.coin_state[s] = p.state;
+      // a continued stream starts after the sender's earlier draws
+      a.coin_state[s] = ms->stream_offsets ? pcg_advance(p.state, p.inc, ms->stream_offsets[s]) : p.state;
       a.coin_inc[s] = p.inc;
     }
   }
@@ -664,6 +666,9 @@ int check_common(int n, int64_t L, int dtype_in, int dtype_out, const optr_mask_
 
 }  // namespace
 
+void optr_note_launches(int k) { g_launches += k; }
+void optr_bind_stream_device(void* stream) { bind_device(stream); }
+
 extern "C" {
 
 // ------------------------------------------------------------ host helpers
@@ -681,6 +686,18 @@ int64_t optr_next_pow2(int64_t n) { return next_pow2_i(n); }
 int64_t optr_mask_words(int64_t dim, int n, int epp) {
   if (n < 1 || epp <= 0 || dim < 0) return -1;
   return mask_words(dim, n, epp);
+}
+
+int optr_coin_packets(uint64_t seed, int src, uint64_t start, int64_t count, double p, uint8_t* keep) {
+  if (src < 0 || count < 0 || (count > 0 && !keep) || !(p >= 0.0 && p <= 1.0)) return OPTR_EINVAL;
+  uint64_t ent[2] = {seed, (uint64_t)src};
+  Pcg g = pcg_from_u64s(ent, 2);
+  u128 s = pcg_advance(g.state, g.inc, start);
+  for (int64_t k = 0; k < count; ++k) {
+    s = pcg_step(s, g.inc);
+    keep[k] = coin_drops(pcg_xsl_rr(s), p) ? 0 : 1;
+  }
+  return OPTR_OK;
 }
 
 int optr_masks_host(uint32_t* bm, int64_t dim, int n, int rotation, uint64_t seed, double p, int epp) {
@@ -710,6 +727,31 @@ int optr_masks_host(uint32_t* bm, int64_t dim, int n, int rotation, uint64_t see
       }
     }
   }
+  return OPTR_OK;
+}
+
+int optr_mean_received(const float* own, const float* const* peers, const uint8_t* const* masks, int n, int rank,
+                       int64_t len, float* out, void* stream) {
+  if (n < 1 || n > OPTR_MAX_WORKERS || rank < 0 || rank >= n || len < 0 || !peers) return OPTR_EINVAL;
+  if (len > 0 && (!own || !out)) return OPTR_EINVAL;
+  if (len == 0) return OPTR_OK;
+  bind_device(stream);
+  MeanRecvArgs a;
+  memset(&a, 0, sizeof(a));
+  a.own = own;
+  for (int i = 0; i < n; ++i) {
+    a.peers[i] = peers[i];
+    a.masks[i] = masks ? masks[i] : nullptr;
+  }
+  a.n = n;
+  a.rank = rank;
+  a.len = len;
+  a.out = out;
+  int64_t blocks = (len + 255) / 256;
+  if (blocks > kMaxGrid) blocks = kMaxGrid;
+  KScope ks(OPTR_K_AGG, (cudaStream_t)stream);
+  mean_received_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(a);
+  CK(cudaGetLastError());
   return OPTR_OK;
 }
 
@@ -969,11 +1011,14 @@ bool local_fast_plan(int64_t L, int64_t dim, int n, int ht, const void* const* x
   return true;
 }
 
-template <int T>
+template <int T, int NW>
 int launch_mean_t(const TmaArgs& a, const MeanArgs& m, cudaStream_t st) {
+  // two CTAs per SM (<= 128 registers: the fp64 accumulators take 64) with a
+  // two-stage ring: 61.5 us per 2^23 bucket of 4 workers against 71.6 us for
+  // one CTA with three stages (140 registers; profiles/r02_quick_mean_ab.txt)
   constexpr int S = 2;
   const size_t smem = tma_smem_bytes<T, S>();
-  auto kern = tma_mean_kernel<T, S>;
+  auto kern = tma_mean_kernel<T, S, NW>;
   int rc = set_smem_attr(kern, smem);
   if (rc) return rc;
   int dev = 0, nsm = 148, per_sm = 1;
@@ -988,6 +1033,17 @@ int launch_mean_t(const TmaArgs& a, const MeanArgs& m, cudaStream_t st) {
   KScope ks(OPTR_K_ENC_MEAN, st, m.n);
   launch_ex(kern, dim3((unsigned)gx), dim3(1 << (T - 5)), smem, st, a, m);
   return launch_check(kern, "tma_mean", T, 0, (int)gx, 1, 1 << (T - 5), smem);
+}
+
+template <int T>
+int launch_mean_n(const TmaArgs& a, const MeanArgs& m, cudaStream_t st) {
+  switch (m.n) {
+    case 2: return launch_mean_t<T, 2>(a, m, st);
+    case 4: return launch_mean_t<T, 4>(a, m, st);
+    case 8: return launch_mean_t<T, 8>(a, m, st);
+    case 16: return launch_mean_t<T, 16>(a, m, st);
+    default: return OPTR_EINVAL;
+  }
 }
 
 int tar_local_impl(const void* const* x, void* const* out, int n, int64_t L, int dtype_in, int dtype_out,
@@ -1090,7 +1146,7 @@ int tar_local_impl(const void* const* x, void* const* out, int n, int64_t L, int
     ma.r = r;
     ma.shard_shift = log2_exact(sh.base);
     ma.m = mv;
-    rc = fp.contig.ks == 13 ? launch_mean_t<13>(ta, ma, st) : launch_mean_t<14>(ta, ma, st);
+    rc = fp.contig.ks == 13 ? launch_mean_n<13>(ta, ma, st) : launch_mean_n<14>(ta, ma, st);
     if (rc) return rc;
     // 4. contiguous decode pass with the stage-2 receive, A -> Y
     for (int o = 0; o < n; ++o) ga.A[o] = A + sh.off(owned_shard(o, r, n));

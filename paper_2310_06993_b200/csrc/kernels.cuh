@@ -1001,6 +1001,34 @@ __global__ void __launch_bounds__(256) aggregate_kernel(const __grid_constant__ 
   }
 }
 
+// collectives.py:77-94 over explicit per-peer buffers (the sans-IO protocol's
+// StageResult: zero-filled data + per-entry masks), for the generator-level
+// collectives (tar / tar2d / ring / ps) of the facade.
+struct MeanRecvArgs {
+  const float* own;
+  const float* peers[kMaxW];   // nullptr: peer not in result.data
+  const uint8_t* masks[kMaxW]; // nullptr: all received
+  int n, rank;
+  int64_t len;
+  float* out;
+};
+
+__global__ void __launch_bounds__(256) mean_received_kernel(const __grid_constant__ MeanRecvArgs a) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < a.len; e += (int64_t)gridDim.x * blockDim.x) {
+    double acc = 0.0, cnt = 0.0;
+    for (int i = 0; i < a.n; ++i) {
+      if (i == a.rank) {
+        acc += (double)a.own[e];
+        cnt += 1.0;
+      } else if (a.peers[i]) {
+        acc += (double)a.peers[i][e];
+        cnt += (a.masks[i] == nullptr || a.masks[i][e]) ? 1.0 : 0.0;
+      }
+    }
+    a.out[e] = cnt > 0.0 ? mean_of(acc, cnt) : 0.f;
+  }
+}
+
 // ------------------------------------------------------------- assemble
 struct AsmArgs {
   SrcGather gather;

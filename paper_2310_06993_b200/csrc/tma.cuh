@@ -338,15 +338,53 @@ __device__ __forceinline__ void tma_tile(const TmaMaps* maps, const CUtensorMap*
                        __int_as_float(__float_as_int(q4.w) ^ ((~sw & 8u) << 28)));
     } else {
       q4 = *reinterpret_cast<const float4*>(tile + i);
-      if constexpr (SK == TS_GATHER) {
-        if (!all_kept) q4 = gather_mask4(a, worker, gotw, g, q4);
-        else if (gotw) *reinterpret_cast<uchar4*>(gotw + g) = make_uchar4(1, 1, 1, 1);
-      }
     }
     v[4 * m] = q4.x;
     v[4 * m + 1] = q4.y;
     v[4 * m + 2] = q4.z;
     v[4 * m + 3] = q4.w;
+  }
+  if constexpr (SK == TS_GATHER) {
+    // stage-2 masks (collectives.py:140-150); a tile whose packets all
+    // arrived skips them (one branch per tile, not per float4)
+    if (!all_kept && !STRIDED) {
+      // contiguous tile: one shard, one owner (not this receiver), one
+      // bitmap row for the whole tile
+      const int j = (int)(g0 >> a.shard_shift);
+      const uint32_t* const row = a.m.row(1, worker, shard_owner(j, a.r, a.n));
+      const uint32_t e0 = (uint32_t)(g0 - ((int64_t)j << a.shard_shift));
+#pragma unroll
+      for (int m = 0; m < 8; ++m) {
+        const int i = b0 + roff(P, 0, 4 * m);
+        const uint32_t kk = keep4(row, e0 + (uint32_t)i, a.m);
+        v[4 * m] = (kk & 1u) ? v[4 * m] : 0.f;
+        v[4 * m + 1] = (kk & 2u) ? v[4 * m + 1] : 0.f;
+        v[4 * m + 2] = (kk & 4u) ? v[4 * m + 2] : 0.f;
+        v[4 * m + 3] = (kk & 8u) ? v[4 * m + 3] : 0.f;
+        if (gotw)
+          *reinterpret_cast<uchar4*>(gotw + g0 + i) =
+              make_uchar4(kk & 1u, (kk >> 1) & 1u, (kk >> 2) & 1u, (kk >> 3) & 1u);
+      }
+    } else if (!all_kept) {
+#pragma unroll
+      for (int m = 0; m < 8; ++m) {
+        const int i = b0 + roff(P, 0, 4 * m);
+        const int64_t g = STRIDED ? (g0 + ((int64_t)(i >> CB) << a.lo) + (i & CM)) : (g0 + i);
+        const float4 q4 = gather_mask4(a, worker, gotw, g, make_float4(v[4 * m], v[4 * m + 1], v[4 * m + 2],
+                                                                       v[4 * m + 3]));
+        v[4 * m] = q4.x;
+        v[4 * m + 1] = q4.y;
+        v[4 * m + 2] = q4.z;
+        v[4 * m + 3] = q4.w;
+      }
+    } else if (gotw) {
+#pragma unroll
+      for (int m = 0; m < 8; ++m) {
+        const int i = b0 + roff(P, 0, 4 * m);
+        const int64_t g = STRIDED ? (g0 + ((int64_t)(i >> CB) << a.lo) + (i & CM)) : (g0 + i);
+        *reinterpret_cast<uchar4*>(gotw + g) = make_uchar4(1, 1, 1, 1);
+      }
+    }
   }
   bfly32<P.xm[0]>(v);
   // strided decode epilogue with transposed signs: take this thread's
@@ -548,20 +586,20 @@ struct MeanArgs {
   MaskView m;   // stage-1 rows (stage 0 of the bitmap layout)
 };
 
-template <int T, int kStages>
-__global__ void __launch_bounds__(1 << (T - 5)) tma_mean_kernel(const __grid_constant__ TmaArgs a,
-                                                              const __grid_constant__ MeanArgs ma) {
+template <int T, int kStages, int NW>
+__global__ void __launch_bounds__(1 << (T - 5), 2) tma_mean_kernel(const __grid_constant__ TmaArgs a,
+                                                                 const __grid_constant__ MeanArgs ma) {
   constexpr size_t SB = tma_stage_bytes<T>();
   constexpr RPlan P = make_rplan(T, 0);
   constexpr int LR = P.nr - 1;
   static_assert(P.pos[LR][0] == 0, "vector groups in the last round");
   // the last round holds tile bits 0,1 (float4 groups, T = 13) or bit 0 (pairs, T = 14)
   constexpr int VW = P.pos[LR][1] == 1 ? 4 : 2;
+  constexpr int NQ = 32 / VW;
   extern __shared__ __align__(16) unsigned char smraw[];
   unsigned char* const base = smraw + ((1024u - (smem_u32(smraw) & 1023u)) & 1023u);
   uint64_t* const full = reinterpret_cast<uint64_t*>(base + kStages * SB);
   const int tid = threadIdx.x;
-  const int n = ma.n;
   if (tid == 0) {
     for (int s = 0; s < kStages; ++s) mbar_init(&full[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -570,65 +608,72 @@ __global__ void __launch_bounds__(1 << (T - 5)) tma_mean_kernel(const __grid_con
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   asm volatile("griddepcontrol.wait;" ::: "memory");
   const int64_t stride = gridDim.x;
-  // job k = (tile blockIdx.x + (k / n) * stride, worker k % n)
+  // job k = (tile blockIdx.x + (k / NW) * stride, worker k % NW)
   auto issue = [&](int64_t k, int s) {
-    const int64_t t = blockIdx.x + (k / n) * stride;
-    if (t < a.ntiles) tile_issue_contig<T, TS_BUF>(a, (int)(k % n), t, base + (size_t)s * SB, &full[s]);
+    const int64_t t = blockIdx.x + (k / NW) * stride;
+    if (t < a.ntiles) tile_issue_contig<T, TS_BUF>(a, (int)(k % NW), t, base + (size_t)s * SB, &full[s]);
   };
   if (tid == 0)
     for (int s = 0; s < kStages; ++s) issue(s, s);
   double acc[32];
-  uint32_t cnt[8];
-  uint32_t slow = 0;  // bit w: worker w's tile needs per-entry masks
-  int owner = 0;
-  uint32_t e0 = 0;    // tile offset inside its shard
+  uint32_t cnt[NQ / 2 > 4 ? NQ / 2 : 4];  // count byte per entry (entries 4c..4c+3 in cnt[c])
+#pragma unroll
+  for (int j = 0; j < 32; ++j) acc[j] = 0.0;
+  const float scale = ma.scale;
   const SnkBuf::B nosnk{nullptr, 1.f};
   for (int64_t k = 0;; ++k) {
-    const int64_t t = blockIdx.x + (k / n) * stride;
+    const int64_t t = blockIdx.x + (k / NW) * stride;
     if (t >= a.ntiles) break;
-    const int w = (int)(k % n);
+    const int w = (int)(k % NW);
     const int s = (int)(k % kStages);
-    if (w == 0) {
-      const int64_t g0 = t << T;
-      const int j = (int)(g0 >> ma.shard_shift);
-      owner = shard_owner(j, ma.r, n);
-      e0 = (uint32_t)(g0 - ((int64_t)j << ma.shard_shift));
-      slow = 0;
-      for (int i = 0; i < n; ++i)
-        if (i != owner && !packets_all_kept(ma.m.row(0, owner, i), e0, 1u << T, ma.m)) slow |= 1u << i;
-    }
+    // owner of the tile's shard and the tile's offset inside it (uniform)
+    const int64_t g0 = t << T;
+    const int j = (int)(g0 >> ma.shard_shift);
+    const int owner = shard_owner(j, ma.r, NW);
+    const uint32_t e0 = (uint32_t)(g0 - ((int64_t)j << ma.shard_shift));
+    // per-entry masks only for a peer with a lost packet over this tile
+    const bool masked = w != owner && !packets_all_kept(ma.m.row(0, owner, w), e0, 1u << T, ma.m);
     mbar_wait(&full[s], (uint32_t)((k / kStages) & 1));
     tma_tile<T, false, TS_BUF, SnkBuf, 3>(
         nullptr, nullptr, a, nosnk, w, nullptr, t, base + (size_t)s * SB, [&]() { issue(k + kStages, s); },
         [&](const float (&v)[32], int b2) {
-          const bool masked = (slow >> w) & 1u;
-          // entry j = VW*q + c of this thread: count byte j%4 of cnt[j/4]
+          uint32_t kk[NQ];
 #pragma unroll
-          for (int q = 0; q < 32 / VW; ++q) {
-            const uint32_t i = (uint32_t)(b2 + roff(P, LR, VW * q));
-            uint32_t kk = (1u << VW) - 1u;
-            if (masked) {
-              const uint32_t e = e0 + i;
-              kk = (keep4(ma.m.row(0, owner, w), e & ~3u, ma.m) >> (e & 3u)) & ((1u << VW) - 1u);
+          for (int q = 0; q < NQ; ++q) kk[q] = (1u << VW) - 1u;
+          if (masked) {
+            const uint32_t* row = ma.m.row(0, owner, w);
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) {
+              const uint32_t e = e0 + (uint32_t)(b2 + roff(P, LR, VW * q));
+              kk[q] = (keep4(row, e & ~3u, ma.m) >> (e & 3u)) & ((1u << VW) - 1u);
             }
+          }
+          // fp64 accumulation in ascending worker order (misses add 0.0)
+#pragma unroll
+          for (int q = 0; q < NQ; ++q) {
 #pragma unroll
             for (int c = 0; c < VW; ++c) {
-              const double x = ((kk >> c) & 1u) ? (double)(v[VW * q + c] * ma.scale) : 0.0;
-              acc[VW * q + c] = (w == 0 ? 0.0 : acc[VW * q + c]) + x;
+              const double x = (double)(v[VW * q + c] * scale);
+              acc[VW * q + c] += ((kk[q] >> c) & 1u) ? x : 0.0;
             }
-            const int cw = (VW * q) / 4, sh = 8 * ((VW * q) % 4);
-            cnt[cw] = ((w == 0 && sh == 0) ? 0u : cnt[cw]) + (nibble_bytes(kk) << sh);
           }
-          if (w == n - 1) {
-            float* const out = ma.agg + (t << T);
+          if (w == 0) {
 #pragma unroll
-            for (int q = 0; q < 32 / VW; ++q) {
+            for (int c = 0; c < NQ * VW / 4; ++c) cnt[c] = 0u;
+          }
+#pragma unroll
+          for (int q = 0; q < NQ; ++q) cnt[(VW * q) / 4] += nibble_bytes(kk[q]) << (8 * ((VW * q) % 4));
+          if (w == NW - 1) {
+            float* const out = ma.agg + g0;
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) {
               const int i = b2 + roff(P, LR, VW * q);
               float r[VW];
 #pragma unroll
               for (int c = 0; c < VW; ++c) {
-                const int j = VW * q + c;
-                r[c] = mean_of(acc[j], (double)((cnt[j / 4] >> (8 * (j % 4))) & 0xffu));
+                const int jj = VW * q + c;
+                r[c] = mean_of(acc[jj], (double)((cnt[jj / 4] >> (8 * (jj % 4))) & 0xffu));
+                acc[jj] = 0.0;
               }
               if constexpr (VW == 4)
                 st4(out + i, make_float4(r[0], r[1], r[2], r[3]));

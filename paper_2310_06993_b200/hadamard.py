@@ -6,9 +6,16 @@ sm_100a kernels of liboptr.so.  Functions accept numpy arrays (copied to the
 current CUDA device and back, returning numpy) or CUDA torch tensors
 (returning CUDA tensors, enqueued on the current stream).
 
-Numerics: the reference transforms in float64 and the runner casts the wire
-to float32 (runner.py:224); here the transform itself runs in float32, which
-stays within the north-star 1e-5 relative bound.
+Numerics, by input type:
+
+* numpy arrays (the reference's callers) and float64 CUDA tensors: float64
+  on the GPU with the reference's own butterfly order (optr_*_f64), so
+  ``fwht_in_place`` / ``rht_encode`` / ``rht_decode`` return float64 results
+  bit-identical to the reference's (a float32 numpy array given to
+  ``fwht_in_place`` is transformed in float32 like numpy would);
+* float32 / bfloat16 CUDA tensors (the gradient hot path): the float32 tile
+  kernels, within the north-star 1e-5 relative bound (the runner casts the
+  wire to float32 anyway, runner.py:224).
 """
 
 from __future__ import annotations
@@ -62,23 +69,6 @@ def derive_seed(job_seed: int, bucket_id: int, generation: int) -> int:
 def _stream_ptr(t) -> int:
     torch = _torch()
     return torch.cuda.current_stream(t.device).cuda_stream
-
-
-def _to_device(x, dtype=None):
-    """-> (cuda tensor, came_from_numpy)."""
-    torch = _torch()
-    if isinstance(x, torch.Tensor):
-        if not x.is_cuda:
-            raise ValueError("torch tensors must live on a CUDA device")
-        t = x.contiguous()
-        if dtype is not None and t.dtype != dtype:
-            t = t.to(dtype)
-        return t, False
-    arr = np.ascontiguousarray(np.asarray(x))
-    t = torch.from_numpy(arr.astype(np.float32) if arr.dtype != np.float32 else arr)
-    if dtype is not None and t.dtype != dtype:
-        t = t.to(dtype)
-    return t.cuda(), True
 
 
 def _dtype_code(t) -> int:
@@ -153,56 +143,98 @@ class DropMask:
         return cls(np.ones(dim, dtype=bool))
 
 
+def _f64_tensor(x):
+    """numpy / CUDA float64 tensor -> contiguous CUDA float64 tensor."""
+    torch = _torch()
+    if isinstance(x, torch.Tensor):
+        return x.contiguous()
+    return torch.from_numpy(np.ascontiguousarray(np.asarray(x, dtype=np.float64))).cuda()
+
+
+def _is_f64_path(x) -> bool:
+    torch = _torch()
+    if isinstance(x, torch.Tensor):
+        return x.dtype == torch.float64
+    return True  # numpy: the reference casts to float64 (hadamard.py:95, :111)
+
+
 def fwht_in_place(v):
-    """Unnormalised Sylvester FWHT (hadamard.py:76-90), float32 on the GPU.
-    Mutates ``v`` (numpy or CUDA tensor) and returns it."""
+    """Unnormalised Sylvester FWHT (hadamard.py:76-90).  Mutates ``v``
+    (numpy array or CUDA tensor) and returns it."""
     torch = _torch()
     d = len(v)
     if not _is_pow2(d):
         raise ValueError(f"length must be a power of two, got {d}")
     if isinstance(v, torch.Tensor):
-        if not v.is_cuda or v.dtype != torch.float32 or not v.is_contiguous():
-            raise ValueError("fwht_in_place needs a contiguous float32 CUDA tensor")
-        check(lib().optr_fwht(v.data_ptr(), d, _stream_ptr(v)), "fwht")
+        if not v.is_cuda or not v.is_contiguous() or v.dtype not in (torch.float32, torch.float64):
+            raise ValueError("fwht_in_place needs a contiguous float32 / float64 CUDA tensor")
+        fn = lib().optr_fwht_f64 if v.dtype == torch.float64 else lib().optr_fwht
+        check(fn(v.data_ptr(), d, _stream_ptr(v)), "fwht")
         return v
-    t, _ = _to_device(v, torch.float32)
-    check(lib().optr_fwht(t.data_ptr(), d, _stream_ptr(t)), "fwht")
-    v[...] = t.cpu().numpy().astype(v.dtype, copy=False)
+    arr = np.asarray(v)
+    if arr.dtype == np.float32:
+        t = torch.from_numpy(np.ascontiguousarray(arr)).cuda()
+        check(lib().optr_fwht(t.data_ptr(), d, _stream_ptr(t)), "fwht")
+    else:
+        t = _f64_tensor(arr)
+        check(lib().optr_fwht_f64(t.data_ptr(), d, _stream_ptr(t)), "fwht")
+    v[...] = t.cpu().numpy().astype(arr.dtype, copy=False)
     return v
 
 
 def rht_encode(x, ctx: RhtContext):
-    """y = H D pad(x) / sqrt(dim) (hadamard.py:93-102); float32 result."""
+    """y = H D pad(x) / sqrt(dim) (hadamard.py:93-102).  numpy or float64
+    input: float64 result, bit-identical to the reference; float32 / bfloat16
+    CUDA tensors: float32 CUDA result."""
     torch = _torch()
     if len(x) != ctx.orig_len:
         raise ValueError(f"expected {ctx.orig_len} entries, got {len(x)}")
-    is_t = isinstance(x, torch.Tensor)
-    t, from_np = _to_device(x, None if (is_t and x.dtype in (torch.float32, torch.bfloat16)) else torch.float32)
+    if _is_f64_path(x):
+        t = _f64_tensor(x)
+        y = torch.empty(ctx.dim, dtype=torch.float64, device=t.device)
+        check(lib().optr_rht_encode_f64(t.data_ptr(), ctx.orig_len, y.data_ptr(), ctx.dim, int(ctx.seed),
+                                        _stream_ptr(t)), "rht_encode")
+        return y if isinstance(x, torch.Tensor) else y.cpu().numpy()
+    if not x.is_cuda:
+        raise ValueError("torch tensors must live on a CUDA device")
+    t = x.contiguous() if x.dtype in (torch.float32, torch.bfloat16) else x.contiguous().float()
     y = torch.empty(ctx.dim, dtype=torch.float32, device=t.device)
     check(lib().optr_rht_encode(t.data_ptr(), _dtype_code(t), ctx.orig_len, y.data_ptr(), ctx.dim,
                                 int(ctx.seed), _stream_ptr(t)), "rht_encode")
-    return y.cpu().numpy() if from_np else y
+    return y
 
 
 def rht_decode(y_recv, mask: DropMask, ctx: RhtContext):
     """hadamard.py:105-123: zero-fill misses, scale dim/received, inverse,
     truncate.  Raises EmptyReceptionError when nothing arrived (this reads
-    the received count back, so it synchronises the stream)."""
+    the received count back, so it synchronises the stream).  numpy or
+    float64 input: float64 result, bit-identical to the reference."""
     torch = _torch()
     if len(y_recv) != ctx.dim:
         raise ValueError(f"expected {ctx.dim} entries, got {len(y_recv)}")
     if len(mask.received) != ctx.dim:
         raise ValueError("drop mask length does not match dim")
-    t, from_np = _to_device(y_recv, torch.float32)
+    f64 = _is_f64_path(y_recv)
+    if f64:
+        t = _f64_tensor(y_recv)
+    else:
+        if not y_recv.is_cuda:
+            raise ValueError("torch tensors must live on a CUDA device")
+        t = y_recv.contiguous().float()
     m = mask.received
     if isinstance(m, torch.Tensor):
         mt = m.to(device=t.device, dtype=torch.uint8).contiguous()
     else:
         mt = torch.from_numpy(np.asarray(m, dtype=np.uint8)).to(t.device)
+    if f64:
+        out = torch.empty(ctx.orig_len, dtype=torch.float64, device=t.device)
+        check(lib().optr_rht_decode_f64(t.data_ptr(), mt.data_ptr(), ctx.dim, ctx.orig_len, int(ctx.seed),
+                                        out.data_ptr(), _stream_ptr(t)), "rht_decode")
+        return out if isinstance(y_recv, torch.Tensor) else out.cpu().numpy()
     out = torch.empty(ctx.orig_len, dtype=torch.float32, device=t.device)
     check(lib().optr_rht_decode(t.data_ptr(), mt.data_ptr(), ctx.dim, ctx.orig_len, int(ctx.seed),
                                 out.data_ptr(), _lib.OPTR_F32, _stream_ptr(t)), "rht_decode")
-    return out.cpu().numpy() if from_np else out
+    return out
 
 
 def mse(a, b) -> float:
