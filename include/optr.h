@@ -19,6 +19,8 @@
  *   optr_masks_host           datagram.py:70-72,111-124 send-side coin, as packet bitmaps
  *   optr_coin_packets         datagram.py:70-72,122 the coin of any sender's k-th packets
  *   optr_mean_received        collectives.py:77-94 _mean_received
+ *   optr_ring_*               collectives.py:248-292 ring_allreduce arithmetic
+ *   optr_packetize / _depacketize  wire.py:36-85,176-208 header codec + framing
  *   optr_tar_local            runner.py:211-276 run_generation hot path (encode ->
  *                             collectives.py:97-150 tar_allreduce -> decode) for n
  *                             workers co-resident on one GPU (the SimSession shape)
@@ -131,6 +133,32 @@ int optr_rht_decode_f64(const double* y, const uint8_t* mask, int64_t dim, int64
  * masks[i] NULL = every entry of peers[i] received (1 byte per entry). */
 int optr_mean_received(const float* own, const float* const* peers, const uint8_t* const* masks, int n,
                        int rank, int64_t len, float* out, void* stream);
+
+/* Ring baseline steps (collectives.py:248-292), float64 partial sums:
+ * optr_ring_cast: out = float32(chunk); optr_ring_step: gather == 0 ->
+ * chunk += data, gather == 1 -> chunk[mask] = data[mask] (mask NULL = all);
+ * optr_ring_finish: out = float32(buf / nodes). */
+int optr_ring_cast(const double* chunk, int64_t n, float* out, void* stream);
+int optr_ring_step(double* chunk, const float* data, const uint8_t* mask, int64_t n, int gather, void* stream);
+int optr_ring_finish(const double* buf, int nodes, int64_t len, float* out, void* stream);
+
+/* Datagram framing on the GPU (wire.py:36-85,176-208).  Packet k of a shard
+ * of n_entries float32 values sits at packets + k*stride (stride >=
+ * 9 + max_payload): a 9-byte big-endian header (bucket_id u16, byte_offset
+ * u32 = base_byte_offset + k*max_payload, timeout_share u8, flags u8 = last-
+ * percentile tag | incast << 1, reserved 0) then the payload bytes.  The
+ * final max(1, total/100) packets carry the tag.  OPTR_EINVAL for the
+ * reference's HeaderError ranges; max_payload must be a multiple of 4.
+ * optr_depacketize zero-fills shard_out / mask_out, then lands every
+ * delivered packet (delivered[k] != 0, or all when NULL) at its header's
+ * offset; packets with a bad header (reserved byte, bucket id, offset) are
+ * skipped and counted in *errors (device u32). */
+int optr_packetize(const float* shard, int64_t n_entries, int bucket_id, uint32_t base_byte_offset,
+                   int max_payload, int timeout_share, int incast, uint8_t* packets, int64_t stride,
+                   void* stream);
+int optr_depacketize(const uint8_t* packets, int64_t n_packets, int64_t stride, const uint8_t* delivered,
+                     int bucket_id, uint32_t base_byte_offset, int max_payload, float* shard_out,
+                     uint8_t* mask_out, int64_t n_entries, unsigned int* errors, void* stream);
 
 /* ------------------------------------------- TAR+RHT, n workers on one GPU */
 /* Workspace bytes for optr_tar_local. */

@@ -58,6 +58,11 @@ SIGNATURES = {
     "optr_version": (ctypes.c_char_p, []),
     "optr_coin_packets": (_int, [_u64, _int, _u64, _i64, ctypes.c_double, _vp]),
     "optr_mean_received": (_int, [_vp, _vp, _vp, _int, _int, _i64, _vp, _vp]),
+    "optr_ring_cast": (_int, [_vp, _i64, _vp, _vp]),
+    "optr_ring_step": (_int, [_vp, _vp, _vp, _i64, _int, _vp]),
+    "optr_ring_finish": (_int, [_vp, _int, _i64, _vp, _vp]),
+    "optr_packetize": (_int, [_vp, _i64, _int, ctypes.c_uint32, _int, _int, _int, _vp, _i64, _vp]),
+    "optr_depacketize": (_int, [_vp, _i64, _i64, _vp, _int, ctypes.c_uint32, _int, _vp, _vp, _i64, _vp, _vp]),
     "optr_rht_signs": (_int, [_vp, _i64, _u64, _vp]),
     "optr_fwht": (_int, [_vp, _i64, _vp]),
     "optr_rht_encode": (_int, [_vp, _int, _i64, _vp, _i64, _u64, _vp]),

@@ -1,11 +1,14 @@
 """Transpose AllReduce with the RHT codec fused in, on the GPU.
 
-Drop-in for the TAR part of ``ubar.collectives`` / ``ubar.schedule`` /
-``ubar.wire`` (``/root/reference/pkg/src/ubar/``).  The reference expresses a
-collective as a sans-IO generator driven by a channel; on a B200 the channel
-is HBM (n workers on one GPU, ``tar_allreduce_local``) or NVLink (one worker
-per GPU, ``paper_2310_06993_b200.dist``), and the lossy transport is replaced
-by seeded per-packet drop masks (``MaskSpec``) that reproduce the reference's
+Drop-in for ``ubar.collectives`` / ``ubar.schedule`` / ``ubar.wire``
+(``/root/reference/pkg/src/ubar/``).  The reference expresses a collective
+as a sans-IO generator driven by a channel: those generators (tar, tar2d,
+ring, ps) and drivers (``run_lossless``, ``run_datagram``) are re-exported
+from ``protocol`` with device buffers and liboptr arithmetic.  The gradient
+hot path batches a whole generation instead: the channel is HBM (n workers
+on one GPU, ``tar_allreduce_local``) or NVLink (one worker per GPU,
+``paper_2310_06993_b200.dist``), and the lossy transport is replaced by
+seeded per-packet drop masks (``MaskSpec``) that reproduce the reference's
 masks bit-exactly.
 
 Host-side index math (shards, owners, schedule) is plain Python here and is
@@ -21,6 +24,24 @@ import numpy as np
 
 from . import _lib
 from ._lib import check, lib
+from .protocol import (  # noqa: F401  the reference's sans-IO protocol (collectives.py:25-401)
+    AllReduceResult,
+    AwaitStage,
+    CollectiveDeadlock,
+    NodeStats,
+    OpenStage,
+    RoundEnd,
+    SendShard,
+    StageResult,
+    _mean_received,
+    ps_allreduce,
+    ring_allreduce,
+    run_datagram,
+    run_lossless,
+    tar2d_allreduce,
+    tar_allreduce,
+)
+from .schedule import PairSchedule, Topology, build_schedule, owned_shard, shard_owner  # noqa: F401
 
 ENTRY_BYTES = 4  # wire.py:23
 MAX_PAYLOAD = 1400  # wire.py:22
@@ -41,30 +62,6 @@ def shard_offsets(length: int, n: int) -> list[int]:
     for ln in shard_lengths(length, n):
         offs.append(offs[-1] + ln)
     return offs
-
-
-def shard_owner(shard_index: int, r: int, n: int) -> int:
-    """schedule.py:42-44."""
-    return (shard_index + r) % n
-
-
-def owned_shard(node: int, r: int, n: int) -> int:
-    """schedule.py:47-49."""
-    return (node - r) % n
-
-
-def build_schedule(n: int, incast: int) -> tuple:
-    """schedule.py:67-78: round k sends i -> i+kI+1 .. i+kI+I (mod n)."""
-    if n < 2:
-        raise ValueError("need at least 2 nodes")
-    if not 1 <= incast <= n - 1:
-        raise ValueError(f"incast factor must be in [1, {n - 1}], got {incast}")
-    n_rounds = -(-(n - 1) // incast)
-    rounds = []
-    for k in range(n_rounds):
-        offsets = range(k * incast + 1, min(k * incast + incast, n - 1) + 1)
-        rounds.append({i: tuple((i + o) % n for o in offsets) for i in range(n)})
-    return tuple(rounds)
 
 
 def n_packets(n_entries: int, epp: int) -> int:
@@ -187,14 +184,6 @@ class MaskSpec:
                                    self.bitmap.data_ptr() if self.bitmap is not None else None, offs)
 
 
-@dataclass
-class AllReduceResult:
-    """collectives.py:65-74: a node's entries plus which arrived."""
-
-    entries: object
-    received: object
-
-
 # -------------------------------------------------------- n workers, 1 GPU
 _WS: dict = {}
 _SLOT: dict = {}
@@ -309,15 +298,14 @@ def tar_allreduce_local(buckets: list, *, rotation: int = 0, ht: bool = False, j
     return out, counts, got
 
 
-def tar_allreduce(entries: list, *, r: int = 0, masks: MaskSpec | None = None) -> list:
-    """The reference's ``tar_allreduce`` (collectives.py:97-150) for all n
-    nodes at once, on their already-encoded vectors (RHT is the runner's job,
-    runner.py:219-258): stage-1 masked fp64 mean at each shard owner, stage-2
-    assembly.  ``entries``: n equal-length CUDA float32 tensors.  Returns one
-    ``AllReduceResult(entries, received)`` per node, like the generator's
-    return value; the generator's channel protocol itself (SendShard /
-    OpenStage / AwaitStage) has no device counterpart -- ``masks`` replaces
-    the channel.  Bit-exact with the reference."""
+def tar_allreduce_batch(entries: list, *, r: int = 0, masks: MaskSpec | None = None) -> list:
+    """``tar_allreduce`` (collectives.py:97-150) for all n nodes at once in
+    one batched launch sequence, on their already-encoded vectors (RHT is the
+    runner's job, runner.py:219-258): stage-1 masked fp64 mean at each shard
+    owner, stage-2 assembly.  ``entries``: n equal-length CUDA float32
+    tensors; ``masks`` replaces the channel.  Returns one
+    ``AllReduceResult(entries, received)`` per node, bit-exact with the
+    reference (the generator form is ``tar_allreduce``)."""
     outs, _counts, got = tar_allreduce_local(entries, rotation=r, ht=False, masks=masks, want_received=True)
     return [AllReduceResult(entries=o, received=g) for o, g in zip(outs, got)]
 

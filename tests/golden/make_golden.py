@@ -21,6 +21,9 @@ reference itself produces on fixed seeds:
                       captured at consumption time (SURVEY finding 2/5) and
                       stored per packet, next to the reference results
                       (runner.py:211-276).
+* ``wire.npz``     -- packet byte streams of wire.iter_packets + encode_header
+                      (wire.py:36-85,183-208) over awkward shard lengths,
+                      header fields and payload sizes.
 * ``sim_gpt2xl.npz`` -- the same capture at the GPT-2 XL bucket shape
                       (BASELINE configs[3]: n=8, 13,107,200 entries, bf16-valued
                       inputs, 5% drops, adaptive timeouts): packed packet masks
@@ -307,6 +310,25 @@ def gen_sim():
                         gens=np.array([c[6] for c in configs]), **rec)
 
 
+def gen_wire():
+    from ubar.wire import encode_header, iter_packets
+
+    cases = [
+        # entries, bucket_id, base_offset, max_payload, timeout_share, incast
+        (0, 1, 0, 1400, 0, 0), (1, 2, 0, 1400, 0, 0), (349, 7, 4, 1400, 3, 1), (350, 65535, 0, 1400, 255, 127),
+        (351, 0, 1400, 1400, 17, 5), (1000, 300, 12, 64, 9, 0), (35_000, 42, 0, 1400, 128, 3),
+        (100_001, 9, 4_000_000, 1400, 1, 2),
+    ]
+    rec = {}
+    for i, (ne, bid, base, mp, ts, inc) in enumerate(cases):
+        x = np.random.default_rng(700 + i).standard_normal(ne).astype(np.float32)
+        pk = [encode_header(h) + p for h, p in iter_packets(bid, x.tobytes(), base, mp, ts, inc)]
+        rec[f"x_{i}"] = x
+        rec[f"lens_{i}"] = np.array([len(p) for p in pk], dtype=np.int64)
+        rec[f"bytes_{i}"] = np.frombuffer(b"".join(pk), dtype=np.uint8)
+    np.savez_compressed(OUT / "wire.npz", cases=np.array(cases, dtype=np.int64), **rec)
+
+
 def bf16_round(x: np.ndarray) -> np.ndarray:
     """float32 -> nearest bfloat16 (ties to even), kept as float32 (torch's
     .to(torch.bfloat16) on finite values)."""
@@ -355,7 +377,7 @@ def gen_sim_large():
 
 
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["rng", "codec", "lossless", "datagram", "sim", "sim_large"]
+    which = sys.argv[1:] or ["rng", "codec", "lossless", "datagram", "sim", "sim_large", "wire"]
     for w in which:
         globals()[f"gen_{w}"]()
         print("wrote", w)

@@ -340,7 +340,7 @@ def test_tar_allreduce_reference_signature(dev):
     bufs = O.make_buckets(4, n, L)
     masks = O.datagram_masks(8, L, n, r, 0.05)
     want = O.tar_masked(bufs, r, masks, 350)
-    res = P.collectives.tar_allreduce([cu(b, dev) for b in bufs], r=r, masks=MaskSpec.coin(8, 0.05))
+    res = P.collectives.tar_allreduce_batch([cu(b, dev) for b in bufs], r=r, masks=MaskSpec.coin(8, 0.05))
     for node in range(n):
         np.testing.assert_array_equal(res[node].entries.cpu().numpy(), want[node][0])
         np.testing.assert_array_equal(res[node].received.cpu().numpy(), want[node][1])

@@ -100,7 +100,7 @@ def test_index_helpers_match_oracle():
             assert [owned_shard(i, r, n) for i in range(n)] == [O.owned_shard(i, r, n) for i in range(n)]
         for inc in range(1, n):
             sched = build_schedule(n, inc)
-            order = [d for rnd in sched for d in rnd[0]]
+            order = [d for rnd in sched.rounds for d in rnd[0]]
             assert order == O.send_order(0, n)
 
 
