@@ -231,8 +231,37 @@ int optr_tar_async(optr_comm c, const void* x, void* out, int64_t L, int dtype_i
 /* Make `stream` wait for every optr_tar_async call issued so far. */
 int optr_comm_join(optr_comm c, void* stream);
 
+/* Per-call transport report (device memory, written by the call): the
+ * numbers StageOutcome / NodeStats carry (simdriver.py:26-45,328-341). */
+typedef struct {
+  uint64_t received[2];  /* entries this rank received, stage 1 / stage 2   */
+  uint64_t cut[2];       /* entries the mask model delivered but a stage
+                            deadline cut off (counted as lost)            */
+  uint64_t t_open_ns;    /* device global timer: this rank's stage 1 opened */
+  uint64_t t_stage1_ns;  /* its last stage-1 (owner) unit was published     */
+  uint64_t t_stage2_ns;  /* its last stage-2 tile landed                    */
+} optr_tar_stats;
+
+/* optr_tar with OptiReduce's bounded stage 1 (UBT hard bound t_B,
+ * transport.py:102-108, simdriver.py:323-326 / datagram.py:165-207): on the
+ * fused plan an owner waits for a peer's encoded tile at most
+ * stage1_deadline_ns after it opened the stage, then aggregates without it;
+ * the cut entries count as lost (stats->cut[0]) and cut_units (optional,
+ * device u32 per stage-1 unit of 2^T/UPT entries) gets each unit's bitmask of
+ * cut peers.  0 = unbounded; the barrier path (other shapes) never cuts.
+ * stats: optional device optr_tar_stats.  async: as optr_tar_async. */
+int optr_tar_bounded(optr_comm c, const void* x, void* out, int64_t L, int dtype_in, int dtype_out,
+                     uint64_t job_seed, uint64_t bucket_id, uint64_t generation, int rotation, int ht,
+                     const optr_mask_spec* masks, uint64_t stage1_deadline_ns, optr_tar_stats* stats,
+                     uint32_t* cut_units, int async, void* stream);
+
 /* Device-side all-rank barrier on `stream` (flags over NVLink). */
 int optr_comm_barrier(optr_comm c, void* stream);
+
+/* Entries per stage-1 unit of the fused plan for (dim, n) -- the granularity
+ * of optr_tar_bounded's deadline cut-offs; 0 when the shape takes the
+ * barrier path (no cut-offs). */
+int64_t optr_fused_unit_entries(int64_t dim, int n);
 
 /* --------------------------------------------------------- instrumentation */
 /* Kernel classes timed when timing is enabled. */

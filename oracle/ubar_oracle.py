@@ -248,13 +248,20 @@ def mean_received(rank: int, own: np.ndarray, data: dict, mask: dict, n: int) ->
     return out.astype(np.float32)
 
 
-def tar_masked(wire: list, r: int, masks: dict, epp: int) -> list:
+def tar_masked(wire: list, r: int, masks: dict, epp: int, entry_masks: dict | None = None) -> list:
     """collectives.py:97-150 over a channel that delivers exactly the packets
     ``masks`` marks (zero-filled misses, simdriver.py:245-247,270-271).
 
     ``wire``: n float32 vectors of equal length.  Returns per node
     ``(entries float32, received bool)`` (AllReduceResult, :65-74).
+    ``entry_masks``: optional {(stage, dst, src): bool[shard len]} replacing
+    the packet expansion (e.g. a stage-1 deadline cut mid-packet).
     """
+    entry_masks = entry_masks or {}
+
+    def emask(key, ln):
+        return entry_masks[key] if key in entry_masks else expand_packets(masks[key], ln, epp)
+
     n = len(wire)
     wire = [np.asarray(w, dtype=np.float32) for w in wire]
     length = len(wire[0])
@@ -272,7 +279,7 @@ def tar_masked(wire: list, r: int, masks: dict, epp: int) -> list:
         for src in range(n):
             if src == dst:
                 continue
-            e = expand_packets(masks[(1, dst, src)], ln, epp)
+            e = emask((1, dst, src), ln)
             data[src] = np.where(e, shard(src, j), np.float32(0.0)).astype(np.float32)
             mk[src] = e
         s_r[dst] = mean_received(dst, shard(dst, j).astype(np.float64), data, mk, n)
@@ -290,7 +297,7 @@ def tar_masked(wire: list, r: int, masks: dict, epp: int) -> list:
                 continue
             j = owned_shard(src, r, n)
             ln = offs[j + 1] - offs[j]
-            e = expand_packets(masks[(2, dst, src)], ln, epp)
+            e = emask((2, dst, src), ln)
             out[offs[j]:offs[j + 1]] = np.where(e, s_r[src], np.float32(0.0))
             got[offs[j]:offs[j + 1]] = e
         results.append((out, got))
@@ -300,7 +307,8 @@ def tar_masked(wire: list, r: int, masks: dict, epp: int) -> list:
 def run_generation(buckets: list, job_seed: int, generation: int, ht: bool,
                    masks: dict | None = None, r: int | None = None,
                    epp: int = MAX_PAYLOAD // ENTRY_BYTES, threads: int = 1,
-                   return_wire: bool = False, bucket_id: int | None = None):
+                   return_wire: bool = False, bucket_id: int | None = None,
+                   entry_masks: dict | None = None):
     """runner.py:211-276 hot-path composition with the channel replaced by
     ``masks``: ht -> RhtContext(derive_seed(seed, g%65536, g)) (:217-222),
     encode every node and cast float32 (:223-225), TAR (:230-246), decode
@@ -328,7 +336,7 @@ def run_generation(buckets: list, job_seed: int, generation: int, ht: bool,
             wire = [np.asarray(b, dtype=np.float32) for b in buckets]
         if masks is None:
             masks = full_masks(dim, n, r, epp)
-        tar = tar_masked(wire, r, masks, epp)
+        tar = tar_masked(wire, r, masks, epp, entry_masks)
         if ht:
             def dec(res):
                 entries, got = res

@@ -89,6 +89,9 @@ SIGNATURES = {
     "optr_tar_async": (_int, [_vp, _vp, _vp, _i64, _int, _int, _u64, _u64, _u64, _int, _int,
                               ctypes.POINTER(optr_mask_spec), _vp, _vp]),
     "optr_comm_join": (_int, [_vp, _vp]),
+    "optr_tar_bounded": (_int, [_vp, _vp, _vp, _i64, _int, _int, _u64, _u64, _u64, _int, _int,
+                                ctypes.POINTER(optr_mask_spec), _u64, _vp, _vp, _int, _vp]),
+    "optr_fused_unit_entries": (_i64, [_i64, _int]),
     "optr_timing_enable": (_int, [_int]),
     "optr_timing_collect": (_int, [ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_i64), ctypes.POINTER(_i64)]),
     "optr_launch_count": (_i64, []),

@@ -1433,7 +1433,8 @@ int optr_comm_join(optr_comm c, void* stream) {
 
 static int tar_enqueue(optr_comm c, const void* x, void* out, int64_t L, int dtype_in, int dtype_out,
                        uint64_t job_seed, uint64_t bucket_id, uint64_t generation, int rotation, int ht,
-                       const optr_mask_spec* masks, uint64_t* received_out, void* stream, bool async);
+                       const optr_mask_spec* masks, uint64_t* received_out, void* stream, bool async,
+                       uint64_t deadline_ns = 0, optr_tar_stats* stats = nullptr, uint32_t* cut_units = nullptr);
 
 int optr_tar(optr_comm c, const void* x, void* out, int64_t L, int dtype_in, int dtype_out, uint64_t job_seed,
              uint64_t bucket_id, uint64_t generation, int rotation, int ht, const optr_mask_spec* masks,
@@ -1447,6 +1448,14 @@ int optr_tar_async(optr_comm c, const void* x, void* out, int64_t L, int dtype_i
                    const optr_mask_spec* masks, uint64_t* received_out, void* stream) {
   return tar_enqueue(c, x, out, L, dtype_in, dtype_out, job_seed, bucket_id, generation, rotation, ht, masks,
                      received_out, stream, true);
+}
+
+int optr_tar_bounded(optr_comm c, const void* x, void* out, int64_t L, int dtype_in, int dtype_out,
+                     uint64_t job_seed, uint64_t bucket_id, uint64_t generation, int rotation, int ht,
+                     const optr_mask_spec* masks, uint64_t stage1_deadline_ns, optr_tar_stats* stats,
+                     uint32_t* cut_units, int async, void* stream) {
+  return tar_enqueue(c, x, out, L, dtype_in, dtype_out, job_seed, bucket_id, generation, rotation, ht, masks,
+                     nullptr, stream, async != 0, stage1_deadline_ns, stats, cut_units);
 }
 
 }  // extern "C"
@@ -1473,6 +1482,30 @@ bool fused_enabled() {
     v = (e && e[0] == '0') ? 0 : 1;
   }
   return v == 1;
+}
+
+// optr_tar_stats bookkeeping (stats words: ST_* in tma.cuh)
+__global__ void stats_init_kernel(unsigned long long* s) {
+  for (int i = 0; i < 7; ++i) s[i] = i == ST_OPEN ? ~0ULL : 0ULL;
+}
+__global__ void stats_stamp_kernel(unsigned long long* s, int field) {
+  const unsigned long long t = (unsigned long long)globaltimer_ns();
+  if (field == ST_OPEN) atomicMin(s + field, t);
+  else atomicMax(s + field, t);
+}
+__global__ void stats_finish_kernel(unsigned long long* s, const unsigned long long* counts, int me, int n) {
+  s[ST_RECV0] = counts[me] - s[ST_CUT0];
+  s[ST_RECV1] = counts[n + me] - s[ST_CUT1];
+}
+int stats_open(optr_tar_stats* s, cudaStream_t st) {
+  stats_init_kernel<<<1, 1, 0, st>>>((unsigned long long*)s);
+  CK(cudaGetLastError());
+  return OPTR_OK;
+}
+int stats_stamp(optr_tar_stats* s, int field, cudaStream_t st) {
+  stats_stamp_kernel<<<1, 1, 0, st>>>((unsigned long long*)s, field);
+  CK(cudaGetLastError());
+  return OPTR_OK;
 }
 
 template <int T, int NW, int S, int NG>
@@ -1526,7 +1559,8 @@ extern "C" {
 
 static int tar_enqueue(optr_comm c, const void* x, void* out, int64_t L, int dtype_in, int dtype_out,
                        uint64_t job_seed, uint64_t bucket_id, uint64_t generation, int rotation, int ht,
-                       const optr_mask_spec* masks, uint64_t* received_out, void* stream, bool async) {
+                       const optr_mask_spec* masks, uint64_t* received_out, void* stream, bool async,
+                       uint64_t deadline_ns, optr_tar_stats* stats, uint32_t* cut_units) {
   if (!c) return OPTR_EINVAL;
   int n = c->n;
   int rc = check_common(n, L, dtype_in, dtype_out, masks);
@@ -1669,6 +1703,11 @@ static int tar_enqueue(optr_comm c, const void* x, void* out, int64_t L, int dty
     f.trace = (uint4*)g_fused_trace;
     f.trace_cap = g_fused_trace_cap;
     f.watchdog_ns = watchdog_ns();
+    f.deadline_ns = deadline_ns;
+    f.stats = (unsigned long long*)stats;
+    f.counts = counts;
+    f.cut_units = cut_units;
+    if (stats && (rc = stats_open(stats, st))) return rc;
     if ((rc = launch_fused(Tc, ae, ad, se, sd, f, st))) return rc < 0 ? OPTR_ECUDA : rc;
     CK(cudaEventRecord(c->fused_done[par], st));
     c->fused_recorded[par] = true;
@@ -1722,6 +1761,7 @@ static int tar_enqueue(optr_comm c, const void* x, void* out, int64_t L, int dty
     CK(cudaGetLastError());
   }
   if ((rc = comm_barrier(c, par, st))) return rc;
+  if (stats && ((rc = stats_open(stats, st)) || (rc = stats_stamp(stats, ST_OPEN, st)))) return rc;
 
   // stage 1: pull my shard from every peer over NVLink, masked mean
   AggArgs ag;
@@ -1746,6 +1786,7 @@ static int tar_enqueue(optr_comm c, const void* x, void* out, int64_t L, int dty
   int64_t smax = sh.base + (sh.extra ? 1 : 0);
   if ((rc = launch_aggregate(ag, 1, smax, st))) return rc;
   if ((rc = comm_barrier(c, par, st))) return rc;
+  if (stats && (rc = stats_stamp(stats, ST_STAGE1, st))) return rc;
 
   // stage 2 receive fused into the first decode pass: from the local G
   // (push) or pulled from every owner's aggregate over NVLink
@@ -1793,10 +1834,34 @@ static int tar_enqueue(optr_comm c, const void* x, void* out, int64_t L, int dty
     CK(cudaMemcpyAsync(received_out, counts + me, 8, cudaMemcpyDeviceToDevice, st));
     CK(cudaMemcpyAsync(received_out + 1, counts + n + me, 8, cudaMemcpyDeviceToDevice, st));
   }
+  if (stats) {  // no deadline on this path: received = the mask-model counts
+    if ((rc = stats_stamp(stats, ST_STAGE2, st))) return rc;
+    stats_finish_kernel<<<1, 1, 0, st>>>((unsigned long long*)stats, counts, me, n);
+    CK(cudaGetLastError());
+  }
   CK(cudaEventRecord(c->done[par], st));
   c->done_recorded[par] = true;
   if (!async) CK(cudaStreamWaitEvent(caller, c->done[par], 0));
   return OPTR_OK;
+}
+
+// Entries per stage-1 unit of the fused kernel (the granularity of deadline
+// cut-offs, optr_tar_bounded's cut_units); 0 when (dim, n) takes the barrier
+// path.  Mirrors tma_fused_kernel's constants.
+int64_t optr_fused_unit_entries(int64_t dim, int n) {
+  if (!is_pow2(dim) || (n != 2 && n != 4 && n != 8)) return 0;
+  PassGeom ps[3];
+  const int nlog = log2_exact(dim);
+  if (plan_passes(nlog, ps, true) != 2 || ps[0].cb != 0) return 0;
+  const int T = ps[0].ks;
+  if ((T != 13 && T != 14) || ps[1].cb != 3 || (ps[1].ks + 3 != 13 && ps[1].ks + 3 != 14)) return 0;
+  if ((dim / n) < (1LL << T)) return 0;
+  const int ch = agg_chunk(n);
+  int sa = kAggBytes / (n * ch * 4);
+  if (sa > 16) sa = 16;
+  const int cpt = (1 << T) / ch;
+  const int upt = cpt / sa >= 4 ? 4 : (cpt / sa >= 2 ? 2 : 1);
+  return (1LL << T) / upt;
 }
 
 // ------------------------------------------------------ instrumentation

@@ -843,7 +843,17 @@ struct FusedArgs {
   uint4* trace;   // debug (optr_debug_trace): per CTA [cap/2 E/D jobs | cap/2 A tiles]
   int trace_cap;
   uint64_t watchdog_ns;
+  // bounded stage 1 (UBT hard bound, transport.py:102-108 / simdriver.py:
+  // 323-326): an owner waits for a peer's encoded tile until deadline_ns
+  // after its CTA started, then aggregates without it (0 = unbounded)
+  uint64_t deadline_ns;
+  unsigned long long* stats;         // optr_tar_stats (device) or null
+  const unsigned long long* counts;  // this rank's [2][n] mask-model received counts
+  uint32_t* cut_units;               // optional [units]: peers cut from each stage-1 unit
 };
+
+// optr_tar_stats field offsets (u64 words, include/optr.h)
+enum { ST_RECV0 = 0, ST_RECV1 = 1, ST_CUT0 = 2, ST_CUT1 = 3, ST_OPEN = 4, ST_STAGE1 = 5, ST_STAGE2 = 6 };
 
 __device__ __forceinline__ unsigned int ld_acquire_sys(const unsigned int* p) {
   unsigned int v;
@@ -928,10 +938,13 @@ __global__ void __launch_bounds__(NG * (1 << (T - 5)) + kAggThreads)
   int* const slot_kind = reinterpret_cast<int*>(abar + SA);                // [NG][4]
   int64_t* const slot_tile = reinterpret_cast<int64_t*>(slot_kind + NG * 4);  // [NG][4]
   int* const aslot = reinterpret_cast<int*>(slot_tile + NG * 4);  // A ring: (unit << 8 | chunk), -1 end
+  uint32_t* const apres = reinterpret_cast<uint32_t*>(aslot + SA);  // A ring: ranks whose data the stage holds
   const int tid = threadIdx.x;
   constexpr int n = NW;
   const int me = f.me;
   const int64_t ns = f.ns;
+  const uint64_t t_cta0 = globaltimer_ns();
+  if (f.stats && tid == 0) atomicMin(f.stats + ST_OPEN, (unsigned long long)t_cta0);
 
   if (tid == 0) {
     for (int s = 0; s < NG * kStages; ++s) mbar_init(&full[s], 1);
@@ -1017,7 +1030,10 @@ __global__ void __launch_bounds__(NG * (1 << (T - 5)) + kAggThreads)
       const int kind = gkind[s];
       const int64_t t = gtile[s];
       if (kind == FJ_END) {
-        if (ltid == 0) release_e();
+        if (ltid == 0) {
+          release_e();
+          if (f.stats) atomicMax(f.stats + ST_STAGE2, (unsigned long long)globaltimer_ns());
+        }
         break;
       }
       if (ltid == 0 && kind != FJ_E) release_e();
@@ -1073,6 +1089,26 @@ __global__ void __launch_bounds__(NG * (1 << (T - 5)) + kAggThreads)
     uint4* const tra = f.trace ? f.trace + (size_t)blockIdx.x * f.trace_cap + f.trace_cap / 2 : nullptr;
     int ntr = 0;
     uint32_t t_claim = 0, t_ready = 0;
+    constexpr uint32_t kAll = (1u << NW) - 1u;
+    uint32_t cur_present = kAll;  // ranks whose encoded unit `cur` is aggregated
+    unsigned long long cut = 0;   // consumer: mask-delivered entries a deadline cut
+    // wait for every rank's encoded tile t; past the deadline a peer that is
+    // still missing is cut from the unit (never this rank's own tile)
+    auto wait_present = [&](int64_t t) {
+      uint32_t pres = 0;
+      for (int q = 0; q < n; ++q) {
+        const unsigned int* p = f.eflag_in + q * f.estride + t;
+        if (q == me || f.deadline_ns == 0) {
+          spin_ge_sys(p, f.epoch, f.watchdog_ns);
+          pres |= 1u << q;
+          continue;
+        }
+        const uint64_t end = t_cta0 + f.deadline_ns;
+        while (ld_relaxed_sys(p) < f.epoch && globaltimer_ns() < end) __nanosleep(64);
+        if (ld_relaxed_sys(p) >= f.epoch) pres |= 1u << q;
+      }
+      return pres;
+    };
     auto tile_ready = [&](int64_t u) {
       const int64_t t = (int64_t)f.own * ns + u / UPT;
       unsigned int v[NW];
@@ -1085,12 +1121,17 @@ __global__ void __launch_bounds__(NG * (1 << (T - 5)) + kAggThreads)
     };
     auto issue_chunk = [&](int s) {
       aslot[s] = (int)((cur << 8) | nxt);
+      apres[s] = cur_present;
       const uint32_t bytes = kAggCh * sizeof(float);
       const int64_t e = ((cur / UPT) << T) + ((int64_t)(cur % UPT) * kCpu + nxt) * kAggCh;  // inside my shard
-      mbar_expect_tx(&abar[s], bytes * n);
+      mbar_expect_tx(&abar[s], bytes * (uint32_t)__popc(cur_present));
       for (int i = 0; i < n; ++i)
-        bulk_load(abuf + ((size_t)s * n + i) * kAggCh, f.Y[i] + soff + e, bytes, &abar[s]);
+        if ((cur_present >> i) & 1u) bulk_load(abuf + ((size_t)s * n + i) * kAggCh, f.Y[i] + soff + e, bytes, &abar[s]);
       ++nxt;
+    };
+    auto decide = [&](uint32_t pres) {  // unit `cur`'s contributors are fixed
+      cur_present = pres;
+      if (f.cut_units && nxt == 0) f.cut_units[cur] = kAll & ~pres;
     };
     auto issue_next = [&](int s) {
       if (pend_first >= 0) {  // the queued unit takes this stage too (SA <= kCpu)
@@ -1110,6 +1151,7 @@ __global__ void __launch_bounds__(NG * (1 << (T - 5)) + kAggThreads)
             pend_count = 1;
             return;
           }
+          decide(kAll);
           if (tra) t_ready = (uint32_t)globaltimer_ns();
           fence_acq_rel_sys();  // acquire
           fence_proxy_async_global();
@@ -1130,7 +1172,7 @@ __global__ void __launch_bounds__(NG * (1 << (T - 5)) + kAggThreads)
       const int s = k % SA;
       if (ta == 0 && s == pend_first) {
         const int64_t t = (int64_t)f.own * ns + cur / UPT;
-        for (int q = 0; q < n; ++q) spin_ge_sys(f.eflag_in + q * f.estride + t, f.epoch, f.watchdog_ns);
+        decide(wait_present(t));
         if (tra) t_ready = (uint32_t)globaltimer_ns();
         fence_acq_rel_sys();  // acquire
         fence_proxy_async_global();
@@ -1144,6 +1186,7 @@ __global__ void __launch_bounds__(NG * (1 << (T - 5)) + kAggThreads)
       if (code < 0) break;
       const int64_t un = code >> 8;  // unit
       const int chunk = code & 255;  // chunk inside the unit
+      const uint32_t pres = apres[s];
 #pragma unroll
       for (int v = 0; v < kAggCh / (4 * kAggThreads); ++v) {
         const int off = 4 * (ta + v * kAggThreads);
@@ -1154,7 +1197,11 @@ __global__ void __launch_bounds__(NG * (1 << (T - 5)) + kAggThreads)
 #pragma unroll
         for (int i = 0; i < n; ++i) {
           const float4 x4 = *reinterpret_cast<const float4*>(src + (size_t)i * kAggCh);
-          const uint32_t kk = i == me ? 0xFu : keep4(f.m.row(0, me, i), (uint32_t)e, f.m);
+          uint32_t kk = i == me ? 0xFu : keep4(f.m.row(0, me, i), (uint32_t)e, f.m);
+          if (!((pres >> i) & 1u)) {  // cut by the stage-1 deadline: a miss
+            cut += (unsigned long long)__popc(kk);
+            kk = 0u;
+          }
           acc[0] += (kk & 1u) ? (double)x4.x : 0.0;  // misses add +0.0 like the reference
           acc[1] += (kk & 2u) ? (double)x4.y : 0.0;
           acc[2] += (kk & 4u) ? (double)x4.z : 0.0;
@@ -1181,6 +1228,10 @@ __global__ void __launch_bounds__(NG * (1 << (T - 5)) + kAggThreads)
         issue_next(s);
       }
     }
+    if (f.stats) {
+      if (cut) atomicAdd(f.stats + ST_CUT0, cut);
+      if (ta == 0) atomicMax(f.stats + ST_STAGE1, (unsigned long long)globaltimer_ns());
+    }
   }
   __syncthreads();
   if (tid == 0) {
@@ -1190,6 +1241,10 @@ __global__ void __launch_bounds__(NG * (1 << (T - 5)) + kAggThreads)
       f.ctr[0] = 0;
       f.ctr[1] = 0;
       f.ctr[2] = 0;
+      if (f.stats) {  // last CTA out: received = mask-model counts - deadline cuts
+        f.stats[ST_RECV0] = f.counts[me] - f.stats[ST_CUT0];
+        f.stats[ST_RECV1] = f.counts[n + me] - f.stats[ST_CUT1];
+      }
       __threadfence();
     }
   }

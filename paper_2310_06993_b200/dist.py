@@ -85,14 +85,22 @@ class TarCommunicator:
 
     def allreduce(self, x, out, *, rotation: int, ht: bool = True, job_seed: int = 0,
                   generation: int = 0, bucket_id: int | None = None, masks: MaskSpec | None = None,
-                  received=None, stream=None, async_op: bool = False):
+                  received=None, stream=None, async_op: bool = False, deadline_ns: int = 0,
+                  stats=None, cut_units=None):
         """This rank's part of one TAR(+RHT) generation.  ``x``/``out`` are
         this rank's CUDA buffers (fp32/bf16).  ``received``: optional CUDA
         int64[2] for (stage-1, stage-2) received entries.
 
         ``async_op=True`` lets consecutive buckets overlap (optr_tar_async):
         the stream does not wait for ``out`` until ``join()``; keep ``x`` and
-        ``out`` untouched until then."""
+        ``out`` untouched until then.
+
+        ``deadline_ns`` bounds stage 1 (optr_tar_bounded): past it an owner
+        aggregates without the peers whose encoded tiles are still missing.
+        ``stats``: optional CUDA int64[7] optr_tar_stats (received[2],
+        cut[2], t_open, t_stage1, t_stage2 in device-timer ns);
+        ``cut_units``: optional CUDA int32 tensor, one word per stage-1 unit
+        (bitmask of the peers cut from it)."""
         import torch
 
         if self._h is None:
@@ -102,11 +110,21 @@ class TarCommunicator:
         masks = masks or MaskSpec.none(self.epp * 4)
         spec = masks.to_c()
         st = stream if stream is not None else torch.cuda.current_stream(self.device)
+        bid = int(generation % 65536 if bucket_id is None else bucket_id)
+        if deadline_ns or stats is not None or cut_units is not None:
+            if received is not None:
+                raise ValueError("pass stats (received counts included) with a deadline")
+            check(lib().optr_tar_bounded(self._h, x.data_ptr(), out.data_ptr(), len(x), _dtype_code(x),
+                                         _dtype_code(out), int(job_seed), bid, int(generation), int(rotation),
+                                         int(bool(ht)), ctypes.byref(spec), int(deadline_ns),
+                                         stats.data_ptr() if stats is not None else None,
+                                         cut_units.data_ptr() if cut_units is not None else None,
+                                         int(bool(async_op)), st.cuda_stream), "tar_bounded")
+            return out
         fn = lib().optr_tar_async if async_op else lib().optr_tar
         check(fn(self._h, x.data_ptr(), out.data_ptr(), len(x), _dtype_code(x), _dtype_code(out),
-                             int(job_seed), int(generation % 65536 if bucket_id is None else bucket_id),
-                             int(generation), int(rotation), int(bool(ht)), ctypes.byref(spec),
-                             received.data_ptr() if received is not None else None, st.cuda_stream),
+                 int(job_seed), bid, int(generation), int(rotation), int(bool(ht)), ctypes.byref(spec),
+                 received.data_ptr() if received is not None else None, st.cuda_stream),
               "tar")
         return out
 

@@ -376,3 +376,103 @@ def test_fused_protocol_async_stress():
                 f = np.load(os.path.join(d, f"async_b{b}_r{r}.npy")).astype(np.float64)
                 c = np.load(os.path.join(d, f"barrier_b{b}_r{r}.npy")).astype(np.float64)
                 assert np.linalg.norm(f - c) / np.linalg.norm(c) < 1e-5, (b, r)
+
+
+# ------------------------------------------- bounded stage 1 (UBT hard bound)
+def _bounded_worker(rank, world, port, outdir):
+    import torch.distributed as dist
+
+    from paper_2310_06993_b200 import _lib
+    from paper_2310_06993_b200.collectives import MaskSpec
+    from paper_2310_06993_b200.dist import TarCommunicator
+    from paper_2310_06993_b200.session import BoundedSession
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(_dev(rank))
+    dev = torch.device("cuda", _dev(rank))
+    _init(rank, world, dev)
+    L, dim = 5_000_000, 1 << 23
+    comm = TarCommunicator(max_len=L)
+    x = torch.from_numpy(O.make_buckets(900, world, L)[rank]).to(dev)
+    out = torch.empty_like(x)
+    unit = int(_lib.lib().optr_fused_unit_entries(dim, world))
+    nunits = (dim // world) // unit
+    for case, (delay, deadline) in enumerate([(False, 10 ** 10), (True, 50_000)]):
+        dist.barrier()
+        torch.cuda.synchronize()
+        if delay and rank != 0:
+            torch.cuda._sleep(200_000_000)  # every peer of rank 0 is late by ~0.1 s
+        stats = torch.zeros(7, dtype=torch.int64, device=dev)
+        cuts = torch.zeros(nunits, dtype=torch.int32, device=dev)
+        comm.allreduce(x, out, rotation=1, ht=True, job_seed=5, generation=case, masks=MaskSpec.coin(77 + case, 0.01),
+                       deadline_ns=deadline, stats=stats, cut_units=cuts)
+        torch.cuda.synchronize()
+        np.save(os.path.join(outdir, f"b{case}_r{rank}.npy"), out.cpu().numpy())
+        np.save(os.path.join(outdir, f"b{case}_r{rank}_stats.npy"), stats.cpu().numpy())
+        np.save(os.path.join(outdir, f"b{case}_r{rank}_cuts.npy"), cuts.cpu().numpy())
+    np.save(os.path.join(outdir, f"unit_r{rank}.npy"), np.array([unit]))
+    # the control loop on device timings: calibration, then bounded generations
+    sess = BoundedSession(comm, seed=11, ht="on", drop_prob=0.01, calibration_iterations=3)
+    acts = []
+    for _g in range(3):
+        rep = sess.run_generation(x)
+        acts.append([rep.generation, rep.rotation, int(rep.action is not None), rep.max_loss,
+                     float(rep.stage_times.min()), sess.control.t_b()])
+    np.save(os.path.join(outdir, f"sess_r{rank}.npy"), np.array(acts, dtype=np.float64))
+    comm.close()
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_bounded_stage1_deadline_vs_oracle():
+    """optr_tar_bounded: with a generous deadline nothing is cut and every
+    rank equals the oracle; with every peer of rank 0 delayed ~0.1 s and a
+    50 us bound, rank 0's owner stops waiting and aggregates without them
+    (cut entries reported, counted as lost) -- and every rank still equals
+    the oracle run with the reported cut-offs applied to the stage-1 masks
+    (1e-5), received / cut counts exact.  Then BoundedSession calibrates t_B
+    from the kernel's own stage times and runs bounded generations."""
+    import torch.multiprocessing as mp
+
+    _need_gpu()
+    world = _world()
+    L, dim = 5_000_000, 1 << 23
+    with tempfile.TemporaryDirectory() as d:
+        mp.spawn(_bounded_worker, args=(world, _free_port(), d), nprocs=world, join=True)
+        unit = int(np.load(os.path.join(d, "unit_r0.npy"))[0])
+        S = dim // world
+        buckets = O.make_buckets(900, world, L)
+        for case in range(2):
+            r = 1 % world
+            masks = O.datagram_masks(77 + case, dim, world, r, 0.01)
+            entry, cut_want = {}, {}
+            for o in range(world):
+                cuts = np.load(os.path.join(d, f"b{case}_r{o}_cuts.npy")).astype(np.uint32)
+                per_entry = np.repeat(cuts, unit)[:S]
+                cut_want[o] = 0
+                for i in range(world):
+                    if i == o:
+                        continue
+                    pk = O.expand_packets(masks[(1, o, i)], S, 350)
+                    keep = pk & ~((per_entry >> i) & 1).astype(bool)
+                    entry[(1, o, i)] = keep
+                    cut_want[o] += int(pk.sum() - keep.sum())
+            want, _w, tar = O.run_generation(buckets, 5, case, True, masks=masks, r=r, return_wire=True,
+                                             entry_masks=entry, threads=world)
+            for rank in range(world):
+                got = np.load(os.path.join(d, f"b{case}_r{rank}.npy"))
+                st = np.load(os.path.join(d, f"b{case}_r{rank}_stats.npy"))
+                rel = np.linalg.norm(got.astype(np.float64) - want[rank]) / np.linalg.norm(want[rank])
+                assert rel < 1e-5, (case, rank, rel)
+                recv1 = sum(int(entry[(1, rank, i)].sum()) for i in range(world) if i != rank)
+                assert st[0] == recv1 and st[2] == cut_want[rank], (case, rank, st)
+                assert st[4] <= st[5] and st[4] <= st[6]  # open <= stage-1 end, stage-2 end
+            if case == 0:
+                assert all(cut_want[o] == 0 for o in range(world))
+            else:
+                assert cut_want[0] > 0  # rank 0 stopped waiting for its late peers
+        for rank in range(world):
+            acts = np.load(os.path.join(d, f"sess_r{rank}.npy"))
+            assert list(acts[:, 0]) == [0, 1, 2] and list(acts[:, 1]) == [g % world for g in range(3)]
+            assert (acts[:, 4] > 0).all() and (acts[:, 5] > 0).all()  # device stage times, calibrated t_B
