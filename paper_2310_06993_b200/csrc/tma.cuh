@@ -347,10 +347,11 @@ __device__ __forceinline__ void tma_tile(const TmaMaps* maps, const CUtensorMap*
   if constexpr (SK == TS_GATHER) {
     // stage-2 masks (collectives.py:140-150); a tile whose packets all
     // arrived skips them (one branch per tile, not per float4)
-    if (!all_kept && !STRIDED) {
-      // contiguous tile: one shard, one owner (not this receiver), one
-      // bitmap row for the whole tile
-      const int j = (int)(g0 >> a.shard_shift);
+    const int jt = STRIDED ? 0 : (int)(g0 >> a.shard_shift);
+    if (!all_kept && !STRIDED && shard_owner(jt, a.r, a.n) != worker) {
+      // contiguous tile: one shard, one owner (not this receiver: its own
+      // shard is never masked), one bitmap row for the whole tile
+      const int j = jt;
       const uint32_t* const row = a.m.row(1, worker, shard_owner(j, a.r, a.n));
       const uint32_t e0 = (uint32_t)(g0 - ((int64_t)j << a.shard_shift));
 #pragma unroll
@@ -365,7 +366,7 @@ __device__ __forceinline__ void tma_tile(const TmaMaps* maps, const CUtensorMap*
           *reinterpret_cast<uchar4*>(gotw + g0 + i) =
               make_uchar4(kk & 1u, (kk >> 1) & 1u, (kk >> 2) & 1u, (kk >> 3) & 1u);
       }
-    } else if (!all_kept) {
+    } else if (!all_kept) {  // strided tiles (several shards) and own contiguous tiles
 #pragma unroll
       for (int m = 0; m < 8; ++m) {
         const int i = b0 + roff(P, 0, 4 * m);
@@ -560,7 +561,7 @@ __global__ void __launch_bounds__(1 << (T - 5)) tma_pass_kernel(const __grid_con
         const int sp = (k - 1) % kStages;
         if (tn < a.ntiles) tile_issue<T, STRIDED, SK, CBW>(maps, a, worker, tn, base + sp * SB, &full[sp]);
       }
-    });
+    }, NoEpi{}, all_kept);
   }
   if constexpr (STRIDED) {
     if (tid == 0) bulk_wait0();
@@ -586,8 +587,10 @@ struct MeanArgs {
   MaskView m;   // stage-1 rows (stage 0 of the bitmap layout)
 };
 
+// two CTAs per SM for 256-thread tiles (T = 13: <= 128 registers), one for
+// 512-thread tiles (T = 14)
 template <int T, int kStages, int NW>
-__global__ void __launch_bounds__(1 << (T - 5), 2) tma_mean_kernel(const __grid_constant__ TmaArgs a,
+__global__ void __launch_bounds__(1 << (T - 5), T == 13 ? 2 : 1) tma_mean_kernel(const __grid_constant__ TmaArgs a,
                                                                  const __grid_constant__ MeanArgs ma) {
   constexpr size_t SB = tma_stage_bytes<T>();
   constexpr RPlan P = make_rplan(T, 0);
@@ -616,7 +619,7 @@ __global__ void __launch_bounds__(1 << (T - 5), 2) tma_mean_kernel(const __grid_
   if (tid == 0)
     for (int s = 0; s < kStages; ++s) issue(s, s);
   double acc[32];
-  uint32_t cnt[NQ / 2 > 4 ? NQ / 2 : 4];  // count byte per entry (entries 4c..4c+3 in cnt[c])
+  uint32_t cnt[8];  // count byte per entry (a thread's entries 4c..4c+3 in cnt[c])
 #pragma unroll
   for (int j = 0; j < 32; ++j) acc[j] = 0.0;
   const float scale = ma.scale;
@@ -659,7 +662,7 @@ __global__ void __launch_bounds__(1 << (T - 5), 2) tma_mean_kernel(const __grid_
           }
           if (w == 0) {
 #pragma unroll
-            for (int c = 0; c < NQ * VW / 4; ++c) cnt[c] = 0u;
+            for (int c = 0; c < 8; ++c) cnt[c] = 0u;
           }
 #pragma unroll
           for (int q = 0; q < NQ; ++q) cnt[(VW * q) / 4] += nibble_bytes(kk[q]) << (8 * ((VW * q) % 4));
