@@ -169,11 +169,11 @@ def step_alg_bytes(buckets, n_workers, s_in, s_out, ht):
 
 # kernel classes -> kernel names in the one-GPU ncu capture (decode order there:
 # strided gather first, contiguous last)
-NCU_NAMES = {  # regexes (stage count free: it depends on the tile shape)
-    "enc_first": r"tma_pass_kernel<\d+, \d, 0, 1,",
-    "enc_last": r"tma_pass_kernel<\d+, \d, 1, 0, SnkBuf",
-    "dec_first": r"tma_pass_kernel<\d+, \d, [01], 2,",
-    "dec_last": r"tma_pass_kernel<\d+, \d, [01], 0, SnkDecode",
+NCU_NAMES = {  # regexes for the one-GPU fast plan (stage count free: it depends on the tile shape)
+    "enc_first": r"tma_pass_kernel<\d+, \d, 1, 1,",
+    "enc_mean": r"tma_mean_kernel",
+    "dec_first": r"tma_pass_kernel<\d+, \d, 0, 2,",
+    "dec_last": r"tma_pass_kernel<\d+, \d, 1, 0, SnkDecode",
     "aggregate": r"tma_agg_kernel",
     "prep": r"prep_kernel",
 }
@@ -185,9 +185,8 @@ def ncu_traffic(cls: str, multi: bool):
         return None
     import glob
 
-    # the newest capture of the current kernels first (``*_head``), else the latest round's
-    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_ncu_full_1gpu_resnet50.json")))
-    files += sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_ncu_full_1gpu_resnet50_head.json")))
+    # the newest capture of the current kernels
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_ncu_full_1gpu_fastplan.json")))
     if not files or cls not in NCU_NAMES:
         return None
     try:
@@ -261,7 +260,7 @@ def run_ours(args):
     stream = torch.cuda.current_stream(dev)
     drop = args.drop
     state = {"gen": 0}
-    overlap = os.environ.get("OPTR_BENCH_SYNC", "0") != "1"  # A/B switch: buckets in order
+    overlap = True  # pass (A): buckets pipelined two in flight
 
     def call_bucket(b, gen, src, dst, async_op):
         masks = MaskSpec.coin(1000003 * gen + b, drop) if drop > 0 else MaskSpec.none()
@@ -273,7 +272,7 @@ def run_ours(args):
             tar_allreduce_local(src[b], rotation=r, ht=ht, job_seed=7, generation=gen,
                                 bucket_id=b, masks=masks, out=dst[b], async_op=async_op)
 
-    def one_step(src=None, dst=None):
+    def one_step(src=None, dst=None, overlap=True):
         gen = state["gen"]
         for b in range(len(buckets)):
             call_bucket(b, gen, src or grads, dst or outs, overlap)
@@ -299,39 +298,43 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
+    def timed(overlap: bool, kernel_events: bool):
+        """K steps between a barrier + synchronize on both sides, CUDA events
+        on the calling stream; optionally every library launch bracketed by
+        its own events (optr_timing_*).  Returns (ms per step over ranks,
+        per-kernel {class: (ms, launches, worker-passes)}, launches)."""
+        barrier()
+        _lib.timing_collect()
+        _lib.timing_enable(kernel_events)
+        launches0 = _lib.launch_count()
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        for _ in range(args.steps):
+            one_step(overlap=overlap)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        launches = _lib.launch_count() - launches0
+        _lib.timing_enable(False)
+        per = _lib.timing_collect()
+        return max_over_ranks(ev0.elapsed_time(ev1)) / args.steps, per, launches
+
     # ---- device-timed steps
     for _ in range(args.warmup):
-        one_step()
+        one_step(overlap=overlap)
     barrier()
     clocks = ClockSampler(local_rank)
     clocks.start()
     time.sleep(0.3)
-    _lib.timing_collect()
-    _lib.timing_enable(True)
-    launches0 = _lib.launch_count()
-    barrier()
-    ev0 = torch.cuda.Event(enable_timing=True)
-    ev1 = torch.cuda.Event(enable_timing=True)
-    ev0.record(stream)
-    for _ in range(args.steps):
-        one_step()
-    ev1.record(stream)
-    torch.cuda.synchronize()
-    launches = _lib.launch_count() - launches0
-    _lib.timing_enable(False)
-    per_kernel = _lib.timing_collect()
-    dev_ms = ev0.elapsed_time(ev1)
-    # an untimed pass without per-kernel events, to confirm they cost nothing
-    barrier()
-    ev0.record(stream)
-    for _ in range(args.steps):
-        one_step()
-    ev1.record(stream)
-    torch.cuda.synchronize()
-    dev_ms_plain = ev0.elapsed_time(ev1)
+    # (A) the headline: buckets pipelined two in flight, as a DDP comm hook runs them
+    ms_per_step, _unused, launches = timed(overlap, False)
+    # (B) the same with every launch bracketed by CUDA events: per-kernel times
+    #     under the two-bucket concurrency (contended: they overlap each other)
+    ms_events, per_contended, _l = timed(overlap, True)
+    # (C) buckets serialised, every launch bracketed: isolated per-kernel times,
+    #     the roofline's denominators
+    ms_serial, per_kernel, _l = timed(False, True)
     clk = clocks.stop()
-    dev_ms = max_over_ranks(min(dev_ms, dev_ms_plain))
-    ms_per_step = dev_ms / args.steps
 
     grad_bytes = s_in * sum(buckets)
     value = n_workers * grad_bytes / (ms_per_step * 1e-3) / 1e9
@@ -389,6 +392,8 @@ def run_ours(args):
 
     e2e_step()
     barrier()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
     ev0.record(stream)
     e2e_steps = max(1, min(args.steps, 5))
     for _ in range(e2e_steps):
@@ -402,19 +407,18 @@ def run_ours(args):
            "ms_per_step": round(e2e_ms, 3), "h2d_bytes_per_step": io_bytes, "d2h_bytes_per_step": io_bytes,
            "pipeline": "per bucket: H2D stream -> TAR call -> D2H stream (D2H of b overlaps H2D of b+1)"}
 
-    # ---- roofline of the dominant kernel class (live CUDA-event durations)
+    # ---- roofline of the dominant kernel class: live CUDA-event durations of
+    # pass (C), where every launch runs alone (buckets serialised); pass (B)'s
+    # contended durations are reported beside them
     peaks = load_peaks()
     live = {k: v for k, v in per_kernel.items() if v[1] > 0}
-    # dominant kernel on the critical path (prep runs on a low-priority side
-    # stream, overlapped with the previous call's kernels)
-    crit = {k: v for k, v in live.items() if k != "prep"} or live
-    dom = max(crit, key=lambda k: crit[k][0])
+    dom = max(live, key=lambda k: live[k][0])
     dom_ms, dom_n, dom_units = live[dom]
 
-    def class_bytes(cls, nvlink=False):
+    def class_bytes(cls, nvlink=False, table=None):
         """Algorithmic bytes the timed launches of `cls` moved: per-worker
         bytes of each bucket x worker-passes (units spread evenly over buckets)."""
-        units = live[cls][2]
+        units = (table or live)[cls][2]
         per_b = 0
         for L in buckets:
             dim = next_pow2(L) if ht else L
@@ -436,15 +440,22 @@ def run_ours(args):
         roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
                 "frac": round(achieved / peaks["hbm_gbs"], 4), "kernel": dom, "peak_src": peaks["src"],
                 "traffic": None}
+    roof["timing"] = ("live CUDA events around every launch, timed pass (C): K steps with the buckets "
+                      "serialised (each launch alone on the GPU)")
     # DRAM traffic of the dominant kernel from the committed ncu --set full capture
-    # (profiles/r01_ncu_full_*.json; per launch = per worker-pass on one GPU)
     tr = ncu_traffic(dom, multi)
     if tr is not None:
-        roof["traffic"], roof["traffic_src"] = tr[0], tr[1] + " (cold-cache ncu replay; the live run reuses L2)"
-    kernels = {k: {"ms_per_step": round(v[0] / args.steps, 4), "launches_per_step": v[1] / args.steps,
-                   "avg_launch_us": round(v[0] / v[1] * 1e3, 2),
-                   "hbm_gbs": round(class_bytes(k) / (v[0] * 1e-3) / 1e9, 1)}
-               for k, v in live.items()}
+        roof["traffic"], roof["traffic_src"] = tr[0], tr[1] + " (cold-cache ncu replay, one launch)"
+
+    def table(per):
+        lv = {k: v for k, v in per.items() if v[1] > 0}
+        return {k: {"ms_per_step": round(v[0] / args.steps, 4), "launches_per_step": v[1] / args.steps,
+                    "avg_launch_us": round(v[0] / v[1] * 1e3, 2),
+                    "hbm_gbs": round(class_bytes(k, table=lv) / (v[0] * 1e-3) / 1e9, 1)}
+                for k, v in lv.items()}
+
+    kernels = table(per_kernel)
+    kernels_contended = table(per_contended)
 
     # whole-step roofline: max(HBM_alg/HBM, NVL/NVLink)
     hbm_alg, nvl = step_alg_bytes(buckets, n_workers, s_in, s_out, ht)
@@ -470,12 +481,20 @@ def run_ours(args):
                    "bucket_entries": per, "total_entries": total, "workers": n_workers,
                    "workers_per_gpu": per_rank_workers, "ht": args.ht, "drop": drop,
                    "mask": "datagram coin, 350-entry packets" if drop > 0 else "lossless",
-                   "parallelism": f"tar{n_workers}", "l2": "inputs larger than L2 (no flush)"},
+                   "parallelism": f"tar{n_workers}", "l2": "inputs larger than L2 (no flush)",
+                   "value_def": "aggregate over all workers: workers x gradient bytes / step time "
+                                "(= n x the per-worker algBW s_in*L/t of SURVEY 8(d))",
+                   "timed_passes": "(A) value / ms_per_step: buckets pipelined, two in flight; "
+                                   "(B) the same with per-launch events -> kernels_contended; "
+                                   "(C) buckets serialised with per-launch events -> kernels, roofline"},
         "algbw_per_worker_gbs": round(grad_bytes / (ms_per_step * 1e-3) / 1e9, 3),
+        "ms_per_step_serialized": round(ms_serial, 4),
+        "ms_per_step_with_kernel_events": round(ms_events, 4),
         "e2e": e2e,
         "roofline": roof,
         "step_roofline": step_roof,
         "kernels": kernels,
+        "kernels_contended": kernels_contended,
         "gpu_launches": int(launches),
         "clocks": clk,
     }
@@ -488,7 +507,7 @@ def run_ours(args):
         for L in buckets:
             _, dt = cpu_baseline(L, n_workers, drop, ht, thr)
             done_b += 1
-            done_bytes += n_workers * 4 * L
+            done_bytes += n_workers * s_in * L
             secs += dt
             if secs >= 10.0 or secs + dt > 30.0:
                 break
@@ -496,6 +515,8 @@ def run_ours(args):
         out["cpu_baseline"] = {"value": round(gbs, 6), "unit": "GB/s", "cores": thr, "kind": "port",
                                "sample": f"{done_b} of {len(buckets)} buckets of the step x {n_workers} workers, "
                                          f"oracle port (numpy, fp64), {secs:.1f}s, {ncores} cores visible"}
+    if not multi and args.workload != "headline":
+        out["headline"] = headline_line(args, dev, stream)
     if rank == 0:
         print(json.dumps(out), flush=True)
     if multi:
@@ -505,39 +526,86 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+def headline_line(args, dev, stream) -> dict:
+    """The north-star bucket (25,000,000 fp32 entries, D = 2^25) at N=1 with
+    the same co-resident workers and drop model, timed like pass (A): K
+    generations, device time, the whole-step roofline of SURVEY 8(d)."""
+    import torch
+
+    from paper_2310_06993_b200.collectives import MaskSpec, local_join, tar_allreduce_local
+
+    L, n = WORKLOADS["headline"][0], args.workers
+    g = torch.Generator(device=dev).manual_seed(4321)
+    xs = [torch.randn(L, device=dev, generator=g) for _ in range(n)]
+    outs = [torch.empty_like(x) for x in xs]
+
+    def step(gen):
+        masks = MaskSpec.coin(7919 * gen + 1, args.drop) if args.drop > 0 else MaskSpec.none()
+        tar_allreduce_local(xs, rotation=gen % n, ht=True, job_seed=7, generation=gen, bucket_id=0, masks=masks,
+                            out=outs, async_op=True)
+        local_join()
+
+    for gen in range(args.warmup):
+        step(gen)
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for gen in range(args.steps):
+        step(args.warmup + gen)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    hbm_alg, _nvl = step_alg_bytes([L], n, 4, 4, True)
+    hbm_alg *= n
+    t_roof = hbm_alg / (load_peaks()["hbm_gbs"] * 1e9)
+    del xs, outs
+    return {"workload": "headline", "desc": WORKLOADS["headline"][3], "workers": n, "steps": args.steps,
+            "ms_per_step": round(ms, 4), "value": round(n * 4 * L / (ms * 1e-3) / 1e9, 3), "unit": "GB/s",
+            "step_roofline": {"t_roof_ms": round(t_roof * 1e3, 4), "frac": round(t_roof * 1e3 / ms, 4),
+                              "hbm_alg_bytes": hbm_alg}}
+
+
 # ------------------------------------------------------------ reference arm
 def run_reference(args):
-    """The reference's CPU algorithm (oracle port of ubar -- /root/reference is
-    not on the GPU box) on this host, rank 0 only."""
+    """The reference's CPU algorithm -- the oracle port of ubar (numpy fp64,
+    /root/reference is not on the GPU box): rht_encode x n, _mean_received per
+    owner, assembly, rht_decode x n under the same datagram-coin masks, on the
+    same buckets as our arm (a step = every bucket of the workload, same
+    metric).  Rank 0 only; the other ranks exit."""
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return
     total, per, dt_name, desc = WORKLOADS[args.workload]
+    buckets = bucket_sizes(total, per)
     n_workers = world if world > 1 else args.workers
     ht = args.ht == "on"
     ncores = len(os.sched_getaffinity(0))
     thr = min(n_workers, ncores)
-    # bounded sample: one bucket, capped so a step stays ~10 s on one core
-    sample = min(per, 1 << 21)
+    # warm-up steps on a 1/16 sample of the first bucket (numpy / allocator
+    # paths warm; the timed steps run the full buckets)
     for _ in range(args.warmup):
-        cpu_baseline(sample, n_workers, args.drop, ht, thr)
+        cpu_baseline(max(1, buckets[0] // 16), n_workers, args.drop, ht, thr)
     secs = []
     for _ in range(args.steps):
-        _, s = cpu_baseline(sample, n_workers, args.drop, ht, thr)
-        secs.append(s)
+        secs.append(sum(cpu_baseline(L, n_workers, args.drop, ht, thr)[1] for L in buckets))
     t = sum(secs) / len(secs)
-    val = n_workers * 4 * sample / t / 1e9
+    s_in = 2 if dt_name == "bf16" else 4
+    val = n_workers * s_in * sum(buckets) / t / 1e9
     out = {
         "metric": "bucket allreduce GB/s (TAR+RHT)", "value": round(val, 6), "unit": "GB/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t * 1e3, 2),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "impl": "reference",
-        "config": {"workload": args.workload, "desc": desc, "workers": n_workers, "ht": args.ht,
-                   "drop": args.drop, "sample_entries": sample},
+        "config": {"workload": args.workload, "desc": desc, "buckets": len(buckets), "bucket_entries": per,
+                   "total_entries": total, "workers": n_workers, "ht": args.ht, "drop": args.drop,
+                   "same_config": True,
+                   "value_def": "aggregate over all workers: workers x gradient bytes / step time"},
         "cpu_baseline": {"value": round(val, 6), "unit": "GB/s", "cores": thr, "kind": "port",
-                         "sample": f"one {sample}-entry bucket x {n_workers} workers per step "
-                                   f"(oracle port of ubar: numpy fp64, threads over workers)"},
+                         "sample": f"every bucket of the workload ({len(buckets)} x up to {per} entries) x "
+                                   f"{n_workers} workers per step (oracle port of ubar: numpy fp64, threads over "
+                                   f"workers); warm-up on a 1/16 sample"},
         "e2e": {"value": round(val, 6), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(out), flush=True)
