@@ -55,23 +55,35 @@ def main():
             t = timeit(lambda s: lib.optr_probe_copy(bufs[1].data_ptr(), loc.data_ptr(), nbytes, blocks, 0,
                                                      s.cuda_stream), d0)
             out.append({"probe": "sm_push_0to1", "blocks": blocks, "GBps": round(nbytes / t / 1e9, 1)})
-        if n >= 3:
-            # pull from all peers at once, each peer's chunk by its own stream
-            chunk = nbytes // (n - 1)
-            streams = [torch.cuda.Stream(d0) for _ in range(n - 1)]
-            def pull_all(s):
-                for k, j in enumerate(range(1, n)):
-                    lib.optr_probe_copy(loc.data_ptr() + k * chunk, bufs[j].data_ptr(), chunk, 148 * 2 // (n - 1) + 1, 0,
-                                        streams[k].cuda_stream)
-                torch.cuda.synchronize(d0)
-            import time
-            for _ in range(3):
-                pull_all(None)
-            t0 = time.perf_counter()
-            for _ in range(10):
-                pull_all(None)
-            t = (time.perf_counter() - t0) / 10
-            out.append({"probe": "sm_pull_all_peers_wallclock", "GBps": round(chunk * (n - 1) / t / 1e9, 1)})
+        # every GPU pulls from every peer at once (the TAR exchange pattern):
+        # chunks of 16-byte multiples, one stream per (GPU, peer), return codes
+        # checked, wall clock around synchronised rounds
+        import time
+
+        chunk = (nbytes // (n - 1)) // MB * MB
+        locs = [torch.empty(nbytes // 4, device=f"cuda:{i}") for i in range(n)]
+        streams = {(i, j): torch.cuda.Stream(torch.device("cuda", i)) for i in range(n) for j in range(n) if i != j}
+        blocks = max(1, 148 * 2 // (n - 1))
+
+        def pull_all():
+            for i in range(n):
+                for k, j in enumerate(p for p in range(n) if p != i):
+                    rc = lib.optr_probe_copy(locs[i].data_ptr() + k * chunk, bufs[j].data_ptr(), chunk, blocks, i,
+                                             streams[(i, j)].cuda_stream)
+                    assert rc == 0, rc
+            for i in range(n):
+                torch.cuda.synchronize(torch.device("cuda", i))
+
+        for _ in range(3):
+            pull_all()
+        t0 = time.perf_counter()
+        reps = 10
+        for _ in range(reps):
+            pull_all()
+        t = (time.perf_counter() - t0) / reps
+        out.append({"probe": "sm_pull_all_gpus_all_peers_wallclock", "gpus": n,
+                    "GBps_per_gpu_in": round(chunk * (n - 1) / t / 1e9, 1),
+                    "note": "every GPU pulls (n-1) chunks from its peers concurrently; wall clock per round"})
     for o in out:
         print(json.dumps(o), flush=True)
 
