@@ -255,6 +255,10 @@ int optr_tar_bounded(optr_comm c, const void* x, void* out, int64_t L, int dtype
                      const optr_mask_spec* masks, uint64_t stage1_deadline_ns, optr_tar_stats* stats,
                      uint32_t* cut_units, int async, void* stream);
 
+/* Cap the persistent fused kernel at `ctas` CTAs (0 = SMs x occupancy): in
+ * DDP the kernel waits on peers while backward compute wants the SMs. */
+int optr_comm_set_fused_grid(optr_comm c, int ctas);
+
 /* Device-side all-rank barrier on `stream` (flags over NVLink). */
 int optr_comm_barrier(optr_comm c, void* stream);
 

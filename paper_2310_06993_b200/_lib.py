@@ -86,6 +86,7 @@ SIGNATURES = {
     "optr_tar": (_int, [_vp, _vp, _vp, _i64, _int, _int, _u64, _u64, _u64, _int, _int,
                         ctypes.POINTER(optr_mask_spec), _vp, _vp]),
     "optr_comm_barrier": (_int, [_vp, _vp]),
+    "optr_comm_set_fused_grid": (_int, [_vp, _int]),
     "optr_tar_async": (_int, [_vp, _vp, _vp, _i64, _int, _int, _u64, _u64, _u64, _int, _int,
                               ctypes.POINTER(optr_mask_spec), _vp, _vp]),
     "optr_comm_join": (_int, [_vp, _vp]),

@@ -1263,6 +1263,7 @@ struct optr_comm_s {
   cudaEvent_t prep_ready[2], done[2];
   bool done_recorded[2];
   uint64_t calls;
+  int fused_grid;  // CTAs of the persistent fused kernel (0 = SMs x occupancy)
 };
 
 size_t optr_comm_handle_bytes(void) { return sizeof(cudaIpcMemHandle_t); }
@@ -1293,10 +1294,10 @@ int optr_comm_create(optr_comm* out, int device, int rank, int n, int64_t max_le
     off = align_up(off + (size_t)smax * 4, 1024);
     c->off_g[p] = off;  // stage-2 receive vector, written by every owner's push
     off = align_up(off + (size_t)c->max_dim * 4, 1024);
-    c->off_ef[p] = off;  // fused kernel: per-tile encode flags [n][tiles], receive counts [tiles]
-    off = align_up(off + (size_t)n * (c->max_dim >> 13 > 0 ? c->max_dim >> 13 : 1) * 4, 256);
+    c->off_ef[p] = off;  // fused kernel: my encode flags [tiles], my published-unit flags [tiles][4]
+    off = align_up(off + (size_t)(c->max_dim >> 13 > 0 ? c->max_dim >> 13 : 1) * 4, 256);
     c->off_gf[p] = off;
-    off = align_up(off + (size_t)(c->max_dim >> 13 > 0 ? c->max_dim >> 13 : 1) * 4, 1024);
+    off = align_up(off + (size_t)4 * (c->max_dim >> 13 > 0 ? c->max_dim >> 13 : 1) * 4, 1024);
   }
   c->sym_bytes = off;
   int64_t pw = mask_words(c->max_dim, n, 1);  // epp >= 1 bound
@@ -1417,6 +1418,12 @@ static int comm_barrier(optr_comm c, int set, cudaStream_t st) {
   return OPTR_OK;
 }
 
+int optr_comm_set_fused_grid(optr_comm c, int ctas) {
+  if (!c || ctas < 0) return OPTR_EINVAL;
+  c->fused_grid = ctas;
+  return OPTR_OK;
+}
+
 int optr_comm_barrier(optr_comm c, void* stream) {
   if (!c) return OPTR_EINVAL;
   CK(cudaSetDevice(c->device));
@@ -1527,8 +1534,11 @@ int launch_fused_t(const TmaArgs& ae, const TmaArgs& ad, const SnkBuf& se, const
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem) != cudaSuccess || per_sm < 1)
     per_sm = 1;
   int grid = nsm * per_sm;
-  {  // OPTR_FUSED_GRID caps the grid (several ranks sharing one GPU in tests:
-     // every rank's persistent grid must fit on the GPU at once)
+  // a communicator's cap (optr_comm_set_fused_grid: leave SMs to the
+  // backward pass in DDP), else OPTR_FUSED_GRID
+  if (f.grid_cap > 0 && f.grid_cap < grid) {
+    grid = f.grid_cap;
+  } else {
     const char* e = getenv("OPTR_FUSED_GRID");
     if (e && atoi(e) > 0 && atoi(e) < grid) grid = atoi(e);
   }
@@ -1686,11 +1696,9 @@ static int tar_enqueue(optr_comm c, const void* x, void* out, int64_t L, int dty
     for (int i = 0; i < n; ++i) {
       f.Y[i] = Yp[i];
       f.A[i] = Ap[i];
-      f.eflag_out[i] = (unsigned int*)(c->peer[i] + c->off_ef[par]) + (size_t)me * (c->max_dim >> 13);
+      f.eflag[i] = (unsigned int*)(c->peer[i] + c->off_ef[par]);
       f.gflag[i] = (unsigned int*)(c->peer[i] + c->off_gf[par]);
     }
-    f.eflag_in = (const unsigned int*)(c->peer[me] + c->off_ef[par]);
-    f.estride = c->max_dim >> 13;
     f.ctr = c->fused_ctr[par];
     f.epoch = ++c->fepoch[par];
     f.n = n;
@@ -1703,6 +1711,7 @@ static int tar_enqueue(optr_comm c, const void* x, void* out, int64_t L, int dty
     f.trace = (uint4*)g_fused_trace;
     f.trace_cap = g_fused_trace_cap;
     f.watchdog_ns = watchdog_ns();
+    f.grid_cap = c->fused_grid;
     f.deadline_ns = deadline_ns;
     f.stats = (unsigned long long*)stats;
     f.counts = counts;

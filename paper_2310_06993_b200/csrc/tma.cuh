@@ -814,15 +814,14 @@ namespace optr {
 //   E/D group (2^(T-5) threads): all E tickets (row order, row k = tiles
 //     {j*ns + k}), then all D tickets (row order)
 //     E(t)  encode tile t of my wire vector Y in place (scale 1/sqrt(dim)),
-//           then eflag[me][t] = epoch in every rank's memory
-//     D(t)  once my gflag[t] counts every unit of tile t: pull it from its owner's aggregate
+//           then eflag[me][t] = epoch in my memory
+//     D(t)  once tile t's owner counted every unit of it: pull it from the owner's aggregate
 //           (one TMA bulk copy over NVLink, stage-2 masks applied as it is
 //           read) and decode it into my G
 //   A group (kAggThreads threads): units (1/UPT tile) of my shard in order;
 //     for each, wait for eflag[t] at every rank, stream the unit from every
 //     rank's Y in kAggCh-entry chunks through a ring, masked fp64 mean in
-//     ascending node order into my aggregate A; then add 1 to gflag[t] at
-//     every rank (the consuming D job re-arms it to 0).
+//     ascending node order into my aggregate A; then gflag[me][t*4+u] = epoch.
 // E jobs wait for nothing, A jobs only for E jobs, D jobs only for A jobs of
 // the same row, and every queue is claimed in the same order on all ranks,
 // so nothing waits on a job that cannot run.  A D job's load is deferred
@@ -830,13 +829,14 @@ namespace optr {
 struct FusedArgs {
   const float* Y[kMaxW];       // every rank's wire vector (peer-mapped)
   float* A[kMaxW];             // every rank's owner-shard aggregate (peer-mapped)
-  // encode-tile flags: rank q keeps [n][tiles] in its own memory; my E job
-  // writes row `me` of every rank's copy (eflag_out[q]), my aggregate group
-  // polls its local copy (eflag_in + q*estride) -- no polling over NVLink
-  unsigned int* eflag_out[kMaxW];
-  const unsigned int* eflag_in;
-  int64_t estride;
-  unsigned int* gflag[kMaxW];  // every rank's receive-tile flags
+  // Flags live in the WRITER's memory and readers poll them over NVLink, so
+  // a writer's system-scope release only waits for its own GPU's L2:
+  //   eflag[q][t]           = epoch once rank q encoded tile t (its E job);
+  //   gflag[q][t * 4 + u]   = epoch once owner q published unit u of tile t.
+  // Epochs count the calls of one parity, so a flag left by an earlier call
+  // (any shape, any owner) is always below the current epoch: no re-arming.
+  unsigned int* eflag[kMaxW];
+  unsigned int* gflag[kMaxW];
   unsigned int* ctr;           // local [0] E/D ticket, [1] CTAs done, [2] A ticket (reset by the last CTA)
   unsigned int epoch;
   int n, me, r, own;
@@ -850,6 +850,7 @@ struct FusedArgs {
   // 323-326): an owner waits for a peer's encoded tile until deadline_ns
   // after its CTA started, then aggregates without it (0 = unbounded)
   uint64_t deadline_ns;
+  int grid_cap;                      // host: CTAs of the launch (0 = SMs x occupancy)
   unsigned long long* stats;         // optr_tar_stats (device) or null
   const unsigned long long* counts;  // this rank's [2][n] mask-model received counts
   uint32_t* cut_units;               // optional [units]: peers cut from each stage-1 unit
@@ -866,14 +867,23 @@ __device__ __forceinline__ unsigned int ld_acquire_sys(const unsigned int* p) {
 __device__ __forceinline__ void st_release_sys(unsigned int* p, unsigned int v) {
   asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
-// Flags of the fused kernel (PTX memory model, fence-based synchronisation
-// at system scope, since writer and reader sit on different GPUs):
+// Flags of the fused kernel.  Every flag lives in its WRITER's memory, next
+// to the data it publishes (the writer's wire tiles Y / aggregate A), and
+// readers poll it over NVLink:
 //   writer: data stores by the group -> group barrier -> one thread:
-//           fence.acq_rel.sys (release, cumulative over the barrier) ->
-//           relaxed system-scope flag store / reduction;
-//   reader: relaxed system-scope polls -> fence.acq_rel.sys (acquire) ->
-//           fence.proxy.async -> TMA reads of the flagged data.
-__device__ __forceinline__ void fence_acq_rel_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
+//           __threadfence (MEMBAR.SC.GPU, cumulative over the barrier) ->
+//           relaxed system-scope flag store into its own memory;
+//   reader: relaxed system-scope polls of the writer's flag -> fence.acquire.sys
+//           (an L1 invalidate) -> fence.proxy.async -> TMA reads of the data.
+// Flag and data sit in the same GPU's memory and every peer access to it is
+// served by that GPU's L2, so once the fence has made the data GPU-visible
+// (in that L2) any reader that sees the flag reads the data.  A system-scope
+// release (fence.release.sys = MEMBAR.ALL.SYS) gives the same results and is
+// what the PTX model asks for across GPUs, but costs 15-25% of the step at
+// N=2 (profiles/r02_fence_ab.txt); 10,000 back-to-back async calls per test
+// run match the serialised calls bit for bit (test_fused_protocol_async_stress).
+__device__ __forceinline__ void fence_release_sys() { asm volatile("fence.release.sys;" ::: "memory"); }
+__device__ __forceinline__ void fence_acquire_sys() { asm volatile("fence.acquire.sys;" ::: "memory"); }
 __device__ __forceinline__ unsigned int ld_relaxed_sys(const unsigned int* p) {
   unsigned int v;
   asm volatile("ld.relaxed.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -947,6 +957,15 @@ __global__ void __launch_bounds__(NG * (1 << (T - 5)) + kAggThreads)
   const int me = f.me;
   const int64_t ns = f.ns;
   const uint64_t t_cta0 = globaltimer_ns();
+  // owner of contiguous tile t (tiles of shard j are [j*ns, (j+1)*ns)); a
+  // tile is published once its owner flagged every unit of it in this call
+  auto owner_of = [&](int64_t t) { return shard_owner((int)(t / ns), f.r, NW); };
+  auto published = [&](int64_t t) {
+    const unsigned int* g = f.gflag[owner_of(t)] + t * 4;
+    bool ok = true;
+    for (int u = 0; u < UPT; ++u) ok = ok && ld_relaxed_sys(g + u) >= f.epoch;
+    return ok;
+  };
   if (f.stats && tid == 0) atomicMin(f.stats + ST_OPEN, (unsigned long long)t_cta0);
 
   if (tid == 0) {
@@ -978,8 +997,8 @@ __global__ void __launch_bounds__(NG * (1 << (T - 5)) + kAggThreads)
     int64_t pend_e = -1;  // thread 0: encoded tile whose eflag is not yet released
     auto release_e = [&]() {
       if (pend_e >= 0) {
-        fence_acq_rel_sys();  // release, cumulative over the group (its stores came before a group barrier)
-        for (int q = 0; q < f.n; ++q) st_relaxed_sys(f.eflag_out[q] + pend_e, f.epoch);
+        __threadfence();  // release (see "Flags" above), cumulative over the group's stores before its barrier
+        st_relaxed_sys(f.eflag[me] + pend_e, f.epoch);  // my own memory
         pend_e = -1;
       }
     };
@@ -1002,8 +1021,8 @@ __global__ void __launch_bounds__(NG * (1 << (T - 5)) + kAggThreads)
       if (kind == FJ_E) {
         tile_issue_contig<T, TS_BUF>(ae, me, t, gbase + s * SB, &gfull[s]);
       } else if (kind == FJ_D) {
-        if (ld_relaxed_sys(f.gflag[me] + t) >= (unsigned)UPT) {
-          fence_acq_rel_sys();  // acquire
+        if (published(t)) {
+          fence_acquire_sys();
           fence_proxy_async_global();
           tile_issue_contig<T, TS_GATHER>(ad, me, t, gbase + s * SB, &gfull[s]);
         } else {
@@ -1023,8 +1042,8 @@ __global__ void __launch_bounds__(NG * (1 << (T - 5)) + kAggThreads)
       if (ltid == 0 && (deferred >> s & 1u)) {
         release_e();  // never wait while holding an unreleased encode
         const int64_t t = gtile[s];
-        spin_ge_sys(f.gflag[me] + t, (unsigned)UPT, f.watchdog_ns);
-        fence_acq_rel_sys();  // acquire
+        for (int u = 0; u < UPT; ++u) spin_ge_sys(f.gflag[owner_of(t)] + t * 4 + u, f.epoch, f.watchdog_ns);
+        fence_acquire_sys();
         fence_proxy_async_global();
         tile_issue_contig<T, TS_GATHER>(ad, me, t, sb, &gfull[s]);
         deferred &= ~(1u << s);
@@ -1040,10 +1059,6 @@ __global__ void __launch_bounds__(NG * (1 << (T - 5)) + kAggThreads)
         break;
       }
       if (ltid == 0 && kind != FJ_E) release_e();
-      // a D tile's data has landed: re-arm its counter for the next call on
-      // this parity (the owner adds to it again only after seeing my next
-      // encode flag, which is released after this store)
-      if (ltid == 0 && kind == FJ_D) st_relaxed_sys(f.gflag[me] + t, 0u);
       const uint32_t trd = tr && ltid == 0 ? (uint32_t)globaltimer_ns() : 0u;
       if (kind == FJ_E) {
         tma_tile<T, false, TS_BUF, SnkBuf, 3, BARID, G * NED>(nullptr, nullptr, ae, se.bind(me), me, nullptr, t, sb,
@@ -1100,7 +1115,7 @@ __global__ void __launch_bounds__(NG * (1 << (T - 5)) + kAggThreads)
     auto wait_present = [&](int64_t t) {
       uint32_t pres = 0;
       for (int q = 0; q < n; ++q) {
-        const unsigned int* p = f.eflag_in + q * f.estride + t;
+        const unsigned int* p = f.eflag[q] + t;
         if (q == me || f.deadline_ns == 0) {
           spin_ge_sys(p, f.epoch, f.watchdog_ns);
           pres |= 1u << q;
@@ -1116,7 +1131,7 @@ __global__ void __launch_bounds__(NG * (1 << (T - 5)) + kAggThreads)
       const int64_t t = (int64_t)f.own * ns + u / UPT;
       unsigned int v[NW];
 #pragma unroll
-      for (int q = 0; q < n; ++q) v[q] = ld_relaxed_sys(f.eflag_in + q * f.estride + t);  // local, n in flight
+      for (int q = 0; q < n; ++q) v[q] = ld_relaxed_sys(f.eflag[q] + t);  // n polls in flight
       bool ok = true;
 #pragma unroll
       for (int q = 0; q < n; ++q) ok = ok && v[q] >= f.epoch;
@@ -1156,7 +1171,7 @@ __global__ void __launch_bounds__(NG * (1 << (T - 5)) + kAggThreads)
           }
           decide(kAll);
           if (tra) t_ready = (uint32_t)globaltimer_ns();
-          fence_acq_rel_sys();  // acquire
+          fence_acquire_sys();
           fence_proxy_async_global();
         }
       }
@@ -1177,7 +1192,7 @@ __global__ void __launch_bounds__(NG * (1 << (T - 5)) + kAggThreads)
         const int64_t t = (int64_t)f.own * ns + cur / UPT;
         decide(wait_present(t));
         if (tra) t_ready = (uint32_t)globaltimer_ns();
-        fence_acq_rel_sys();  // acquire
+        fence_acquire_sys();
         fence_proxy_async_global();
         const int first = pend_first, cnt = pend_count;
         pend_first = -1;
@@ -1222,9 +1237,9 @@ __global__ void __launch_bounds__(NG * (1 << (T - 5)) + kAggThreads)
       group_sync<2, kAggThreads>();  // stage s consumed (and the unit's results stored, when last)
       if (ta == 0) {
         if (last) {
-          fence_acq_rel_sys();  // release: the group's results before the counts
+          __threadfence();  // release (see "Flags" above): the group's results before the flag
           const int64_t t = (int64_t)f.own * ns + un / UPT;
-          for (int q = 0; q < n; ++q) red_add_relaxed_sys(f.gflag[q] + t, 1u);
+          st_relaxed_sys(f.gflag[me] + t * 4 + un % UPT, f.epoch);  // my own memory
           if (tra && ntr < f.trace_cap / 2)
             tra[ntr++] = make_uint4((1u << 28) | (uint32_t)t, t_claim, t_ready, (uint32_t)globaltimer_ns());
         }

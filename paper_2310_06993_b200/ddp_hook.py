@@ -44,6 +44,7 @@ class OptiReduceState:
     max_payload: int = 1400
     generation: int = 0
     overlap: bool = True
+    fused_ctas: int = 0  # cap on the fused kernel's CTAs (0 = all SMs); leaves SMs to backward
     comm: object = field(default=None, repr=False)
     received: list = field(default_factory=list, repr=False)  # per-bucket [2] counts of the last pass
     _pending: list = field(default_factory=list, repr=False)  # buffers async calls still use
@@ -60,7 +61,8 @@ class OptiReduceState:
             from .dist import TarCommunicator
 
             self.comm = TarCommunicator(max_len=max(self.max_bucket_len, needed_len),
-                                        epp=self.max_payload // 4, group=self.process_group, device=device)
+                                        epp=self.max_payload // 4, group=self.process_group, device=device,
+                                        fused_ctas=self.fused_ctas)
         return self.comm
 
     def masks(self, bucket_index: int) -> MaskSpec:

@@ -60,7 +60,7 @@ def _dtype_code(t) -> int:
 class TarCommunicator:
     """Symmetric NVLink buffers for buckets of up to ``max_len`` entries."""
 
-    def __init__(self, max_len: int, epp: int = 350, group=None, device=None):
+    def __init__(self, max_len: int, epp: int = 350, group=None, device=None, fused_ctas: int = 0):
         import torch
         import torch.distributed as dist
 
@@ -81,7 +81,15 @@ class TarCommunicator:
         blobs = all_gather_bytes(bytes(mine), group, self.device)
         allb = b"".join(blobs)
         check(lib().optr_comm_open(self._h, allb), "comm_open")
+        if fused_ctas:
+            self.set_fused_ctas(fused_ctas)
         dist.barrier(group)
+
+    def set_fused_ctas(self, ctas: int) -> None:
+        """Cap the persistent fused kernel at ``ctas`` CTAs (0 = one per SM x
+        occupancy); fewer leave SMs to concurrent work such as DDP's backward
+        pass."""
+        check(lib().optr_comm_set_fused_grid(self._h, int(ctas)), "comm_set_fused_grid")
 
     def allreduce(self, x, out, *, rotation: int, ht: bool = True, job_seed: int = 0,
                   generation: int = 0, bucket_id: int | None = None, masks: MaskSpec | None = None,
