@@ -68,7 +68,15 @@ def load_peaks() -> dict:
         return {"hbm_gbs": 6650.0, "src": "fallback"}
 
 
-NVLINK_GBS = 770.0  # measured peer copy per direction (B200_PROFILING.md)
+NVLINK_GBS = 770.0  # measured single-peer SM pull, GB/s per direction (profiles/r02_nvlink_probe_2gpu.jsonl)
+# every GPU pulling from every peer at once (the TAR exchange pattern), GB/s in
+# per GPU, wall clock (profiles/r02_nvlink_probe_{2,4}gpu.jsonl); the roofline's
+# NVLink denominator where measured, else the single-peer figure
+NVLINK_ALLPEER_GBS = {2: 646.1, 4: 606.4}
+
+
+def nvlink_peak(n: int) -> float:
+    return NVLINK_ALLPEER_GBS.get(n, NVLINK_GBS)
 
 
 # ------------------------------------------------------------ clocks
@@ -437,8 +445,9 @@ def run_ours(args):
     achieved = class_bytes(dom) / (dom_ms * 1e-3) / 1e9
     if multi and dom in ("aggregate", "dec_first", "fused"):
         nv_ach = class_bytes(dom, nvlink=True) / (dom_ms * 1e-3) / 1e9
-        roof = {"bound": "nvlink", "achieved": round(nv_ach, 1), "peak": NVLINK_GBS, "unit": "GB/s",
-                "frac": round(nv_ach / NVLINK_GBS, 4), "kernel": dom, "peak_src": "measured peer copy",
+        roof = {"bound": "nvlink", "achieved": round(nv_ach, 1), "peak": nvlink_peak(n_workers), "unit": "GB/s",
+                "frac": round(nv_ach / nvlink_peak(n_workers), 4), "kernel": dom,
+                "peak_src": "measured all-peer SM pull" if n_workers in NVLINK_ALLPEER_GBS else "measured single-peer pull",
                 "hbm_achieved": round(achieved, 1), "traffic": None}
     else:
         roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
@@ -464,7 +473,7 @@ def run_ours(args):
     # whole-step roofline: max(HBM_alg/HBM, NVL/NVLink)
     hbm_alg, nvl = step_alg_bytes(buckets, n_workers, s_in, s_out, ht)
     hbm_alg *= per_rank_workers
-    t_roof = max(hbm_alg / (peaks["hbm_gbs"] * 1e9), (nvl / (NVLINK_GBS * 1e9)) if multi else 0.0)
+    t_roof = max(hbm_alg / (peaks["hbm_gbs"] * 1e9), (nvl / (nvlink_peak(n_workers) * 1e9)) if multi else 0.0)
     step_roof = {"t_roof_ms": round(t_roof * 1e3, 4), "frac": round(t_roof * 1e3 / ms_per_step, 4),
                  "hbm_alg_bytes": hbm_alg, "nvlink_bytes_per_dir": nvl if multi else 0}
 

@@ -258,7 +258,7 @@ template <int T, bool STRIDED, int SK, class Snk, int CBW, int BAR = 0, int TID_
 __device__ __forceinline__ void tma_tile(const TmaMaps* maps, const CUtensorMap* dst, const TmaArgs& a,
                                          const typename Snk::B& d, int worker, uint8_t* gotw, int64_t t,
                                          unsigned char* sb, Refill&& refill, Epi&& epi = Epi{},
-                                         bool all_kept = false) {
+                                         bool all_kept = false, const float* radd = nullptr) {
   constexpr int CB = STRIDED ? CBW : 0;  // untransformed column bits (8 or 32 columns)
   constexpr int CM = (1 << CB) - 1;
   constexpr RPlan P = make_rplan(T, CB);
@@ -338,6 +338,12 @@ __device__ __forceinline__ void tma_tile(const TmaMaps* maps, const CUtensorMap*
                        __int_as_float(__float_as_int(q4.w) ^ ((~sw & 8u) << 28)));
     } else {
       q4 = *reinterpret_cast<const float4*>(tile + i);
+      if (radd) {  // contiguous TS_BUF: a pre-accumulated sum of other tiles (linearity)
+        q4.x += radd[4 * m];
+        q4.y += radd[4 * m + 1];
+        q4.z += radd[4 * m + 2];
+        q4.w += radd[4 * m + 3];
+      }
     }
     v[4 * m] = q4.x;
     v[4 * m + 1] = q4.y;
@@ -620,6 +626,10 @@ __global__ void __launch_bounds__(1 << (T - 5), T == 13 ? 2 : 1) tma_mean_kernel
     for (int s = 0; s < kStages; ++s) issue(s, s);
   double acc[32];
   uint32_t cnt[8];  // count byte per entry (a thread's entries 4c..4c+3 in cnt[c])
+  float vacc[32];   // clean tiles: running fp32 sum of the first-pass tiles (round-A layout)
+  bool clean = false;
+  constexpr RPlan P0 = make_rplan(T, 0);
+  const int b0 = thread_base<T>(P0, 0, tid);
 #pragma unroll
   for (int j = 0; j < 32; ++j) acc[j] = 0.0;
   const float scale = ma.scale;
@@ -636,7 +646,51 @@ __global__ void __launch_bounds__(1 << (T - 5), T == 13 ? 2 : 1) tma_mean_kernel
     const uint32_t e0 = (uint32_t)(g0 - ((int64_t)j << ma.shard_shift));
     // per-entry masks only for a peer with a lost packet over this tile
     const bool masked = w != owner && !packets_all_kept(ma.m.row(0, owner, w), e0, 1u << T, ma.m);
+    if (w == 0) {  // a clean tile: every peer's packets over it arrived at the owner
+      clean = true;
+      for (int i = 0; i < NW; ++i)
+        if (i != owner && !packets_all_kept(ma.m.row(0, owner, i), e0, 1u << T, ma.m)) clean = false;
+    }
     mbar_wait(&full[s], (uint32_t)((k / kStages) & 1));
+    if (clean) {
+      // linearity: the mean of the n transformed tiles is the transform of
+      // their sum, so a clean tile is summed as it arrives (first-pass fp32
+      // values) and transformed once, by the last worker's job (n-fold less
+      // FWHT work; float32 sum, within the 1e-5 codec tolerance)
+      float* const tile = reinterpret_cast<float*>(base + (size_t)s * SB);
+      if (w < NW - 1) {
+#pragma unroll
+        for (int m = 0; m < 8; ++m) {
+          const float4 q4 = *reinterpret_cast<const float4*>(tile + b0 + roff(P0, 0, 4 * m));
+          vacc[4 * m] = (w == 0 ? 0.f : vacc[4 * m]) + q4.x;
+          vacc[4 * m + 1] = (w == 0 ? 0.f : vacc[4 * m + 1]) + q4.y;
+          vacc[4 * m + 2] = (w == 0 ? 0.f : vacc[4 * m + 2]) + q4.z;
+          vacc[4 * m + 3] = (w == 0 ? 0.f : vacc[4 * m + 3]) + q4.w;
+        }
+        __syncthreads();  // every thread has read the stage
+        if (tid == 0) issue(k + kStages, s);
+        continue;
+      }
+      tma_tile<T, false, TS_BUF, SnkBuf, 3>(
+          nullptr, nullptr, a, nosnk, w, nullptr, t, base + (size_t)s * SB, [&]() { issue(k + kStages, s); },
+          [&](const float (&v)[32], int b2) {
+            float* const out = ma.agg + g0;
+            const float inv_n = 1.f / (float)NW;  // exact: NW is a power of two
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) {
+              const int i = b2 + roff(P, LR, VW * q);
+              float r[VW];
+#pragma unroll
+              for (int c = 0; c < VW; ++c) r[c] = v[VW * q + c] * scale * inv_n;
+              if constexpr (VW == 4)
+                st4(out + i, make_float4(r[0], r[1], r[2], r[3]));
+              else
+                *reinterpret_cast<float2*>(out + i) = make_float2(r[0], r[1]);
+            }
+          },
+          false, vacc);
+      continue;
+    }
     tma_tile<T, false, TS_BUF, SnkBuf, 3>(
         nullptr, nullptr, a, nosnk, w, nullptr, t, base + (size_t)s * SB, [&]() { issue(k + kStages, s); },
         [&](const float (&v)[32], int b2) {
