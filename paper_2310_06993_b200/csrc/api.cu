@@ -334,6 +334,7 @@ int try_tma(int cls, const PassGeom& pg, int nlog, int worker, int nworkers, con
       a.m = src.m;
       a.got = src.got;
       a.dim = src.dim;
+      a.tile_ok2 = (pg.cb == 0 && pg.lo == 0) ? src.tile_ok2 : nullptr;  // tiles of the fast plan's contiguous pass
     }
     if (pg.cb == 3 || pg.cb == 5) {  // strided: tensor boxes in, tensor boxes out
       if constexpr (kEnc) {
@@ -907,7 +908,7 @@ extern "C" {
 
 // -------------------------------------------------- TAR, n workers, one GPU
 struct LocalLayout {
-  size_t y, a, signs, signs_t, bitmap, counts, total;
+  size_t y, a, signs, signs_t, bitmap, counts, tileok, total;
   int64_t dim, smax, astride, pw;
 };
 
@@ -931,6 +932,8 @@ static LocalLayout local_layout(int n, int64_t L, int ht, int epp) {
   off = align_up(off + (size_t)2 * n * n * l.pw * 4, 256);
   l.counts = off;
   off = align_up(off + (size_t)2 * n * 8, 256);
+  l.tileok = off;  // per-tile mask summaries of the fast plan: 2 x (dim / 2^13) words
+  off = align_up(off + (size_t)2 * ((l.dim >> 13) + 1) * 4, 256);
   l.total = off;
   return l;
 }
@@ -1090,6 +1093,13 @@ int tar_local_impl(const void* const* x, void* const* out, int n, int64_t L, int
   }
   const uint32_t* cbits = nullptr;
   if ((rc = setup_masks(pa, masks, dim, n, r, epp, bitmap, counts, 0, n, &cbits))) return rc;
+  uint32_t* const tile_ok = fast ? (uint32_t*)(ws + lay.tileok) : nullptr;
+  if (tile_ok) {  // per-tile summaries of the masks, cleared by prep where a packet is lost
+    pa.tile_ok = tile_ok;
+    pa.tile_shift = fp.contig.ks;
+    pa.ntiles = dim >> fp.contig.ks;
+    CK(cudaMemsetAsync(tile_ok, 0xFF, (size_t)2 * pa.ntiles * 4, st));
+  }
   if ((rc = launch_prep(pa, st))) return rc;
   MaskView mv{cbits, pa.pw, n, epp, make_divider((uint32_t)epp)};
 
@@ -1146,10 +1156,12 @@ int tar_local_impl(const void* const* x, void* const* out, int n, int64_t L, int
     ma.r = r;
     ma.shard_shift = log2_exact(sh.base);
     ma.m = mv;
+    ma.tile_ok1 = tile_ok;
     rc = fp.contig.ks == 13 ? launch_mean_n<13>(ta, ma, st) : launch_mean_n<14>(ta, ma, st);
     if (rc) return rc;
     // 4. contiguous decode pass with the stage-2 receive, A -> Y
     for (int o = 0; o < n; ++o) ga.A[o] = A + sh.off(owned_shard(o, r, n));
+    ga.tile_ok2 = tile_ok + (dim >> fp.contig.ks);
     SrcBuf buf;
     memset(&buf, 0, sizeof(buf));
     for (int w = 0; w < n; ++w) buf.y[w] = mid.y[w];

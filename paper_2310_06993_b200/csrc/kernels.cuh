@@ -209,6 +209,13 @@ struct PrepArgs {
   int dst_lo, dst_hi;
   int64_t mask_threads;
   unsigned long long* counts;  // [2][n] received entries per (stage,dst)
+  // optional per-tile summaries of the masks (tiles of 2^tile_shift vector
+  // entries, preset to all ones): tile_ok[stage * ntiles + t] bit i is
+  // cleared when a packet over tile t is lost -- stage 1: from sender i to
+  // the tile's owner; stage 2: from the tile's owner to receiver i
+  uint32_t* tile_ok;
+  int tile_shift;
+  int64_t ntiles;
 };
 
 constexpr int kSignsPerThread = 128;
@@ -316,6 +323,19 @@ __device__ __forceinline__ void prep_item(const PrepArgs& a, int64_t t) {
   } else {
     bits = cnt >= 32 ? 0xffffffffu : (cnt > 0 ? ((1u << cnt) - 1u) : 0u);
     a.bitmap_out[idx] = bits;
+  }
+  if (a.tile_ok && cnt > 0) {
+    uint32_t lost = ~bits & (cnt >= 32 ? 0xffffffffu : ((1u << cnt) - 1u));
+    const int64_t off = a.sh.off(j);
+    const uint32_t bit = 1u << (stage == 0 ? src : dst);
+    while (lost) {  // rare: one atomic per lost packet per tile it touches
+      const int b = __ffs(lost) - 1;
+      lost &= lost - 1;
+      const int64_t e_lo = off + (p0 + b) * a.epp;
+      const int64_t e_hi = off + ((p0 + b + 1) * a.epp < len ? (p0 + b + 1) * a.epp : len) - 1;
+      for (int64_t tt = e_lo >> a.tile_shift; tt <= (e_hi >> a.tile_shift); ++tt)
+        atomicAnd(a.tile_ok + stage * a.ntiles + tt, ~bit);
+    }
   }
   if (bits) {
     unsigned long long e = (unsigned long long)__popc(bits) * (unsigned long long)a.epp;
@@ -442,6 +462,7 @@ struct SrcGather {
   uint8_t* got;  // optional [n][dim]
   int64_t dim;
   int pow2_shift;  // log2(shard length) when all shards are one power of two, else -1
+  const uint32_t* tile_ok2;  // optional stage-2 tile summaries (TMA contiguous passes)
   struct B {
     const SrcGather* p;  // param space
     int q;

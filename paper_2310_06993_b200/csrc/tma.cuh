@@ -61,6 +61,7 @@ struct TmaArgs {
   MaskView m;
   uint8_t* got;  // optional [worker][dim]
   int64_t dim;
+  const uint32_t* tile_ok2;  // optional stage-2 tile summaries (PrepArgs.tile_ok + ntiles)
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -227,6 +228,7 @@ __device__ __forceinline__ bool gather_tile_all_kept(const TmaArgs& a, int q, in
   const int j = (int)(g0 >> a.shard_shift);
   const int owner = shard_owner(j, a.r, a.n);
   if (owner == q) return true;
+  if (a.tile_ok2) return (__ldg(a.tile_ok2 + t) >> q) & 1u;  // prep's per-tile summary
   return packets_all_kept(a.m.row(1, q, owner), (uint32_t)(g0 - ((int64_t)j << a.shard_shift)), 1u << T, a.m);
 }
 
@@ -591,6 +593,7 @@ struct MeanArgs {
   float scale;  // 1/sqrt(dim)
   int n, r, shard_shift;
   MaskView m;   // stage-1 rows (stage 0 of the bitmap layout)
+  const uint32_t* tile_ok1;  // stage-1 tile summaries (PrepArgs.tile_ok): bit i = sender i's packets all arrived
 };
 
 // two CTAs per SM for 256-thread tiles (T = 13: <= 128 registers), one for
@@ -624,14 +627,21 @@ __global__ void __launch_bounds__(1 << (T - 5), T == 13 ? 2 : 1) tma_mean_kernel
   };
   if (tid == 0)
     for (int s = 0; s < kStages; ++s) issue(s, s);
-  double acc[32];
+  // Per tile, C = the ranks whose packets over it all arrived at the owner
+  // (the owner included).  By linearity the C tiles are summed as they
+  // arrive (first-pass values, fp32) and transformed ONCE, by the job of the
+  // last rank in C; each remaining rank (a lost packet over the tile) is
+  // transformed and accumulated under its per-entry masks.  A 1% drop rate
+  // leaves most tiles with |C| = n (one transform instead of n).  fp32
+  // accumulation (the RHT-on path is float32 anyway; the tolerance is 1e-5).
+  float acc[32];
   uint32_t cnt[8];  // count byte per entry (a thread's entries 4c..4c+3 in cnt[c])
-  float vacc[32];   // clean tiles: running fp32 sum of the first-pass tiles (round-A layout)
-  bool clean = false;
+  float vacc[32];   // running sum of the C tiles (round-A layout)
+  uint32_t cset = 0;
+  int last_c = 0;
+  constexpr uint32_t kAllW = (NW >= 32) ? 0xffffffffu : ((1u << NW) - 1u);
   constexpr RPlan P0 = make_rplan(T, 0);
   const int b0 = thread_base<T>(P0, 0, tid);
-#pragma unroll
-  for (int j = 0; j < 32; ++j) acc[j] = 0.0;
   const float scale = ma.scale;
   const SnkBuf::B nosnk{nullptr, 1.f};
   for (int64_t k = 0;; ++k) {
@@ -644,82 +654,51 @@ __global__ void __launch_bounds__(1 << (T - 5), T == 13 ? 2 : 1) tma_mean_kernel
     const int j = (int)(g0 >> ma.shard_shift);
     const int owner = shard_owner(j, ma.r, NW);
     const uint32_t e0 = (uint32_t)(g0 - ((int64_t)j << ma.shard_shift));
-    // per-entry masks only for a peer with a lost packet over this tile
-    const bool masked = w != owner && !packets_all_kept(ma.m.row(0, owner, w), e0, 1u << T, ma.m);
-    if (w == 0) {  // a clean tile: every peer's packets over it arrived at the owner
-      clean = true;
-      for (int i = 0; i < NW; ++i)
-        if (i != owner && !packets_all_kept(ma.m.row(0, owner, i), e0, 1u << T, ma.m)) clean = false;
+    if (w == 0) {
+      cset = (__ldg(ma.tile_ok1 + t) | (1u << owner)) & kAllW;
+      last_c = 31 - __clz(cset);
+      const uint32_t c0 = (uint32_t)__popc(cset) * 0x01010101u;
+#pragma unroll
+      for (int c = 0; c < 8; ++c) cnt[c] = c0;
+#pragma unroll
+      for (int jj = 0; jj < 32; ++jj) acc[jj] = 0.f;
     }
+    const bool in_c = (cset >> w) & 1u;
     mbar_wait(&full[s], (uint32_t)((k / kStages) & 1));
-    if (clean) {
-      // linearity: the mean of the n transformed tiles is the transform of
-      // their sum, so a clean tile is summed as it arrives (first-pass fp32
-      // values) and transformed once, by the last worker's job (n-fold less
-      // FWHT work; float32 sum, within the 1e-5 codec tolerance)
-      float* const tile = reinterpret_cast<float*>(base + (size_t)s * SB);
-      if (w < NW - 1) {
+    float* const tile = reinterpret_cast<float*>(base + (size_t)s * SB);
+    if (in_c && w != last_c) {  // add the raw tile to the C sum, no transform
 #pragma unroll
-        for (int m = 0; m < 8; ++m) {
-          const float4 q4 = *reinterpret_cast<const float4*>(tile + b0 + roff(P0, 0, 4 * m));
-          vacc[4 * m] = (w == 0 ? 0.f : vacc[4 * m]) + q4.x;
-          vacc[4 * m + 1] = (w == 0 ? 0.f : vacc[4 * m + 1]) + q4.y;
-          vacc[4 * m + 2] = (w == 0 ? 0.f : vacc[4 * m + 2]) + q4.z;
-          vacc[4 * m + 3] = (w == 0 ? 0.f : vacc[4 * m + 3]) + q4.w;
-        }
-        __syncthreads();  // every thread has read the stage
-        if (tid == 0) issue(k + kStages, s);
-        continue;
+      for (int m = 0; m < 8; ++m) {
+        const float4 q4 = *reinterpret_cast<const float4*>(tile + b0 + roff(P0, 0, 4 * m));
+        const bool first = w == (__ffs(cset) - 1);
+        vacc[4 * m] = (first ? 0.f : vacc[4 * m]) + q4.x;
+        vacc[4 * m + 1] = (first ? 0.f : vacc[4 * m + 1]) + q4.y;
+        vacc[4 * m + 2] = (first ? 0.f : vacc[4 * m + 2]) + q4.z;
+        vacc[4 * m + 3] = (first ? 0.f : vacc[4 * m + 3]) + q4.w;
       }
-      tma_tile<T, false, TS_BUF, SnkBuf, 3>(
-          nullptr, nullptr, a, nosnk, w, nullptr, t, base + (size_t)s * SB, [&]() { issue(k + kStages, s); },
-          [&](const float (&v)[32], int b2) {
-            float* const out = ma.agg + g0;
-            const float inv_n = 1.f / (float)NW;  // exact: NW is a power of two
-#pragma unroll
-            for (int q = 0; q < NQ; ++q) {
-              const int i = b2 + roff(P, LR, VW * q);
-              float r[VW];
-#pragma unroll
-              for (int c = 0; c < VW; ++c) r[c] = v[VW * q + c] * scale * inv_n;
-              if constexpr (VW == 4)
-                st4(out + i, make_float4(r[0], r[1], r[2], r[3]));
-              else
-                *reinterpret_cast<float2*>(out + i) = make_float2(r[0], r[1]);
-            }
-          },
-          false, vacc);
+      __syncthreads();  // every thread has read the stage
+      if (tid == 0) issue(k + kStages, s);
       continue;
     }
+    const bool sum_job = in_c;  // the last C rank: transform of the C sum
+    const bool has_sum = sum_job && __popc(cset) > 1;
     tma_tile<T, false, TS_BUF, SnkBuf, 3>(
         nullptr, nullptr, a, nosnk, w, nullptr, t, base + (size_t)s * SB, [&]() { issue(k + kStages, s); },
         [&](const float (&v)[32], int b2) {
-          uint32_t kk[NQ];
+          if (sum_job) {
 #pragma unroll
-          for (int q = 0; q < NQ; ++q) kk[q] = (1u << VW) - 1u;
-          if (masked) {
+            for (int jj = 0; jj < 32; ++jj) acc[jj] += v[jj] * scale;
+          } else {
             const uint32_t* row = ma.m.row(0, owner, w);
 #pragma unroll
             for (int q = 0; q < NQ; ++q) {
               const uint32_t e = e0 + (uint32_t)(b2 + roff(P, LR, VW * q));
-              kk[q] = (keep4(row, e & ~3u, ma.m) >> (e & 3u)) & ((1u << VW) - 1u);
+              const uint32_t kk = (keep4(row, e & ~3u, ma.m) >> (e & 3u)) & ((1u << VW) - 1u);
+#pragma unroll
+              for (int c = 0; c < VW; ++c) acc[VW * q + c] += ((kk >> c) & 1u) ? v[VW * q + c] * scale : 0.f;
+              cnt[(VW * q) / 4] += nibble_bytes(kk) << (8 * ((VW * q) % 4));
             }
           }
-          // fp64 accumulation in ascending worker order (misses add 0.0)
-#pragma unroll
-          for (int q = 0; q < NQ; ++q) {
-#pragma unroll
-            for (int c = 0; c < VW; ++c) {
-              const double x = (double)(v[VW * q + c] * scale);
-              acc[VW * q + c] += ((kk[q] >> c) & 1u) ? x : 0.0;
-            }
-          }
-          if (w == 0) {
-#pragma unroll
-            for (int c = 0; c < 8; ++c) cnt[c] = 0u;
-          }
-#pragma unroll
-          for (int q = 0; q < NQ; ++q) cnt[(VW * q) / 4] += nibble_bytes(kk[q]) << (8 * ((VW * q) % 4));
           if (w == NW - 1) {
             float* const out = ma.agg + g0;
 #pragma unroll
@@ -729,8 +708,10 @@ __global__ void __launch_bounds__(1 << (T - 5), T == 13 ? 2 : 1) tma_mean_kernel
 #pragma unroll
               for (int c = 0; c < VW; ++c) {
                 const int jj = VW * q + c;
-                r[c] = mean_of(acc[jj], (double)((cnt[jj / 4] >> (8 * (jj % 4))) & 0xffu));
-                acc[jj] = 0.0;
+                const uint32_t cn = (cnt[jj / 4] >> (8 * (jj % 4))) & 0xffu;
+                // a power-of-two count divides exactly; others round once
+                r[c] = (cn & (cn - 1)) == 0 ? acc[jj] * __int_as_float((127 - (__ffs(cn) - 1)) << 23)
+                                            : __fdiv_rn(acc[jj], (float)cn);
               }
               if constexpr (VW == 4)
                 st4(out + i, make_float4(r[0], r[1], r[2], r[3]));
@@ -738,7 +719,8 @@ __global__ void __launch_bounds__(1 << (T - 5), T == 13 ? 2 : 1) tma_mean_kernel
                 *reinterpret_cast<float2*>(out + i) = make_float2(r[0], r[1]);
             }
           }
-        });
+        },
+        false, has_sum ? vacc : nullptr);
   }
 }
 
