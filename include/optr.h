@@ -284,7 +284,9 @@ int64_t optr_fused_unit_entries(int64_t dim, int n);
                                with the stage-1 mean (wire never written)   */
 #define OPTR_K_FUSED 12     /* multi-GPU: contiguous encode + stage 1 + stage 2
                                + contiguous decode, one persistent launch  */
-#define OPTR_K_CLASSES 13
+#define OPTR_K_SMALL 13     /* multi-GPU buckets <= 2^20 entries: the whole call
+                               in one cooperative launch                    */
+#define OPTR_K_CLASSES 14
 /* Enable (1) / disable (0) CUDA-event timing of every kernel launch. */
 int optr_timing_enable(int on);
 /* Debug: event trace of the fused multi-GPU kernel into a device buffer of

@@ -30,7 +30,7 @@ MAX_WORKERS = 16
 
 # kernel classes of optr_timing_collect (optr.h OPTR_K_*)
 K_NAMES = ["prep", "enc_first", "enc_mid", "enc_last", "aggregate", "dec_first", "dec_mid",
-           "dec_last", "assemble", "barrier", "other", "enc_mean", "fused"]
+           "dec_last", "assemble", "barrier", "other", "enc_mean", "fused", "small"]
 
 
 class optr_mask_spec(ctypes.Structure):

@@ -13,6 +13,7 @@
 #include "../../include/optr.h"
 #include "kernels.cuh"
 #include "tma.cuh"
+#include "small.cuh"
 #include "internal.h"
 
 #include <cudaTypedefs.h>
@@ -1276,6 +1277,14 @@ struct optr_comm_s {
   bool done_recorded[2];
   uint64_t calls;
   int fused_grid;  // CTAs of the persistent fused kernel (0 = SMs x occupancy)
+  // small-bucket path (tar_small_kernel): wire Y | aggregate A | flags
+  // [2][kMaxW] in the symmetric block, signs | bitmap | counts | barrier
+  // counter in `slocal`; 0 bytes when max_len is below the small range
+  int64_t small_dim;  // largest small-path dim (0 = off)
+  size_t off_sy, off_sa, off_sf;
+  char* slocal;
+  size_t s_signs, s_bitmap, s_counts, s_bar;
+  unsigned long long s_epoch, s_bar_base;
 };
 
 size_t optr_comm_handle_bytes(void) { return sizeof(cudaIpcMemHandle_t); }
@@ -1311,6 +1320,16 @@ int optr_comm_create(optr_comm* out, int device, int rank, int n, int64_t max_le
     c->off_gf[p] = off;
     off = align_up(off + (size_t)4 * (c->max_dim >> 13 > 0 ? c->max_dim >> 13 : 1) * 4, 1024);
   }
+  c->small_dim = c->max_dim < (1LL << kSmallMinLog) ? 0
+                 : (c->max_dim < (1LL << kSmallMaxLog) ? c->max_dim : (1LL << kSmallMaxLog));
+  if (c->small_dim) {
+    c->off_sy = off;
+    off = align_up(off + (size_t)c->small_dim * 4, 1024);
+    c->off_sa = off;
+    off = align_up(off + (size_t)(c->small_dim / 2) * 4, 1024);  // a shard, n >= 2
+    c->off_sf = off;
+    off = align_up(off + (size_t)2 * kMaxW * 8, 1024);
+  }
   c->sym_bytes = off;
   int64_t pw = mask_words(c->max_dim, n, 1);  // epp >= 1 bound
   off = 0;
@@ -1325,14 +1344,29 @@ int optr_comm_create(optr_comm* out, int device, int rank, int n, int64_t max_le
   c->off_ctr = off;
   off = align_up(off + 4 * sizeof(unsigned int), 256);
   c->local_bytes = off;
+  size_t soff = 0;
+  if (c->small_dim) {
+    const int64_t spw = mask_words(c->small_dim, n, 1);
+    c->s_signs = soff;
+    soff = align_up(soff + (size_t)(c->small_dim / 32) * 4, 256);
+    c->s_bitmap = soff;
+    soff = align_up(soff + (size_t)2 * n * n * spw * 4, 256);
+    c->s_counts = soff;  // two call parities of [2][n]
+    soff = align_up(soff + (size_t)2 * 2 * n * 8, 256);
+    c->s_bar = soff;
+    soff = align_up(soff + 8, 256);
+  }
   if (cudaMalloc((void**)&c->sym, c->sym_bytes) != cudaSuccess ||
-      cudaMalloc((void**)&c->local, 2 * c->local_bytes) != cudaSuccess) {
+      cudaMalloc((void**)&c->local, 2 * c->local_bytes) != cudaSuccess ||
+      (soff && cudaMalloc((void**)&c->slocal, soff) != cudaSuccess)) {
     cudaFree(c->sym);
+    cudaFree(c->local);
     free(c);
     return OPTR_ENOMEM;
   }
   CK(cudaMemset(c->sym, 0, c->sym_bytes));
   CK(cudaMemset(c->local, 0, 2 * c->local_bytes));
+  if (soff) CK(cudaMemset(c->slocal, 0, soff));
   for (int p = 0; p < 2; ++p) c->fused_ctr[p] = (unsigned int*)(c->local + p * c->local_bytes + c->off_ctr);
   // prep (ALU-heavy, off the critical path) at the lowest priority, the call
   // streams at the highest: the block scheduler gives prep leftover SMs
@@ -1385,6 +1419,7 @@ int optr_comm_destroy(optr_comm c) {
     if (c->opened[i]) cudaIpcCloseMemHandle(c->peer[i]);
   cudaFree(c->sym);
   cudaFree(c->local);
+  if (c->slocal) cudaFree(c->slocal);
   cudaStreamDestroy(c->pstream);
   for (int p = 0; p < 2; ++p) {
     cudaEventDestroy(c->prep_ready[p]);
@@ -1480,6 +1515,7 @@ int optr_tar_bounded(optr_comm c, const void* x, void* out, int64_t L, int dtype
 }  // extern "C"
 
 namespace {
+void* g_small_trace = nullptr;  // optr_debug_trace with per_cta < 0: small-kernel phase stamps
 void* g_fused_trace = nullptr;  // optr_debug_trace
 int g_fused_trace_cap = 0;
 // OPTR_FUSED=0 keeps the barrier-separated encode / aggregate / decode path.
@@ -1559,6 +1595,75 @@ int launch_fused_t(const TmaArgs& ae, const TmaArgs& ad, const SnkBuf& se, const
   return launch_check(kern, "tma_fused", T, 0, grid, 1, threads, smem);
 }
 
+bool small_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("OPTR_SMALL");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
+template <int K>
+int launch_small_t(const SmallArgs& a, int grid, cudaStream_t st) {
+  auto kern = tar_small_kernel<K>;
+  const size_t smem = sizeof(float) * (size_t)pad(1 << kSmallT);
+  int rc = set_smem_attr(kern, smem);
+  if (rc) return rc;
+  cudaLaunchConfig_t cfg;
+  memset(&cfg, 0, sizeof(cfg));
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(1u << (kSmallT - 5));
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;  // grid barriers: every CTA co-resident
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  static const int coop = [] {
+    const char* e = getenv("OPTR_SMALL_COOP");
+    return (e && e[0] == '0') ? 0 : 1;
+  }();
+  cfg.numAttrs = coop;
+  KScope ks(OPTR_K_SMALL, st);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, a);
+  if (e != cudaSuccess) {
+    fprintf(stderr, "optr: tar_small_kernel<%d> grid=%d launch failed: %s\n", K, grid, cudaGetErrorString(e));
+    return OPTR_ECUDA;
+  }
+  return OPTR_OK;
+}
+
+int launch_small(int K, const SmallArgs& a, int grid, cudaStream_t st) {
+  switch (K) {
+    case 13: return launch_small_t<13>(a, grid, st);
+    case 14: return launch_small_t<14>(a, grid, st);
+    case 15: return launch_small_t<15>(a, grid, st);
+    case 16: return launch_small_t<16>(a, grid, st);
+    case 17: return launch_small_t<17>(a, grid, st);
+    case 18: return launch_small_t<18>(a, grid, st);
+    case 19: return launch_small_t<19>(a, grid, st);
+    case 20: return launch_small_t<20>(a, grid, st);
+    default: return OPTR_EINVAL;
+  }
+}
+
+// CTAs of the small kernel: one per SM (stage 1's NVLink loads, the signs
+// and the masks spread over the whole grid; the tile passes use D/2^13)
+int small_grid(int K) {
+  static int cap = 0;
+  if (!cap) {
+    int dev = 0, nsm = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    cap = nsm > 0 ? nsm : 148;
+    const char* e = getenv("OPTR_SMALL_GRID");
+    if (e && atoi(e) > 0 && atoi(e) < cap) cap = atoi(e);
+  }
+  (void)K;
+  return cap;
+}
+
 int launch_fused(int T, const TmaArgs& ae, const TmaArgs& ad, const SnkBuf& se, const SnkBuf& sd,
                  const FusedArgs& f, cudaStream_t st) {
   // (a 3-stage E/D ring for T = 13 measured slower: 0.504 vs 0.490 ms/step)
@@ -1599,6 +1704,63 @@ static int tar_enqueue(optr_comm c, const void* x, void* out, int64_t L, int dty
   const int me = c->rank;
   const int r = ((rotation % n) + n) % n;
   const int par = (int)(c->calls++ & 1);
+  // ---- small buckets (2^13..2^20 entries, power-of-two n <= 8): the whole
+  // call is one cooperative kernel (small.cuh).  Serialised after the
+  // previous call, on the caller's stream (no stream hop); the next call's
+  // fused kernel waits for it.
+  const Shards sh = make_shards(dim, n);
+  const int klog = ht ? log2_exact(dim) : 0;
+  if (ht && small_enabled() && c->small_dim && dim <= c->small_dim && klog >= kSmallMinLog &&
+      klog <= kSmallMaxLog && n <= kSmallMaxRanks && (n & (n - 1)) == 0 && deadline_ns == 0 && !stats &&
+      !cut_units) {
+    const cudaStream_t st = caller;
+    if (c->done_recorded[par ^ 1]) CK(cudaStreamWaitEvent(st, c->done[par ^ 1], 0));
+    char* const sl = c->slocal;
+    SmallArgs a;
+    memset(&a, 0, sizeof(a));
+    unsigned long long* const scounts = (unsigned long long*)(sl + c->s_counts);
+    uint32_t* const sbitmap = (uint32_t*)(sl + c->s_bitmap);
+    const uint32_t* cb = nullptr;
+    if ((rc = setup_masks(a.pa, masks, dim, n, r, epp, sbitmap, scounts, me, me + 1, &cb))) return rc;
+    if ((rc = ensure_device_init())) return rc;
+    const Pcg sp = sign_pcg(derive_seed(job_seed, bucket_id, generation));
+    a.signs = (uint32_t*)(sl + c->s_signs);
+    a.sign_state = sp.state;
+    a.sign_inc = sp.inc;
+    a.x = x;
+    a.out = out;
+    a.dtype_in = dtype_in;
+    a.dtype_out = dtype_out;
+    a.L = L;
+    a.dim = dim;
+    for (int i = 0; i < n; ++i) {
+      a.Y[i] = (float*)(c->peer[i] + c->off_sy);
+      a.A[i] = (float*)(c->peer[i] + c->off_sa);
+      a.flags[i] = (unsigned long long*)(c->peer[i] + c->off_sf);
+    }
+    const int grid = small_grid(klog);
+    a.bar = (unsigned long long*)(sl + c->s_bar);
+    a.bar_base = c->s_bar_base;
+    a.epoch = ++c->s_epoch;
+    a.counts = scounts + (c->s_epoch & 1) * 2 * n;  // zeroed by the previous call (or at create)
+    a.counts_next = scounts + ((c->s_epoch + 1) & 1) * 2 * n;
+    a.received_out = (unsigned long long*)received_out;
+    a.m = MaskView{cb, a.pa.pw, n, epp, make_divider((uint32_t)epp)};
+    a.n = n;
+    a.me = me;
+    a.r = r;
+    a.shard_shift = log2_exact(sh.base);
+    a.watchdog_ns = watchdog_ns();
+    a.trace = (unsigned long long*)g_small_trace;
+    if ((rc = launch_small(klog, a, grid, st))) return rc;
+    c->s_bar_base += (unsigned long long)kSmallBarriers * grid;
+    CK(cudaEventRecord(c->done[par], st));
+    c->done_recorded[par] = true;
+    CK(cudaEventRecord(c->fused_done[par], st));  // the next fused kernel starts after it
+    c->fused_recorded[par] = true;
+    return OPTR_OK;
+  }
+
   // this call's kernels run on the parity's work stream, after the caller's
   // prior work (inputs ready)
   const cudaStream_t st = c->ws[par];
@@ -1616,8 +1778,6 @@ static int tar_enqueue(optr_comm c, const void* x, void* out, int64_t L, int dty
     Ap[i] = (float*)(c->peer[i] + c->off_a[par]);
     Gp[i] = (float*)(c->peer[i] + c->off_g[par]);
   }
-  Shards sh = make_shards(dim, n);
-
   // ---- fused path: strided encode pass, then ONE persistent kernel for the
   // contiguous encode pass + stage 1 + stage 2 + contiguous decode pass with
   // per-tile flags over NVLink (no barriers), then the strided decode pass.
@@ -1887,6 +2047,10 @@ int64_t optr_fused_unit_entries(int64_t dim, int n) {
 
 // ------------------------------------------------------ instrumentation
 int optr_debug_trace(void* dev_buf, int64_t per_cta) {
+  if (per_cta < 0) {  // small-bucket kernel: [64][16] u64 phase stamps
+    g_small_trace = dev_buf;
+    return OPTR_OK;
+  }
   g_fused_trace = dev_buf;
   g_fused_trace_cap = (int)per_cta;
   return OPTR_OK;

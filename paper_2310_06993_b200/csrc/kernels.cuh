@@ -18,6 +18,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <type_traits>
+
 #include "../../include/optr.h"
 #include "pcg.h"
 
@@ -789,18 +791,30 @@ __host__ __device__ constexpr int64_t remap_c(int i) {
   return ((int64_t)(i >> CB) << LO) | (int64_t)(i & ((1 << CB) - 1));
 }
 
-template <int T, int CB, int LO, class Src, class Snk>
-__global__ void __launch_bounds__(1 << (T - 5)) rtile_kernel(PassGeom pg, int worker_base,
-                                                          const __grid_constant__ Src src,
-                                                          const __grid_constant__ Snk snk) {
+// Sources with a two-step load (raw4: every memory access, fix4: the math
+// on the loaded words) declare `static constexpr bool kSplit = true`.
+template <class S, class = void>
+struct split_load : std::false_type {};
+template <class S>
+struct split_load<S, std::enable_if_t<S::kSplit>> : std::true_type {};
+
+// Sinks with a two-step store (pre: the word a group of stores needs, e.g.
+// its sign word; store4w / store2w: the stores) declare kSplitStore.
+template <class S, class = void>
+struct split_store : std::false_type {};
+template <class S>
+struct split_store<S, std::enable_if_t<S::kSplitStore>> : std::true_type {};
+
+// One 2^T-entry tile t of a pass over vector bits [LO, LO + T - CB) with
+// 2^CB contiguous columns, by a CTA of 2^(T-5) threads (32 values each in
+// registers, rounds exchanged through `sm`, pad(2^T) floats).  Callable in a
+// loop: the leading barrier protects the previous tile's shared-memory reads.
+template <int T, int CB, int LO, class SB, class DB>
+__device__ __forceinline__ void rtile_do(SB& s, const DB& d, int64_t t, float* sm) {
   constexpr RPlan P = make_rplan(T, CB);
   constexpr int NR = P.nr;
   constexpr int KS = T - CB;
-  extern __shared__ float sm[];
   const int tid = threadIdx.x;
-  const int w = worker_base + blockIdx.y;
-  auto s = src.bind(w);
-  const auto d = snk.bind(w);
   const int b0 = thread_base<T>(P, 0, tid);
   const int b1 = NR > 1 ? thread_base<T>(P, 1, tid) : 0;
   const int b2 = NR > 2 ? thread_base<T>(P, 2, tid) : 0;
@@ -812,18 +826,35 @@ __global__ void __launch_bounds__(1 << (T - 5)) rtile_kernel(PassGeom pg, int wo
   float* const s1 = sm + pad(b1);
   float* const s2 = sm + pad(b2);
   float* const s3 = sm + pad(b3);
-  for (int64_t t = blockIdx.x; t < pg.ntiles; t += gridDim.x) {
+  {
     constexpr int CGB = LO - CB;
     const int64_t g0 = ((t >> CGB) << (LO + KS)) + ((t & ((1LL << CGB) - 1)) << CB);
     s.begin_tile(g0, g0 + remap_c<CB, LO>((1 << T) - 1));
     float v[32];
 #pragma unroll
-    for (int m = 0; m < 8; ++m) {
-      const float4 q = s.load4(g0 + r0 + remap_c<CB, LO>(roff(P, 0, 4 * m)));
-      v[4 * m] = q.x;
-      v[4 * m + 1] = q.y;
-      v[4 * m + 2] = q.z;
-      v[4 * m + 3] = q.w;
+    if constexpr (split_load<SB>::value) {
+      // latency-bound callers (the small-bucket kernel: one tile per CTA):
+      // all eight raw loads in flight before any result is used
+      typename SB::Raw raw[8];
+#pragma unroll
+      for (int m = 0; m < 8; ++m) raw[m] = s.raw4(g0 + r0 + remap_c<CB, LO>(roff(P, 0, 4 * m)));
+#pragma unroll
+      for (int m = 0; m < 8; ++m) {
+        const float4 q = s.fix4(g0 + r0 + remap_c<CB, LO>(roff(P, 0, 4 * m)), raw[m]);
+        v[4 * m] = q.x;
+        v[4 * m + 1] = q.y;
+        v[4 * m + 2] = q.z;
+        v[4 * m + 3] = q.w;
+      }
+    } else {
+#pragma unroll
+      for (int m = 0; m < 8; ++m) {
+        const float4 q = s.load4(g0 + r0 + remap_c<CB, LO>(roff(P, 0, 4 * m)));
+        v[4 * m] = q.x;
+        v[4 * m + 1] = q.y;
+        v[4 * m + 2] = q.z;
+        v[4 * m + 3] = q.w;
+      }
     }
     bfly32<P.xm[0]>(v);
     if constexpr (NR > 1) {
@@ -851,11 +882,26 @@ __global__ void __launch_bounds__(1 << (T - 5)) rtile_kernel(PassGeom pg, int wo
       for (int j = 0; j < 32; ++j) v[j] = s3[pad(roff(P, 3, j))];
       bfly32<P.xm[3]>(v);
     }
-    if constexpr (P.pos[LR][0] == 0 && P.pos[LR][1] == 1) {
+    if constexpr (P.pos[LR][0] == 0 && P.pos[LR][1] == 1 && split_store<DB>::value) {
+      uint32_t wd[8];  // every sink-side load in flight before the stores
+#pragma unroll
+      for (int m = 0; m < 8; ++m) wd[m] = d.pre(g0 + rl + remap_c<CB, LO>(roff(P, LR, 4 * m)));
+#pragma unroll
+      for (int m = 0; m < 8; ++m)
+        d.store4w(g0 + rl + remap_c<CB, LO>(roff(P, LR, 4 * m)),
+                  make_float4(v[4 * m], v[4 * m + 1], v[4 * m + 2], v[4 * m + 3]), wd[m]);
+    } else if constexpr (P.pos[LR][0] == 0 && P.pos[LR][1] == 1) {
 #pragma unroll
       for (int m = 0; m < 8; ++m)
         d.store4(g0 + rl + remap_c<CB, LO>(roff(P, LR, 4 * m)),
                  make_float4(v[4 * m], v[4 * m + 1], v[4 * m + 2], v[4 * m + 3]));
+    } else if constexpr (P.pos[LR][0] == 0 && split_store<DB>::value) {
+      uint32_t wd[16];
+#pragma unroll
+      for (int m = 0; m < 16; ++m) wd[m] = d.pre(g0 + rl + remap_c<CB, LO>(roff(P, LR, 2 * m)));
+#pragma unroll
+      for (int m = 0; m < 16; ++m)
+        d.store2w(g0 + rl + remap_c<CB, LO>(roff(P, LR, 2 * m)), v[2 * m], v[2 * m + 1], wd[m]);
     } else if constexpr (P.pos[LR][0] == 0) {
 #pragma unroll
       for (int m = 0; m < 16; ++m)
@@ -865,6 +911,17 @@ __global__ void __launch_bounds__(1 << (T - 5)) rtile_kernel(PassGeom pg, int wo
       for (int j = 0; j < 32; ++j) d.store1(g0 + rl + remap_c<CB, LO>(roff(P, LR, j)), v[j]);
     }
   }
+}
+
+template <int T, int CB, int LO, class Src, class Snk>
+__global__ void __launch_bounds__(1 << (T - 5)) rtile_kernel(PassGeom pg, int worker_base,
+                                                          const __grid_constant__ Src src,
+                                                          const __grid_constant__ Snk snk) {
+  extern __shared__ float sm[];
+  const int w = worker_base + blockIdx.y;
+  auto s = src.bind(w);
+  const auto d = snk.bind(w);
+  for (int64_t t = blockIdx.x; t < pg.ntiles; t += gridDim.x) rtile_do<T, CB, LO>(s, d, t, sm);
 }
 
 // ------------------------------------------------ small tiles (shared mem)

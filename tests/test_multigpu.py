@@ -108,7 +108,9 @@ def test_handle_exchange_gloo_world2():
 # ------------------------------------------------------------ multi-GPU
 CASES = [
     # L, p, gen, ht, dtype, max world (the oracle's cost bounds the big cases)
-    (1 << 16, 0.05, 3, True, "f32", 8),
+    (1 << 16, 0.05, 3, True, "f32", 8),       # small-bucket kernel (one launch), D = 2^16
+    (5_000, 0.05, 1, True, "f32", 8),         # small-bucket kernel, D = 2^13 (one pass each way)
+    (100_003, 0.02, 5, True, "bf16", 8),      # small-bucket kernel, bf16 in, ragged L
     (1_048_576, 0.01, 2, True, "f32", 8),     # BASELINE configs[0] shape (1M entries, 1%)
     (12_345, 0.05, 2, False, "f32", 8),       # RHT off: bit-exact
     (1 << 20, 0.02, 4, True, "bf16", 8),
@@ -297,7 +299,8 @@ def test_ddp_comm_hook_vs_mean_and_oracle(big):
 
 
 # ------------------------------------------- fused kernel protocol stress
-LENS = [5_000_000, 8_388_608, 3_000_000, 16_000_000, 5_000_000]
+# D = 2^23..2^24 (fused kernel), 2^22 (barrier path), 2^13..2^20 (small-bucket kernel)
+LENS = [5_000_000, 8_388_608, 300_000, 3_000_000, 16_000_000, 9_000, 5_000_000, 1_048_576]
 
 
 def _checksum(t):
@@ -310,6 +313,7 @@ def _checksum(t):
 
 def _seq_worker(rank, world, port, outdir, mode, reps):
     os.environ["OPTR_FUSED"] = "0" if mode == "barrier" else "1"
+    os.environ["OPTR_SMALL"] = "0" if mode == "barrier" else "1"
     import torch.distributed as dist
 
     from paper_2310_06993_b200.collectives import MaskSpec
@@ -353,10 +357,11 @@ def test_fused_protocol_async_stress():
     """The fused kernel's per-tile flags under back-to-back async calls (two
     call parities in flight, epochs advancing) give bit-identical results and
     received counts to the same calls fully serialised (host sync and an
-    all-rank barrier between calls), over reps x 5 buckets of D = 2^22..2^24;
-    and the barrier-separated unfused path agrees within the float32 codec
+    all-rank barrier between calls), over reps x 8 buckets of D = 2^13..2^24
+    (fused kernel, small-bucket kernel and barrier path interleaved); and the
+    barrier-separated unfused path agrees within the float32 codec
     tolerance (its pass order differs).  OPTR_TEST_STRESS=reps scales it up
-    (profiles/: 2,000 reps = 10,000 calls per mode on 2 GPUs)."""
+    (profiles/: 2,000 reps = 16,000 calls per mode on 2 GPUs)."""
     import torch.multiprocessing as mp
 
     _need_gpu()
