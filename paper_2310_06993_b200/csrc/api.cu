@@ -124,10 +124,13 @@ int plan_passes(int n, PassGeom* out, bool encode_order) {
     // three passes (D >= 2^26): the strided passes take 32 columns (128-byte
     // rows, full L2 lines) while T = ks + 5 <= 14; with 8 columns their tiles
     // were 2^9..2^10 entries of 32-byte rows at multi-MB strides (~1.2-1.5
-    // TB/s).  OPTR_WIDE3=0 keeps 8 columns.
+    // TB/s).
+    // The high pass takes 6 bits (T = 11): the multi-GPU decode ends with it
+    // and the TMA decode epilogue needs float4 groups in its last register
+    // round (32-column T = 11 / 14 tiles; T = 12 / 13 end on other bits).
     int rest = n - kContigBits;
-    int k1 = rest / 2;
-    const int cb = rest - k1 + 5 <= 14 ? 5 : kColBits;
+    int k1 = rest - 6 <= 9 ? rest - 6 : rest / 2;
+    const int cb = k1 + 5 <= 14 ? 5 : kColBits;
     p[np++] = PassGeom{0, kContigBits, 0, 0};
     p[np++] = PassGeom{kContigBits, k1, cb, 0};
     p[np++] = PassGeom{kContigBits + k1, rest - k1, cb, 0};
@@ -402,6 +405,7 @@ int try_tma(int cls, const PassGeom& pg, int nlog, int worker, int nworkers, con
               default: break;
             }
           }
+          if (T == 11) return launch_tma_pass<11, true, SK, Snk, 5>(cls, maps, dmaps, a, snk, worker, nworkers, st);
           if (T != 14) return -1;
           return launch_tma_pass<14, true, SK, Snk, 5>(cls, maps, dmaps, a, snk, worker, nworkers, st);
         }
