@@ -17,10 +17,17 @@
 #include "internal.h"
 
 #include <cudaTypedefs.h>
+#include <nvtx3/nvToolsExt.h>
 
 using namespace optr;
 
 namespace {
+
+// NVTX range around a public entry point (visible in nsys / ncu --nvtx)
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
 
 #define CK(call)                                                          \
   do {                                                                    \
@@ -253,9 +260,46 @@ bool tma_enabled() {
   return g_tma_mode == 1;
 }
 
-// tensor [d2][d1][d0] (d0 contiguous) of fp32 / bf16, boxes of box0 x box1 x 1
+// tensor [d2][d1][d0] (d0 contiguous) of fp32 / bf16, boxes of box0 x box1 x 1.
+// Encoded maps are cached per host thread (the key determines the map): the
+// same buckets / workspaces recur every step.
+struct MapKey {
+  const void* base;
+  uint64_t d0, d1, d2;
+  uint32_t box0, box1;
+  int dtype;
+  bool operator==(const MapKey& o) const {
+    return base == o.base && d0 == o.d0 && d1 == o.d1 && d2 == o.d2 && box0 == o.box0 && box1 == o.box1 &&
+           dtype == o.dtype;
+  }
+};
+bool make_map3_uncached(CUtensorMap* m, const void* base, uint64_t d0, uint64_t d1, uint64_t d2, uint32_t box1,
+                        int dtype, uint32_t box0);
 bool make_map3(CUtensorMap* m, const void* base, uint64_t d0, uint64_t d1, uint64_t d2, uint32_t box1,
                int dtype = OPTR_F32, uint32_t box0 = 8) {
+  constexpr int kSlots = 256;
+  struct Slot {
+    MapKey k;
+    CUtensorMap m;
+    bool valid;
+  };
+  thread_local Slot cache[kSlots];
+  const MapKey k{base, d0, d1, d2, box0, box1, dtype};
+  uint64_t h = (uint64_t)(uintptr_t)base * 0x9E3779B97F4A7C15ULL ^ (d0 * 31 + d1 * 17 + d2 * 7 + box0 * 3 + box1 + dtype);
+  h ^= h >> 29;
+  Slot& sl = cache[h % kSlots];
+  if (sl.valid && sl.k == k) {
+    *m = sl.m;
+    return true;
+  }
+  if (!make_map3_uncached(m, base, d0, d1, d2, box1, dtype, box0)) return false;
+  sl.k = k;
+  sl.m = *m;
+  sl.valid = true;
+  return true;
+}
+bool make_map3_uncached(CUtensorMap* m, const void* base, uint64_t d0, uint64_t d1, uint64_t d2, uint32_t box1,
+                        int dtype, uint32_t box0) {
   const uint64_t esz = dtype == OPTR_BF16 ? 2 : 4;
   cuuint64_t dims[3] = {d0, d1, d2};
   cuuint64_t strides[2] = {d0 * esz, d0 * d1 * esz};
@@ -952,6 +996,7 @@ int optr_tar_local(const void* const* x, void* const* out, int n, int64_t L, int
                    uint64_t job_seed, uint64_t bucket_id, uint64_t generation, int rotation, int ht,
                    const optr_mask_spec* masks, void* workspace, size_t workspace_bytes,
                    uint64_t* received_out, uint8_t* got_out, void* stream) {
+  NvtxRange nr("optr_tar_local");
   bind_device(stream);
   return tar_local_impl(x, out, n, L, dtype_in, dtype_out, job_seed, bucket_id, generation, rotation, ht, masks,
                         workspace, workspace_bytes, received_out, got_out, (cudaStream_t)stream, 0);
@@ -961,6 +1006,7 @@ int optr_tar_local_async(const void* const* x, void* const* out, int n, int64_t 
                          uint64_t job_seed, uint64_t bucket_id, uint64_t generation, int rotation, int ht,
                          const optr_mask_spec* masks, void* workspace, size_t workspace_bytes,
                          uint64_t* received_out, uint8_t* got_out, int slot, void* stream) {
+  NvtxRange nr("optr_tar_local_async");
   if (slot < 0 || slot > 1) return OPTR_EINVAL;
   bind_device(stream);
   LocalAsync* la = local_async();
@@ -1692,6 +1738,7 @@ static int tar_enqueue(optr_comm c, const void* x, void* out, int64_t L, int dty
                        uint64_t job_seed, uint64_t bucket_id, uint64_t generation, int rotation, int ht,
                        const optr_mask_spec* masks, uint64_t* received_out, void* stream, bool async,
                        uint64_t deadline_ns, optr_tar_stats* stats, uint32_t* cut_units) {
+  NvtxRange nr("optr_tar");
   if (!c) return OPTR_EINVAL;
   int n = c->n;
   int rc = check_common(n, L, dtype_in, dtype_out, masks);

@@ -17,7 +17,7 @@ import torch
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
-from bench import NVLINK_GBS, load_peaks, next_pow2  # noqa: E402
+from bench import load_peaks, next_pow2, nvlink_peak  # noqa: E402
 from paper_2310_06993_b200 import _lib  # noqa: E402
 from paper_2310_06993_b200.collectives import MaskSpec, tar_allreduce_local  # noqa: E402
 
@@ -83,7 +83,7 @@ def main():
         Y = 4 * D
         hbm = per_rank * (8 * L + 3 * Y + Y // n)
         nvl = 2 * Y * (n - 1) // n if multi else 0
-        t_roof = max(hbm / (peaks["hbm_gbs"] * 1e9), nvl / (NVLINK_GBS * 1e9))
+        t_roof = max(hbm / (peaks["hbm_gbs"] * 1e9), nvl / (nvlink_peak(n) * 1e9))
         if rank == 0:
             print(json.dumps({"bucket_MB": round(4 * L / 2**20, 4), "entries": L, "dim": D, "workers": n,
                               "gpus": world, "ms": round(ms, 4), "algbw_GBps": round(4 * L / (ms * 1e-3) / 1e9, 2),
