@@ -1616,7 +1616,7 @@ int stats_stamp(optr_tar_stats* s, int field, cudaStream_t st) {
 template <int T, int NW, int S, int NG>
 int launch_fused_t(const TmaArgs& ae, const TmaArgs& ad, const SnkBuf& se, const SnkBuf& sd, const FusedArgs& f,
                    cudaStream_t st) {
-  const size_t smem = tma_fused_smem_bytes<T, S, NG>();
+  const size_t smem = tma_fused_smem_bytes<T, S, NG, NW>();
   auto kern = tma_fused_kernel<T, S, NW, NG>;
   int rc = set_smem_attr(kern, smem);
   if (rc) return rc;
@@ -2089,7 +2089,7 @@ int64_t optr_fused_unit_entries(int64_t dim, int n) {
   if ((T != 13 && T != 14) || ps[1].cb != 3 || (ps[1].ks + 3 != 13 && ps[1].ks + 3 != 14)) return 0;
   if ((dim / n) < (1LL << T)) return 0;
   const int ch = agg_chunk(n);
-  int sa = kAggBytes / (n * ch * 4);
+  int sa = agg_bytes(T, n) / (n * ch * 4);
   if (sa > 16) sa = 16;
   const int cpt = (1 << T) / ch;
   const int upt = cpt / sa >= 4 ? 4 : (cpt / sa >= 2 ? 2 : 1);

@@ -955,11 +955,15 @@ __device__ __noinline__ void spin_ge_sys(const unsigned int* p, unsigned int v, 
 constexpr int kAggThreads = 256;
 // entries per rank per aggregate chunk: 4096/n (>= one float4 per thread)
 __host__ __device__ constexpr int agg_chunk(int n) { return 4096 / n > 1024 ? 4096 / n : 1024; }
-constexpr int kAggBytes = 64 * 1024;  // A-group ring
+// A-group ring bytes.  (A 32 KB ring at 2^13 tiles, n <= 4, so that a
+// strided-pass CTA of the next bucket fits beside a fused CTA, made the fused
+// kernel 86 -> 94 us per 2^23 bucket at N=2 and the step slower; two-stage
+// strided passes beside the 64 KB ring: 0.492 -> 0.533 ms per resnet50 step.)
+__host__ __device__ constexpr int agg_bytes(int, int) { return 64 * 1024; }
 
-template <int T, int S, int NG>
+template <int T, int S, int NG, int NW>
 __host__ __device__ constexpr size_t tma_fused_smem_bytes() {
-  return (size_t)NG * S * tma_stage_bytes<T>() + kAggBytes + 512 + 1024;
+  return (size_t)NG * S * tma_stage_bytes<T>() + agg_bytes(T, NW) + 512 + 1024;
 }
 
 enum FusedJob { FJ_END = -1, FJ_E = 0, FJ_D = 2, FJ_NOP = 3 };
@@ -972,6 +976,7 @@ __global__ void __launch_bounds__(NG * (1 << (T - 5)) + kAggThreads)
   constexpr int NED = 1 << (T - 5);
   constexpr size_t SB = tma_stage_bytes<T>();
   constexpr int kAggCh = agg_chunk(NW);
+  constexpr int kAggBytes = agg_bytes(T, NW);
   constexpr int SA = kAggBytes / (NW * kAggCh * 4) < 16 ? kAggBytes / (NW * kAggCh * 4) : 16;
   // aggregate work unit = 1/UPT of a tile (finer units shorten the A tail);
   // a unit must cover every ring stage queued behind a not-ready unit
