@@ -157,6 +157,10 @@ def kernel_bytes(cls: str, dim: int, L: int, n: int, s_in: int, s_out: int) -> i
         # shard in from n wire vectors + mean out to n receive vectors (local
         # side only: S in, S out), contiguous decode pass in place (2Y)
         "fused": 4 * Y + 2 * S,
+        # multi-GPU small-bucket kernel (the whole call in one launch): x in,
+        # four in-place passes over the wire vector, owner shard in + mean
+        # out, stage-2 receive written to the wire vector, out
+        "small": s_in * L + 8 * Y + 2 * S + Y + s_out * L,
     }.get(cls, 0)
 
 
@@ -436,14 +440,14 @@ def run_ours(args):
             dim = next_pow2(L) if ht else L
             if nvlink:
                 # stage 1 in (+ stage 2 in for the fused kernel), per direction
-                k = 2 if cls == "fused" else 1
+                k = 2 if cls in ("fused", "small") else 1
                 per_b += k * 4 * dim * (n_workers - 1) // n_workers
             else:
                 per_b += kernel_bytes(cls, dim, L, n_workers, s_in, s_out)
         return units * per_b / len(buckets)
 
     achieved = class_bytes(dom) / (dom_ms * 1e-3) / 1e9
-    if multi and dom in ("aggregate", "dec_first", "fused"):
+    if multi and dom in ("aggregate", "dec_first", "fused", "small"):
         nv_ach = class_bytes(dom, nvlink=True) / (dom_ms * 1e-3) / 1e9
         roof = {"bound": "nvlink", "achieved": round(nv_ach, 1), "peak": nvlink_peak(n_workers), "unit": "GB/s",
                 "frac": round(nv_ach / nvlink_peak(n_workers), 4), "kernel": dom,

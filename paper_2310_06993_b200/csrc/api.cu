@@ -637,7 +637,8 @@ void fill_sign_args(PrepArgs& a, uint32_t* signs, int64_t dim, uint64_t seed) {
   a.dim = dim;
   a.sign_state = p.state;
   a.sign_inc = p.inc;
-  a.sign_threads = (dim + kSignsPerThread - 1) / kSignsPerThread;
+  a.sign_chunks = (dim + kSignsPerThread - 1) / kSignsPerThread;
+  a.sign_threads = ((a.sign_chunks + 1) / 2 + 31) & ~31LL;  // two chunks per thread, whole warps
 }
 
 // cap_per_sm > 0: at most that many CTAs per SM (grid-stride), for a prep
