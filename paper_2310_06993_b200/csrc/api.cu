@@ -637,8 +637,7 @@ void fill_sign_args(PrepArgs& a, uint32_t* signs, int64_t dim, uint64_t seed) {
   a.dim = dim;
   a.sign_state = p.state;
   a.sign_inc = p.inc;
-  a.sign_chunks = (dim + kSignsPerThread - 1) / kSignsPerThread;
-  a.sign_threads = ((a.sign_chunks + 1) / 2 + 31) & ~31LL;  // two chunks per thread, whole warps
+  a.sign_threads = (dim + kSignsPerThread - 1) / kSignsPerThread;
 }
 
 // cap_per_sm > 0: at most that many CTAs per SM (grid-stride), for a prep
@@ -1865,7 +1864,10 @@ static int tar_enqueue(optr_comm c, const void* x, void* out, int64_t L, int dty
   const uint32_t* cbits = nullptr;
   if ((rc = setup_masks(pa, masks, dim, n, r, epp, bitmap, counts, me, me + 1, &cbits))) return rc;
   // background prep: a few small CTAs per SM, beside the previous call's
-  // fused kernel (a full-width prep delayed the strided passes)
+  // fused kernel (a full-width prep delayed the strided passes; on the call
+  // stream at full width it costs more than its overlap with the strided
+  // decode pass does; two PCG chains per thread or rank-sharded signs stored
+  // into every rank's copy were slower too, profiles/r02_prep_ab.txt)
   if ((rc = launch_prep(pa, ps, 2))) return rc;
   CK(cudaEventRecord(c->prep_ready[par], ps));
   CK(cudaStreamWaitEvent(st, c->prep_ready[par], 0));

@@ -193,8 +193,7 @@ struct PrepArgs {
   uint32_t* signs;
   int64_t dim;
   u128 sign_state, sign_inc;
-  int64_t sign_threads;  // threads of the sign part: two 128-sign chunks each (i, i + sign_threads)
-  int64_t sign_chunks;   // ceil(dim / 128)
+  int64_t sign_threads;
   // optional second layout for strided passes (tma.cuh): sign byte of
   // entries row*2^t_lo + 8*cg .. +7 at signs_t[cg * 2^t_ks + row]
   uint8_t* signs_t;
@@ -252,58 +251,39 @@ __global__ void __launch_bounds__(256) prep_kernel(const __grid_constant__ PrepA
 __device__ __forceinline__ void prep_item(const PrepArgs& a, int64_t t) {
   if (t < a.sign_threads) {
     // signs 128c .. 128c+127 = outputs 64c .. 64c+63; Lemire bit of u32 halves.
-    // Two chunks per thread (items t and t + sign_threads) stepped in
-    // lockstep: the 128-bit LCG chain is latency-bound, two independent
-    // chains double a warp's throughput (prep runs as a thin background
-    // kernel beside the multi-GPU fused kernel).
-    const int64_t i1 = t + a.sign_threads;
-    const bool two = i1 < a.sign_chunks;
-    int64_t c[2], row[2] = {0, 0}, cg16[2] = {0, 0};
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      // natural layout: chunk c = item.  With the transposed layout too, a
-      // warp takes 32 consecutive rows of one 128-column chunk (coalesced bytes)
-      const int64_t it = h == 0 ? t : (two ? i1 : t);
-      c[h] = it;
-      if (a.signs_t) {
-        const int64_t rows = 1LL << a.t_ks;
-        const int64_t w = it >> 5;
-        row[h] = ((w % (rows >> 5)) << 5) | (it & 31);
-        cg16[h] = w / (rows >> 5);
-        c[h] = ((row[h] << a.t_lo) >> 7) + cg16[h];
-      }
+    // Natural layout: chunk c = t.  With the transposed layout too, a warp
+    // takes 32 consecutive rows of one 128-column chunk (coalesced bytes).
+    int64_t c = t, row = 0, cg16 = 0;
+    if (a.signs_t) {
+      const int64_t rows = 1LL << a.t_ks;
+      const int64_t w = t >> 5;
+      row = ((w % (rows >> 5)) << 5) | (t & 31);
+      cg16 = w / (rows >> 5);
+      c = ((row << a.t_lo) >> 7) + cg16;
     }
-    u128 s0 = jump(a.sign_state, a.sign_inc, (uint64_t)c[0] * 64 + 1);
-    u128 s1 = jump(a.sign_state, a.sign_inc, (uint64_t)c[1] * 64 + 1);
+    u128 s = jump(a.sign_state, a.sign_inc, (uint64_t)c * 64 + 1);
     const int64_t nwords = (a.dim + 31) >> 5;
+    const int64_t w0 = c * 4;
 #pragma unroll
     for (int wd = 0; wd < 4; ++wd) {
-      uint32_t word0 = 0, word1 = 0;
+      uint32_t word = 0;
 #pragma unroll
       for (int i = 0; i < 16; ++i) {
-        const uint64_t o0 = pcg_xsl_rr(s0), o1 = pcg_xsl_rr(s1);
-        word0 |= (uint32_t)((o0 >> 31) & 1u) << (2 * i);
-        word0 |= (uint32_t)(o0 >> 63) << (2 * i + 1);
-        word1 |= (uint32_t)((o1 >> 31) & 1u) << (2 * i);
-        word1 |= (uint32_t)(o1 >> 63) << (2 * i + 1);
-        s0 = pcg_step(s0, a.sign_inc);
-        s1 = pcg_step(s1, a.sign_inc);
+        uint64_t out = pcg_xsl_rr(s);
+        word |= (uint32_t)((out >> 31) & 1u) << (2 * i);
+        word |= (uint32_t)(out >> 63) << (2 * i + 1);
+        s = pcg_step(s, a.sign_inc);
       }
+      int64_t wi = w0 + wd;
+      if (wi < nwords) {
+        int64_t valid = a.dim - wi * 32;  // zero the bits past dim
+        if (valid < 32) word &= (1u << valid) - 1u;
+        a.signs[wi] = word;
+        if (a.signs_t) {
+          const int64_t rows = 1LL << a.t_ks;
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        if (h == 1 && !two) break;
-        uint32_t word = h == 0 ? word0 : word1;
-        const int64_t wi = c[h] * 4 + wd;
-        if (wi < nwords) {
-          const int64_t valid = a.dim - wi * 32;  // zero the bits past dim
-          if (valid < 32) word &= (1u << valid) - 1u;
-          a.signs[wi] = word;
-          if (a.signs_t) {
-            const int64_t rows = 1LL << a.t_ks;
-#pragma unroll
-            for (int b = 0; b < 4; ++b)
-              a.signs_t[(cg16[h] * 16 + wd * 4 + b) * rows + row[h]] = (uint8_t)(word >> (8 * b));
-          }
+          for (int b = 0; b < 4; ++b)
+            a.signs_t[(cg16 * 16 + wd * 4 + b) * rows + row] = (uint8_t)(word >> (8 * b));
         }
       }
     }

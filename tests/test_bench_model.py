@@ -30,7 +30,7 @@ def test_step_alg_bytes_rht_off_and_bf16():
 
 def test_kernel_bytes_classes():
     dim, L, n = 1 << 23, 6_553_600, 4
-    for cls in ("enc_first", "enc_last", "enc_mean", "aggregate", "dec_first", "dec_last", "fused", "prep"):
+    for cls in ("enc_first", "enc_last", "enc_mean", "aggregate", "dec_first", "dec_last", "fused", "prep", "small"):
         assert bench.kernel_bytes(cls, dim, L, n, 4, 4) > 0
     # the fused last-pass + stage-1 mean reads the wire once and writes one
     # shard's mean per worker: less than the last pass plus the aggregate
