@@ -1327,11 +1327,11 @@ struct optr_comm_s {
   bool done_recorded[2];
   uint64_t calls;
   int fused_grid;  // CTAs of the persistent fused kernel (0 = SMs x occupancy)
-  // small-bucket path (tar_small_kernel): wire Y | aggregate A | flags
+  // small-bucket path (tar_small_kernel): wire / receive vector Y | flags
   // [2][kMaxW] in the symmetric block, signs | bitmap | counts | barrier
   // counter in `slocal`; 0 bytes when max_len is below the small range
   int64_t small_dim;  // largest small-path dim (0 = off)
-  size_t off_sy, off_sa, off_sf;
+  size_t off_sy, off_sf;
   char* slocal;
   size_t s_signs, s_bitmap, s_counts, s_bar;
   unsigned long long s_epoch, s_bar_base;
@@ -1375,8 +1375,6 @@ int optr_comm_create(optr_comm* out, int device, int rank, int n, int64_t max_le
   if (c->small_dim) {
     c->off_sy = off;
     off = align_up(off + (size_t)c->small_dim * 4, 1024);
-    c->off_sa = off;
-    off = align_up(off + (size_t)(c->small_dim / 2) * 4, 1024);  // a shard, n >= 2
     c->off_sf = off;
     off = align_up(off + (size_t)2 * kMaxW * 8, 1024);
   }
@@ -1786,7 +1784,6 @@ static int tar_enqueue(optr_comm c, const void* x, void* out, int64_t L, int dty
     a.dim = dim;
     for (int i = 0; i < n; ++i) {
       a.Y[i] = (float*)(c->peer[i] + c->off_sy);
-      a.A[i] = (float*)(c->peer[i] + c->off_sa);
       a.flags[i] = (unsigned long long*)(c->peer[i] + c->off_sf);
     }
     const int grid = small_grid(klog);

@@ -8,29 +8,31 @@
 // both decode passes -- separated by grid barriers on the GPU and by two
 // flag handshakes over NVLink:
 //
-//   phase 0  signs (32 per item), zero the received counts
-//   phase 1  masks + counts of my receive rows (prep_item); encode pass 1:
-//            contiguous 2^13 tiles of x -> Y[me] (pad, signs, bf16 upcast)
+//   phase 1  each tile CTA: its tile's signs (one PCG jump per 32), then
+//            encode pass 1 (contiguous 2^13 tiles of x -> Y[me]: pad, signs,
+//            bf16 upcast); the other CTAs: packet masks and received counts
 //   phase 2  encode pass 2: strided bits [13, K) in place, x 1/sqrt(D)
 //            -> ready1: push my epoch into every peer's flag block
 //   phase 3  wait ready1 of every peer; stage 1: masked fp64 mean of my
-//            shard over every rank's Y (peer loads) -> A[me]
+//            shard over every rank's Y (peer loads), and stage 2 as a push:
+//            the mean goes into every rank's Y at my shard's offset under
+//            that receiver's stage-2 mask (peer stores; system-scope fence)
 //            -> ready2
-//   phase 4  wait ready2 of every peer; stage 2: every CTA pulls a slice of
-//            the owners' A (peer loads, stage-2 masks) -> Y[me]
-//   phase 5  decode pass 1: contiguous tiles of Y[me] in place
-//   phase 6  decode pass 2: strided bits, D/count scale, signs, truncate,
+//   phase 4  wait ready2 of every peer (my Y now holds the stage-2
+//            receive); decode pass 1: contiguous tiles in place
+//   phase 5  decode pass 2: strided bits, D/count scale, signs, truncate,
 //            cast -> out
 //
 // References: hadamard.py:93-123 (encode / decode), collectives.py:97-150
 // (tar_allreduce), collectives.py:77-94 (_mean_received), datagram.py:70-72
 // (coin masks, via prep_item).
 //
-// Buffer reuse across calls needs no extra synchronisation: Y[me] is
-// rewritten (phase 4) only after every peer's ready2, i.e. after every peer
-// finished reading it in phase 3; A[me] is rewritten (phase 3 of the next
-// call) only after every peer's next ready1, i.e. after that peer's whole
-// previous call (stream order).  Flags carry the call epoch and only grow.
+// Buffer reuse needs no extra synchronisation: in phase 3 owner j reads
+// every rank's Y at shard j's offset and writes its mean back to exactly
+// those entries (same thread, read before write); other owners touch other
+// shards.  Owner j pushes call c+1's means into my Y only after my ready1 of
+// c+1, i.e. after my whole call c (stream order).  Flags carry the call
+// epoch and only grow.
 #pragma once
 
 #include "kernels.cuh"
@@ -40,7 +42,7 @@ namespace optr {
 constexpr int kSmallT = 13;        // tile bits of both passes (256 threads, 32 values each)
 constexpr int kSmallMinLog = 13;   // 32 KB fp32
 constexpr int kSmallMaxLog = 20;   // 4 MB fp32
-constexpr int kSmallBarriers = 6;  // grid barriers per call
+constexpr int kSmallBarriers = 4;  // grid barriers per call
 constexpr int kSmallMaxRanks = 8;
 
 __device__ __forceinline__ uint64_t small_clock_ns() {
@@ -57,8 +59,7 @@ struct SmallArgs {
   void* out;
   int dtype_in, dtype_out;
   int64_t L, dim;
-  float* Y[kMaxW];                   // every rank's wire vector (peer-mapped)
-  float* A[kMaxW];                   // every rank's aggregate of its shard
+  float* Y[kMaxW];                   // every rank's wire / stage-2 receive vector (peer-mapped)
   unsigned long long* flags[kMaxW];  // every rank's flag block [2][kMaxW]
   unsigned long long* bar;           // grid-barrier arrivals (monotonic)
   unsigned long long bar_base;
@@ -162,9 +163,14 @@ struct SmallEncodeSrc {
         const uint2 u = __ldg(reinterpret_cast<const uint2*>((const __nv_bfloat16*)e.x + g));
         r.v = make_float4(__uint_as_float(u.x), __uint_as_float(u.y), 0.f, 0.f);
       }
-      r.w = __ldg(e.signs + (g >> 5));
+      r.w = __ldcg(e.signs + (g >> 5));  // written by this CTA in this phase
     } else {
-      r.v = make_float4(e.load1(g), e.load1(g + 1), e.load1(g + 2), e.load1(g + 3));
+      float f[4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        f[c] = g + c < e.L ? sgn(__ldcg(e.signs + ((g + c) >> 5)), (int)((g + c) & 31), load_elem(e.x, e.dtype, g + c))
+                           : 0.f;
+      r.v = make_float4(f[0], f[1], f[2], f[3]);
       r.w = 0;
     }
     return r;
@@ -210,41 +216,6 @@ __device__ __forceinline__ uint32_t keep4_words(uint32_t e, uint32_t w0, uint32_
   }
   return k;
 }
-
-// stage-2 receive (collectives.py:140-150): shard j's entries from its
-// owner's aggregate over NVLink, zero where the owner's packet to me was lost
-struct SmallGatherSrc {
-  static constexpr bool kSplit = true;
-  const SmallArgs* a;
-  struct Raw {
-    float4 v;
-    uint32_t w0, w1;
-  };
-  __device__ __forceinline__ void begin_tile(int64_t, int64_t) {}
-  __device__ __forceinline__ Raw raw4(int64_t g) const {
-    const int j = (int)(g >> a->shard_shift);
-    const uint32_t e = (uint32_t)(g & ((1LL << a->shard_shift) - 1));
-    const int owner = shard_owner(j, a->r, a->n);
-    Raw r;
-    r.v = ld_cg4(a->A[owner] + e);
-    r.w0 = r.w1 = 0xffffffffu;
-    if (owner != a->me) {
-      const uint32_t* row = a->m.row(1, a->me, owner);
-      const uint32_t wi = a->m.dv.div(e) >> 5;
-      r.w0 = __ldg(row + wi);
-      r.w1 = wi + 1 < (uint32_t)a->m.pw ? __ldg(row + wi + 1) : 0u;
-    }
-    return r;
-  }
-  __device__ __forceinline__ float4 fix4(int64_t g, const Raw& r) const {
-    const int j = (int)(g >> a->shard_shift);
-    if (shard_owner(j, a->r, a->n) == a->me) return r.v;
-    const uint32_t e = (uint32_t)(g & ((1LL << a->shard_shift) - 1));
-    const uint32_t kk = keep4_words(e, r.w0, r.w1, a->m);
-    return make_float4((kk & 1u) ? r.v.x : 0.f, (kk & 2u) ? r.v.y : 0.f, (kk & 4u) ? r.v.z : 0.f,
-                       (kk & 8u) ? r.v.w : 0.f);
-  }
-};
 
 // signs * v * (D/count)/sqrt(D), truncated, cast; scalar stores for unaligned out
 struct SmallDecodeSnk {
@@ -303,11 +274,12 @@ struct SmallDecodeSnk {
   }
 };
 
-// Packet masks of the rows (stage, dst = me, src), one packet per thread,
-// a warp per bitmap word (prep_item's per-word loop, spread out: the coin of
-// packet k is output k of the sender's stream, datagram.py:70-72,122), and
-// the received entries per stage (simdriver.py:188-189: the last packet of a
-// transfer is short).  Every row has np packets (equal shards).
+// Packet masks, one packet per thread, a warp per bitmap word (prep_item's
+// per-word loop, spread out: the coin of packet k is output k of the
+// sender's stream, datagram.py:70-72,122): my receive rows (stage, dst = me,
+// src) with the received entries per stage (simdriver.py:188-189: the last
+// packet of a transfer is short), then my stage-2 send rows (dst = q, src =
+// me) for the push.  Every row has np packets (equal shards).
 __device__ __forceinline__ void small_masks(const SmallArgs& a, int64_t gtid, int64_t gthreads,
                                             const JumpSmem& jt) {
   const PrepArgs& pa = a.pa;
@@ -315,16 +287,18 @@ __device__ __forceinline__ void small_masks(const SmallArgs& a, int64_t gtid, in
   const int64_t len = 1LL << a.shard_shift;
   const int64_t np = n_packets(len, pa.epp);
   const int64_t per_row = pa.pw * 32;
-  const int64_t total = (int64_t)2 * (n - 1) * per_row;  // a multiple of 32: whole warps per word
+  const int64_t total = (int64_t)3 * (n - 1) * per_row;  // a multiple of 32: whole warps per word
   for (int64_t t = gtid; t < total; t += gthreads) {
     const int row = (int)(t / per_row);
     const int64_t p = t - (int64_t)row * per_row;
-    const int stage = row / (n - 1), srci = row - stage * (n - 1);
-    const int src = srci < me ? srci : srci + 1;
-    const int64_t widx = ((int64_t)(stage * n + me) * n + src) * pa.pw + (p >> 5);
+    const bool recv = row < 2 * (n - 1);
+    const int stage = recv ? row / (n - 1) : 1, oi = row - (recv ? stage : 2) * (n - 1);
+    const int other = oi < me ? oi : oi + 1;
+    const int src = recv ? other : me, dst = recv ? me : other;
+    const int64_t widx = ((int64_t)(stage * n + dst) * n + src) * pa.pw + (p >> 5);
     bool keep = p < np;
     if (pa.kind == OPTR_MASK_COIN && keep) {
-      const u128 s = jump_s(pa.coin_state[src], pa.coin_inc[src], coin_base(pa, stage, src, me) + (uint64_t)p + 1, jt);
+      const u128 s = jump_s(pa.coin_state[src], pa.coin_inc[src], coin_base(pa, stage, src, dst) + (uint64_t)p + 1, jt);
       keep = !coin_drops(pcg_xsl_rr(s), pa.drop_prob);
     } else if (pa.kind == OPTR_MASK_BITMAP && keep) {
       keep = (__ldg(pa.bitmap_in + widx) >> (p & 31)) & 1u;
@@ -332,7 +306,7 @@ __device__ __forceinline__ void small_masks(const SmallArgs& a, int64_t gtid, in
     const uint32_t bits = __ballot_sync(0xffffffffu, keep);
     if ((threadIdx.x & 31) == 0) {
       if (pa.kind != OPTR_MASK_BITMAP) pa.bitmap_out[widx] = bits;
-      if (bits) {
+      if (bits && recv) {
         unsigned long long e = (unsigned long long)__popc(bits) * (unsigned long long)pa.epp;
         const int64_t last = np - 1 - (p & ~31LL);  // bit of the short last packet, if in this word
         if (last >= 0 && last < 32 && ((bits >> last) & 1u)) e -= (unsigned long long)(np * pa.epp - len);
@@ -343,18 +317,19 @@ __device__ __forceinline__ void small_masks(const SmallArgs& a, int64_t gtid, in
 }
 
 // Stage 1 at the owner (collectives.py:77-94; aggregate_kernel): masked
-// mean of my shard over every rank's Y, fp64 in ascending rank order.  Each
-// thread keeps 8 / NR float4 groups' loads (NR ranks each, mostly over
+// mean of my shard over every rank's Y, fp64 in ascending rank order; then
+// stage 2 (collectives.py:133-150) as a push: the mean into every rank's Y
+// at the same entries, zero where my packet to that receiver was lost.
+// Each thread keeps 8 / NR float4 groups' loads (NR ranks each, mostly over
 // NVLink) in flight before it computes.
 template <int NR>
 __device__ __forceinline__ void small_mean(const SmallArgs& a, int64_t gtid, int64_t gthreads) {
   constexpr int U = 8 / NR;
   const int j = owned_shard(a.me, a.r, NR);
   const int64_t n4 = (1LL << a.shard_shift) >> 2, off = (int64_t)j << a.shard_shift;
-  float* const out = a.A[a.me];
   for (int64_t b4 = gtid; b4 < n4; b4 += gthreads * U) {
     float4 v[U][NR];
-    uint32_t w0[U][NR], w1[U][NR];
+    uint32_t w0[U][NR], w1[U][NR], s0[U][NR], s1[U][NR];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int64_t e4 = b4 + u * gthreads;
@@ -366,6 +341,9 @@ __device__ __forceinline__ void small_mean(const SmallArgs& a, int64_t gtid, int
           const uint32_t* row = a.m.row(0, a.me, i);
           w0[u][i] = i == a.me ? 0xffffffffu : __ldg(row + wi);
           w1[u][i] = (i == a.me || wi + 1 >= (uint32_t)a.m.pw) ? 0xffffffffu : __ldg(row + wi + 1);
+          const uint32_t* srow = a.m.row(1, i, a.me);  // my stage-2 packets to receiver i
+          s0[u][i] = i == a.me ? 0xffffffffu : __ldg(srow + wi);
+          s1[u][i] = (i == a.me || wi + 1 >= (uint32_t)a.m.pw) ? 0xffffffffu : __ldg(srow + wi + 1);
         }
       }
     }
@@ -387,8 +365,14 @@ __device__ __forceinline__ void small_mean(const SmallArgs& a, int64_t gtid, int
           cnt[2] += (kk & 4u) ? 1.0 : 0.0;
           cnt[3] += (kk & 8u) ? 1.0 : 0.0;
         }
-        st4(out + e, make_float4(mean_of(acc[0], cnt[0]), mean_of(acc[1], cnt[1]), mean_of(acc[2], cnt[2]),
-                                 mean_of(acc[3], cnt[3])));
+        const float4 mv = make_float4(mean_of(acc[0], cnt[0]), mean_of(acc[1], cnt[1]), mean_of(acc[2], cnt[2]),
+                                      mean_of(acc[3], cnt[3]));
+#pragma unroll
+        for (int i = 0; i < NR; ++i) {
+          const uint32_t kk = i == a.me ? 0xFu : keep4_words(e, s0[u][i], s1[u][i], a.m);
+          st4(a.Y[i] + off + e, make_float4((kk & 1u) ? mv.x : 0.f, (kk & 2u) ? mv.y : 0.f, (kk & 4u) ? mv.z : 0.f,
+                                            (kk & 8u) ? mv.w : 0.f));
+        }
       }
     }
   }
@@ -412,37 +396,36 @@ __global__ void __launch_bounds__(1 << (kSmallT - 5)) tar_small_kernel(const __g
     jt.g[tid] = c_jump.g[tid];
   }
   __syncthreads();
-
-  // phase 0: signs, 32 per item = PCG64 outputs 16w..16w+15 (hadamard.py:49-51);
-  // masks and received counts of my receive rows, one packet per thread
   if (blockIdx.x == 0 && tid < 2 * a.n) a.counts_next[tid] = 0ULL;
-  // (masks from the last CTA down: the signs occupy the first ones)
+  // packet masks and received counts, from the last CTA down (the tile CTAs
+  // are the first ones)
   small_masks(a, (int64_t)(G - 1 - blockIdx.x) * blockDim.x + tid, gthreads, jt);
-  for (int64_t w = gtid; w < (a.dim >> 5); w += gthreads) {
-    u128 s = jump_s(a.sign_state, a.sign_inc, (uint64_t)w * 16 + 1, jt);
-    uint32_t word = 0;
-#pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      const uint64_t o = pcg_xsl_rr(s);
-      word |= (uint32_t)((o >> 31) & 1u) << (2 * i);
-      word |= (uint32_t)(o >> 63) << (2 * i + 1);
-      s = pcg_step(s, a.sign_inc);
-    }
-    a.signs[w] = word;
-  }
   small_stamp(a, 1);
-  small_grid_sync(a.bar, a.bar_base + (unsigned long long)G);
-  small_stamp(a, 2);
 
-  // phase 1: encode pass 1 (contiguous)
+  // phase 1: per tile, its 2^13 signs = PCG64 outputs 16w..16w+15 of words
+  // w = 256t + tid (hadamard.py:49-51), then encode pass 1 (contiguous)
   {
     SrcEncode::B eb{a.x, a.dtype_in, a.L, a.signs};
     SmallEncodeSrc src{eb, (((uintptr_t)a.x) & (a.dtype_in == OPTR_F32 ? 15 : 7)) == 0};
     const SnkBuf::B dst{ym, K == T ? (float)(1.0 / sqrt((double)a.dim)) : 1.f};
-    for (int64_t t = blockIdx.x; t < ntiles; t += G) rtile_do<T, 0, 0>(src, dst, t, sm);
+    for (int64_t t = blockIdx.x; t < ntiles; t += G) {
+      const int64_t w = (t << (T - 5)) + tid;  // 2^(T-5) threads: one sign word each
+      u128 st = jump_s(a.sign_state, a.sign_inc, (uint64_t)w * 16 + 1, jt);
+      uint32_t word = 0;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const uint64_t o = pcg_xsl_rr(st);
+        word |= (uint32_t)((o >> 31) & 1u) << (2 * i);
+        word |= (uint32_t)(o >> 63) << (2 * i + 1);
+        st = pcg_step(st, a.sign_inc);
+      }
+      a.signs[w] = word;
+      __syncthreads();  // the tile's sign words are written (read back through L2)
+      rtile_do<T, 0, 0>(src, dst, t, sm);
+    }
   }
   small_stamp(a, 4);
-  small_grid_sync(a.bar, a.bar_base + 2ULL * G);
+  small_grid_sync(a.bar, a.bar_base + 1ULL * G);
   small_stamp(a, 5);
 
   // phase 2: encode pass 2 (strided, in place) -> ready1
@@ -452,13 +435,12 @@ __global__ void __launch_bounds__(1 << (kSmallT - 5)) tar_small_kernel(const __g
     for (int64_t t = blockIdx.x; t < ntiles; t += G) rtile_do<T, CB, T>(src, dst, t, sm);
   }
   small_stamp(a, 6);
-  small_grid_sync(a.bar, a.bar_base + 3ULL * G);
+  small_grid_sync(a.bar, a.bar_base + 2ULL * G);
   small_stamp(a, 7);
   small_signal(a, 0);
   small_stamp(a, 8);
 
-  // phase 3: stage 1 at the owner, fp64 in ascending rank order
-  // (collectives.py:77-94; aggregate_kernel) -> ready2
+  // phase 3: stage 1 at the owner + the stage-2 push -> ready2
   small_wait_peers(a, 0);
   small_stamp(a, 9);
   switch (a.n) {
@@ -466,13 +448,15 @@ __global__ void __launch_bounds__(1 << (kSmallT - 5)) tar_small_kernel(const __g
     case 4: small_mean<4>(a, gtid, gthreads); break;
     default: small_mean<8>(a, gtid, gthreads); break;
   }
+  // my peer stores have landed before this CTA arrives at the barrier, so
+  // before the flag that follows it (the data lives in the READER's memory)
+  __threadfence_system();
   small_stamp(a, 10);
-  small_grid_sync(a.bar, a.bar_base + 4ULL * G);
+  small_grid_sync(a.bar, a.bar_base + 3ULL * G);
   small_signal(a, 1);
   small_stamp(a, 11);
 
-  // phase 4: stage 2 + decode pass 1 (contiguous); my Y is free once every
-  // owner published (it read my Y before)
+  // phase 4: every owner's push landed in my Y; decode pass 1 (contiguous, in place)
   small_wait_peers(a, 1);
   small_stamp(a, 12);
   SnkDecode::B db;
@@ -482,25 +466,6 @@ __global__ void __launch_bounds__(1 << (kSmallT - 5)) tar_small_kernel(const __g
     db = SnkDecode::B{a.out, a.dtype_out, a.L, a.signs, c == 0 ? 0.f : (float)((D / (double)c) / sqrt(D))};
   }
   const bool ovec = (((uintptr_t)a.out) & (a.dtype_out == OPTR_F32 ? 15 : 7)) == 0;
-  {  // every CTA pulls a slice: U float4 per thread in flight
-    constexpr int U = 4;
-    const SmallGatherSrc src{&a};
-    const int64_t n4 = a.dim >> 2;
-    for (int64_t b4 = gtid; b4 < n4; b4 += gthreads * U) {
-      SmallGatherSrc::Raw raw[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u)
-        if (b4 + u * gthreads < n4) raw[u] = src.raw4((b4 + u * gthreads) * 4);
-#pragma unroll
-      for (int u = 0; u < U; ++u)
-        if (b4 + u * gthreads < n4) st4(ym + (b4 + u * gthreads) * 4, src.fix4((b4 + u * gthreads) * 4, raw[u]));
-    }
-  }
-  small_stamp(a, 13);
-  small_grid_sync(a.bar, a.bar_base + 5ULL * G);
-  small_stamp(a, 14);
-
-  // phase 5: decode pass 1 (contiguous, in place)
   {
     SmallBufSrc src{ym};
     if constexpr (K == T) {
@@ -511,9 +476,11 @@ __global__ void __launch_bounds__(1 << (kSmallT - 5)) tar_small_kernel(const __g
       for (int64_t t = blockIdx.x; t < ntiles; t += G) rtile_do<T, 0, 0>(src, dst, t, sm);
     }
   }
-  small_grid_sync(a.bar, a.bar_base + 6ULL * G);
+  small_stamp(a, 13);
+  small_grid_sync(a.bar, a.bar_base + 4ULL * G);
+  small_stamp(a, 14);
 
-  // phase 6: decode pass 2 (strided) -> out
+  // phase 5: decode pass 2 (strided) -> out
   if constexpr (K > T) {
     SmallBufSrc src{ym};
     const SmallDecodeSnk dst{db, ovec};
