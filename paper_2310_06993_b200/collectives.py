@@ -271,7 +271,8 @@ def tar_allreduce_local(buckets: list, *, rotation: int = 0, ht: bool = False, j
     with torch.cuda.stream(st):
         if out is None:
             out = [torch.empty(L, dtype=out_dtype, device=dev) for _ in range(n)]
-        counts = torch.zeros((2, n), dtype=torch.int64, device=dev)
+        # every entry is written by the call (L > 0)
+        counts = (torch.empty if L > 0 else torch.zeros)((2, n), dtype=torch.int64, device=dev)
         got = torch.empty((n, dim), dtype=torch.uint8, device=dev) if want_received else None
     xs = (ctypes.c_void_p * n)(*[b.data_ptr() for b in buckets])
     os_ = (ctypes.c_void_p * n)(*[o.data_ptr() for o in out])

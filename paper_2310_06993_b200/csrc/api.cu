@@ -957,7 +957,7 @@ extern "C" {
 
 // -------------------------------------------------- TAR, n workers, one GPU
 struct LocalLayout {
-  size_t y, a, signs, signs_t, bitmap, counts, tileok, total;
+  size_t y, a, signs, signs_t, bitmap, counts, bar, tileok, total;
   int64_t dim, smax, astride, pw;
 };
 
@@ -980,7 +980,9 @@ static LocalLayout local_layout(int n, int64_t L, int ht, int epp) {
   l.bitmap = off;
   off = align_up(off + (size_t)2 * n * n * l.pw * 4, 256);
   l.counts = off;
-  off = align_up(off + (size_t)2 * n * 8, 256);
+  off = align_up(off + (size_t)2 * n * 8, 8);
+  l.bar = off;  // small-bucket kernel's grid-barrier counter (zeroed with the counts)
+  off = align_up(off + 8, 256);
   l.tileok = off;  // per-tile mask summaries of the fast plan: 2 x (dim / 2^13) words
   off = align_up(off + (size_t)2 * ((l.dim >> 13) + 1) * 4, 256);
   l.total = off;
@@ -1100,6 +1102,103 @@ int launch_mean_n(const TmaArgs& a, const MeanArgs& m, cudaStream_t st) {
   }
 }
 
+void* g_small_trace = nullptr;  // optr_debug_trace with per_cta < 0: small-kernel phase stamps
+
+bool small_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("OPTR_SMALL");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
+template <int K>
+int launch_small_local_t(const SmallLocalArgs& a, cudaStream_t st) {
+  auto kern = tar_small_local_kernel<K>;
+  const size_t smem = sizeof(float) * (size_t)pad(1 << kSmallT);
+  int rc = set_smem_attr(kern, smem);
+  if (rc) return rc;
+  int dev = 0, nsm = 148, per_sm = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  // every co-resident CTA (cooperative): more tile jobs per pass in flight
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 1 << (kSmallT - 5), smem) != cudaSuccess ||
+      per_sm < 1)
+    per_sm = 1;
+  if (per_sm > 2) per_sm = 2;
+  if ((a.dim >> kSmallT) * a.n <= nsm) per_sm = 1;  // few tile jobs: cheaper barriers
+  cudaLaunchConfig_t cfg;
+  memset(&cfg, 0, sizeof(cfg));
+  cfg.gridDim = dim3((unsigned)((nsm > 0 ? nsm : 148) * per_sm));
+  cfg.blockDim = dim3(1u << (kSmallT - 5));
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;  // grid barriers: every CTA co-resident
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  KScope ks(OPTR_K_SMALL, st, a.n);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, a);
+  if (e != cudaSuccess) {
+    fprintf(stderr, "optr: tar_small_local_kernel<%d> launch failed: %s\n", K, cudaGetErrorString(e));
+    return OPTR_ECUDA;
+  }
+  return OPTR_OK;
+}
+
+// n co-resident workers, D = 2^13..2^20 (RHT on, n a power of two <= 8):
+// the whole call in one cooperative launch (small.cuh)
+int tar_local_small(const void* const* x, void* const* out, int n, int64_t L, int dtype_in, int dtype_out,
+                    uint64_t seed, int r, const optr_mask_spec* masks, char* ws, const LocalLayout& lay,
+                    int epp, uint64_t* received_out, uint8_t* got_out, cudaStream_t st) {
+  const int64_t dim = lay.dim;
+  unsigned long long* counts = (unsigned long long*)(ws + lay.counts);
+  CK(cudaMemsetAsync(counts, 0, lay.bar + 8 - lay.counts, st));  // counts + barrier counter
+  SmallLocalArgs a;
+  memset(&a, 0, sizeof(a));
+  const uint32_t* cb = nullptr;
+  int rc = setup_masks(a.pa, masks, dim, n, r, epp, (uint32_t*)(ws + lay.bitmap), counts, 0, n, &cb);
+  if (rc) return rc;
+  if ((rc = ensure_device_init())) return rc;
+  const Pcg sp = sign_pcg(seed);
+  a.signs = (uint32_t*)(ws + lay.signs);
+  a.sign_state = sp.state;
+  a.sign_inc = sp.inc;
+  for (int w = 0; w < n; ++w) {
+    a.x[w] = x[w];
+    a.out[w] = out[w];
+    a.Y[w] = (float*)(ws + lay.y) + (size_t)w * dim;
+  }
+  a.dtype_in = dtype_in;
+  a.dtype_out = dtype_out;
+  a.L = L;
+  a.dim = dim;
+  a.bar = (unsigned long long*)(ws + lay.bar);
+  a.counts = counts;
+  a.got = got_out;
+  a.m = MaskView{cb, a.pa.pw, n, epp, make_divider((uint32_t)epp)};
+  a.n = n;
+  a.r = r;
+  a.shard_shift = log2_exact(dim / n);
+  a.trace = (unsigned long long*)g_small_trace;
+  switch (log2_exact(dim)) {
+    case 13: rc = launch_small_local_t<13>(a, st); break;
+    case 14: rc = launch_small_local_t<14>(a, st); break;
+    case 15: rc = launch_small_local_t<15>(a, st); break;
+    case 16: rc = launch_small_local_t<16>(a, st); break;
+    case 17: rc = launch_small_local_t<17>(a, st); break;
+    case 18: rc = launch_small_local_t<18>(a, st); break;
+    case 19: rc = launch_small_local_t<19>(a, st); break;
+    case 20: rc = launch_small_local_t<20>(a, st); break;
+    default: return OPTR_EINVAL;
+  }
+  if (rc) return rc;
+  if (received_out) CK(cudaMemcpyAsync(received_out, counts, (size_t)2 * n * 8, cudaMemcpyDeviceToDevice, st));
+  return OPTR_OK;
+}
+
 int tar_local_impl(const void* const* x, void* const* out, int n, int64_t L, int dtype_in, int dtype_out,
                    uint64_t job_seed, uint64_t bucket_id, uint64_t generation, int rotation, int ht,
                    const optr_mask_spec* masks, void* workspace, size_t workspace_bytes,
@@ -1121,9 +1220,13 @@ int tar_local_impl(const void* const* x, void* const* out, int n, int64_t L, int
   uint32_t* bitmap = (uint32_t*)(ws + lay.bitmap);
   unsigned long long* counts = (unsigned long long*)(ws + lay.counts);
   const Shards sh = make_shards(dim, n);
+  const int nlog = ht ? log2_exact(dim) : 0;
+  if (ht && small_enabled() && nlog >= kSmallMinLog && nlog <= kSmallMaxLog && n <= kSmallMaxRanks &&
+      (n & (n - 1)) == 0)
+    return tar_local_small(x, out, n, L, dtype_in, dtype_out, derive_seed(job_seed, bucket_id, generation), r,
+                           masks, ws, lay, epp, received_out, got_out, st);
   FastPlan fp;
   const bool fast = local_fast_plan(L, dim, n, ht, x, out, &fp);
-  const int nlog = ht ? log2_exact(dim) : 0;
 
   // 1. signs (+ transposed sign bytes for the strided passes) + masks + counts
   CK(cudaMemsetAsync(counts, 0, (size_t)2 * n * 8, st));
@@ -1563,7 +1666,6 @@ int optr_tar_bounded(optr_comm c, const void* x, void* out, int64_t L, int dtype
 }  // extern "C"
 
 namespace {
-void* g_small_trace = nullptr;  // optr_debug_trace with per_cta < 0: small-kernel phase stamps
 void* g_fused_trace = nullptr;  // optr_debug_trace
 int g_fused_trace_cap = 0;
 // OPTR_FUSED=0 keeps the barrier-separated encode / aggregate / decode path.
@@ -1641,15 +1743,6 @@ int launch_fused_t(const TmaArgs& ae, const TmaArgs& ad, const SnkBuf& se, const
   KScope ks(OPTR_K_FUSED, st);
   launch_ex(kern, dim3((unsigned)grid), dim3(threads), smem, st, ae, ad, se, sd, f);
   return launch_check(kern, "tma_fused", T, 0, grid, 1, threads, smem);
-}
-
-bool small_enabled() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("OPTR_SMALL");
-    v = (e && e[0] == '0') ? 0 : 1;
-  }
-  return v == 1;
 }
 
 template <int K>

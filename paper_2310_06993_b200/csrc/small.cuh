@@ -491,3 +491,222 @@ __global__ void __launch_bounds__(1 << (kSmallT - 5)) tar_small_kernel(const __g
 }
 
 }  // namespace optr
+
+namespace optr {
+
+// ---------------------------------------------------------------------------
+// The same one-launch plan for n co-resident workers on ONE GPU
+// (optr_tar_local, the reference simulator's shape: BASELINE configs[0]),
+// without flags: (0) signs + every (stage, dst, src) mask row + counts;
+// (1), (2) both encode passes of every worker; (3) every owner's stage-1
+// mean pushed into every receiver's Y under its stage-2 mask (received
+// flags optional); (4), (5) both decode passes of every worker.  Five grid
+// barriers on a counter the caller zeroes with the counts.
+struct SmallLocalArgs {
+  PrepArgs pa;  // every (stage, dst) row; counts zeroed before the launch
+  uint32_t* signs;
+  u128 sign_state, sign_inc;
+  const void* x[kMaxW];
+  void* out[kMaxW];
+  int dtype_in, dtype_out;
+  int64_t L, dim;
+  float* Y[kMaxW];                 // per-worker wire / stage-2 receive vectors
+  unsigned long long* bar;         // grid-barrier arrivals (zeroed before the launch)
+  unsigned long long* counts;      // [2][n]
+  uint8_t* got;                    // optional [n][dim] received flags
+  MaskView m;
+  int n, r, shard_shift;
+  unsigned long long* trace;  // optional debug stamps [8] (CTA 0, globaltimer ns)
+};
+
+__device__ __forceinline__ void small_local_stamp(const SmallLocalArgs& a, int i) {
+  if (a.trace && blockIdx.x == 0 && threadIdx.x == 0) a.trace[i] = small_clock_ns();
+}
+
+// every row (stage, dst, src != dst), one packet per thread (small_masks)
+__device__ __forceinline__ void small_local_masks(const SmallLocalArgs& a, int64_t gtid, int64_t gthreads,
+                                                  const JumpSmem& jt) {
+  const PrepArgs& pa = a.pa;
+  const int n = a.n;
+  const int64_t len = 1LL << a.shard_shift;
+  const int64_t np = n_packets(len, pa.epp);
+  const int64_t per_row = pa.pw * 32;
+  const int64_t total = (int64_t)2 * n * (n - 1) * per_row;
+  for (int64_t t = gtid; t < total; t += gthreads) {
+    const int row = (int)(t / per_row);
+    const int64_t p = t - (int64_t)row * per_row;
+    const int stage = row / (n * (n - 1));
+    const int rem = row - stage * n * (n - 1);
+    const int dst = rem / (n - 1), srci = rem - dst * (n - 1);
+    const int src = srci < dst ? srci : srci + 1;
+    const int64_t widx = ((int64_t)(stage * n + dst) * n + src) * pa.pw + (p >> 5);
+    bool keep = p < np;
+    if (pa.kind == OPTR_MASK_COIN && keep) {
+      const u128 s = jump_s(pa.coin_state[src], pa.coin_inc[src], coin_base(pa, stage, src, dst) + (uint64_t)p + 1, jt);
+      keep = !coin_drops(pcg_xsl_rr(s), pa.drop_prob);
+    } else if (pa.kind == OPTR_MASK_BITMAP && keep) {
+      keep = (__ldg(pa.bitmap_in + widx) >> (p & 31)) & 1u;
+    }
+    const uint32_t bits = __ballot_sync(0xffffffffu, keep);
+    if ((threadIdx.x & 31) == 0) {
+      if (pa.kind != OPTR_MASK_BITMAP) pa.bitmap_out[widx] = bits;
+      if (bits) {
+        unsigned long long e = (unsigned long long)__popc(bits) * (unsigned long long)pa.epp;
+        const int64_t last = np - 1 - (p & ~31LL);
+        if (last >= 0 && last < 32 && ((bits >> last) & 1u)) e -= (unsigned long long)(np * pa.epp - len);
+        atomicAdd(a.counts + stage * n + dst, e);
+      }
+    }
+  }
+}
+
+// every owner's masked mean (fp64, ascending worker order) pushed into every
+// receiver's Y under its stage-2 mask (collectives.py:77-94, 133-150)
+template <int NR>
+__device__ __forceinline__ void small_local_mean(const SmallLocalArgs& a, int64_t gtid, int64_t gthreads) {
+  const int64_t n4 = a.dim >> 2;
+  const int64_t smask = (1LL << a.shard_shift) - 1;
+#pragma unroll 2
+  for (int64_t g4 = gtid; g4 < n4; g4 += gthreads) {
+    const int64_t g = g4 * 4;
+    const int j = (int)(g >> a.shard_shift);
+    const int o = shard_owner(j, a.r, NR);
+    const uint32_t e = (uint32_t)(g & smask), wi = a.m.dv.div(e) >> 5;
+    float4 v[NR];
+    uint32_t w0[NR], w1[NR], s0[NR], s1[NR];
+#pragma unroll
+    for (int i = 0; i < NR; ++i) {
+      v[i] = ld_cg4(a.Y[i] + g);
+      const uint32_t* row = a.m.row(0, o, i);  // stage 1: sender i -> owner o
+      const uint32_t* srow = a.m.row(1, i, o);  // stage 2: owner o -> receiver i
+      const bool own = i == o;
+      w0[i] = own ? 0xffffffffu : __ldg(row + wi);
+      w1[i] = (own || wi + 1 >= (uint32_t)a.m.pw) ? 0xffffffffu : __ldg(row + wi + 1);
+      s0[i] = own ? 0xffffffffu : __ldg(srow + wi);
+      s1[i] = (own || wi + 1 >= (uint32_t)a.m.pw) ? 0xffffffffu : __ldg(srow + wi + 1);
+    }
+    double acc[4] = {0.0, 0.0, 0.0, 0.0}, cnt[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+    for (int i = 0; i < NR; ++i) {
+      const uint32_t kk = i == o ? 0xFu : keep4_words(e, w0[i], w1[i], a.m);
+      acc[0] += (kk & 1u) ? (double)v[i].x : 0.0;
+      acc[1] += (kk & 2u) ? (double)v[i].y : 0.0;
+      acc[2] += (kk & 4u) ? (double)v[i].z : 0.0;
+      acc[3] += (kk & 8u) ? (double)v[i].w : 0.0;
+      cnt[0] += (kk & 1u) ? 1.0 : 0.0;
+      cnt[1] += (kk & 2u) ? 1.0 : 0.0;
+      cnt[2] += (kk & 4u) ? 1.0 : 0.0;
+      cnt[3] += (kk & 8u) ? 1.0 : 0.0;
+    }
+    const float4 mv = make_float4(mean_of(acc[0], cnt[0]), mean_of(acc[1], cnt[1]), mean_of(acc[2], cnt[2]),
+                                  mean_of(acc[3], cnt[3]));
+#pragma unroll
+    for (int q = 0; q < NR; ++q) {
+      const uint32_t kk = q == o ? 0xFu : keep4_words(e, s0[q], s1[q], a.m);
+      st4(a.Y[q] + g, make_float4((kk & 1u) ? mv.x : 0.f, (kk & 2u) ? mv.y : 0.f, (kk & 4u) ? mv.z : 0.f,
+                                  (kk & 8u) ? mv.w : 0.f));
+      if (a.got)
+        *reinterpret_cast<uchar4*>(a.got + (int64_t)q * a.dim + g) =
+            make_uchar4(kk & 1u, (kk >> 1) & 1u, (kk >> 2) & 1u, (kk >> 3) & 1u);
+    }
+  }
+}
+
+template <int K>
+__global__ void __launch_bounds__(1 << (kSmallT - 5)) tar_small_local_kernel(const __grid_constant__ SmallLocalArgs a) {
+  extern __shared__ float sm[];
+  constexpr int T = kSmallT;
+  constexpr int CB = 2 * T - K;
+  const int64_t ntiles = a.dim >> T;
+  const int64_t njobs = ntiles * a.n;  // job = worker * ntiles + tile
+  const int G = gridDim.x;
+  const int tid = threadIdx.x;
+  const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + tid;
+  const int64_t gthreads = (int64_t)G * blockDim.x;
+  small_local_stamp(a, 0);
+  __shared__ JumpSmem jt;
+  if (tid < 64) {
+    jt.a[tid] = c_jump.a[tid];
+    jt.g[tid] = c_jump.g[tid];
+  }
+  __syncthreads();
+
+  // phase 0: signs (32 per item, hadamard.py:49-51), masks, counts
+  for (int64_t w = gtid; w < (a.dim >> 5); w += gthreads) {
+    u128 s = jump_s(a.sign_state, a.sign_inc, (uint64_t)w * 16 + 1, jt);
+    uint32_t word = 0;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const uint64_t o = pcg_xsl_rr(s);
+      word |= (uint32_t)((o >> 31) & 1u) << (2 * i);
+      word |= (uint32_t)(o >> 63) << (2 * i + 1);
+      s = pcg_step(s, a.sign_inc);
+    }
+    a.signs[w] = word;
+  }
+  small_local_masks(a, (int64_t)(G - 1 - blockIdx.x) * blockDim.x + tid, gthreads, jt);
+  small_grid_sync(a.bar, 1ULL * G);
+  small_local_stamp(a, 1);
+
+  // phase 1: encode pass 1 (contiguous) of every worker
+  for (int64_t k = blockIdx.x; k < njobs; k += G) {
+    const int w = (int)(k / ntiles);
+    SrcEncode::B eb{a.x[w], a.dtype_in, a.L, a.signs};
+    SmallEncodeSrc src{eb, (((uintptr_t)a.x[w]) & (a.dtype_in == OPTR_F32 ? 15 : 7)) == 0};
+    const SnkBuf::B dst{a.Y[w], K == T ? (float)(1.0 / sqrt((double)a.dim)) : 1.f};
+    rtile_do<T, 0, 0>(src, dst, k - (int64_t)w * ntiles, sm);
+  }
+  small_grid_sync(a.bar, 2ULL * G);
+  small_local_stamp(a, 2);
+
+  // phase 2: encode pass 2 (strided, in place)
+  if constexpr (K > T) {
+    for (int64_t k = blockIdx.x; k < njobs; k += G) {
+      const int w = (int)(k / ntiles);
+      SmallBufSrc src{a.Y[w]};
+      const SnkBuf::B dst{a.Y[w], (float)(1.0 / sqrt((double)a.dim))};
+      rtile_do<T, CB, T>(src, dst, k - (int64_t)w * ntiles, sm);
+    }
+  }
+  small_grid_sync(a.bar, 3ULL * G);
+  small_local_stamp(a, 3);
+
+  // phase 3: stage 1 at every owner, stage 2 pushed into every receiver
+  switch (a.n) {
+    case 2: small_local_mean<2>(a, gtid, gthreads); break;
+    case 4: small_local_mean<4>(a, gtid, gthreads); break;
+    default: small_local_mean<8>(a, gtid, gthreads); break;
+  }
+  small_grid_sync(a.bar, 4ULL * G);
+  small_local_stamp(a, 4);
+
+  // phases 4, 5: the decode passes of every worker (count scale, signs, cast)
+  const double D = (double)a.dim;
+  auto dec_sink = [&](int w) {
+    const unsigned long long c = (1ULL << a.shard_shift) + __ldcg(a.counts + a.n + w);
+    const SnkDecode::B db{a.out[w], a.dtype_out, a.L, a.signs, c == 0 ? 0.f : (float)((D / (double)c) / sqrt(D))};
+    return SmallDecodeSnk{db, (((uintptr_t)a.out[w]) & (a.dtype_out == OPTR_F32 ? 15 : 7)) == 0};
+  };
+  for (int64_t k = blockIdx.x; k < njobs; k += G) {
+    const int w = (int)(k / ntiles);
+    SmallBufSrc src{a.Y[w]};
+    if constexpr (K == T) {
+      rtile_do<T, 0, 0>(src, dec_sink(w), k - (int64_t)w * ntiles, sm);
+    } else {
+      const SnkBuf::B dst{a.Y[w], 1.f};
+      rtile_do<T, 0, 0>(src, dst, k - (int64_t)w * ntiles, sm);
+    }
+  }
+  if constexpr (K > T) {
+    small_grid_sync(a.bar, 5ULL * G);
+    small_local_stamp(a, 5);
+    for (int64_t k = blockIdx.x; k < njobs; k += G) {
+      const int w = (int)(k / ntiles);
+      SmallBufSrc src{a.Y[w]};
+      rtile_do<T, CB, T>(src, dec_sink(w), k - (int64_t)w * ntiles, sm);
+    }
+  }
+  small_local_stamp(a, 6);
+}
+
+}  // namespace optr
