@@ -1178,6 +1178,7 @@ int tar_local_small(const void* const* x, void* const* out, int n, int64_t L, in
   a.bar = (unsigned long long*)(ws + lay.bar);
   a.counts = counts;
   a.got = got_out;
+  a.received_out = (unsigned long long*)received_out;
   a.m = MaskView{cb, a.pa.pw, n, epp, make_divider((uint32_t)epp)};
   a.n = n;
   a.r = r;
@@ -1194,9 +1195,7 @@ int tar_local_small(const void* const* x, void* const* out, int n, int64_t L, in
     case 20: rc = launch_small_local_t<20>(a, st); break;
     default: return OPTR_EINVAL;
   }
-  if (rc) return rc;
-  if (received_out) CK(cudaMemcpyAsync(received_out, counts, (size_t)2 * n * 8, cudaMemcpyDeviceToDevice, st));
-  return OPTR_OK;
+  return rc;
 }
 
 int tar_local_impl(const void* const* x, void* const* out, int n, int64_t L, int dtype_in, int dtype_out,

@@ -514,6 +514,7 @@ struct SmallLocalArgs {
   unsigned long long* bar;         // grid-barrier arrivals (zeroed before the launch)
   unsigned long long* counts;      // [2][n]
   uint8_t* got;                    // optional [n][dim] received flags
+  unsigned long long* received_out;  // optional [2][n] copy of the counts
   MaskView m;
   int n, r, shard_shift;
   unsigned long long* trace;  // optional debug stamps [8] (CTA 0, globaltimer ns)
@@ -679,6 +680,7 @@ __global__ void __launch_bounds__(1 << (kSmallT - 5)) tar_small_local_kernel(con
   }
   small_grid_sync(a.bar, 4ULL * G);
   small_local_stamp(a, 4);
+  if (a.received_out && blockIdx.x == 0 && tid < 2 * a.n) a.received_out[tid] = __ldcg(a.counts + tid);
 
   // phases 4, 5: the decode passes of every worker (count scale, signs, cast)
   const double D = (double)a.dim;
