@@ -724,6 +724,95 @@ __global__ void __launch_bounds__(1 << (T - 5), T == 13 ? 2 : 1) tma_mean_kernel
   }
 }
 
+// ------------------ stage-2 receive + contiguous decode pass (one GPU)
+// Every co-resident receiver's decode input for contiguous tile t is the
+// owner's aggregate tile under that receiver's stage-2 mask, transformed.
+// Receivers whose stage-2 packets over the tile all arrived (tile_ok2 bit;
+// the owner always) get the SAME tile: one transform, stored into each of
+// their wire vectors; a receiver with a lost packet over the tile gets its
+// own masked transform.  A CTA walks its tiles; per tile one job for the
+// clean group, then one per masked receiver, each job one TMA load of the
+// (L2-resident) aggregate tile through the ring.
+struct GatherSharedArgs {
+  float* y[kMaxW];  // each receiver's decode buffer (its wire vector)
+};
+
+template <int T, int kStages, int NW>
+__global__ void __launch_bounds__(1 << (T - 5), T == 13 ? 2 : 1)
+    tma_gather_shared_kernel(const __grid_constant__ TmaArgs a, const __grid_constant__ GatherSharedArgs ys) {
+  constexpr size_t SB = tma_stage_bytes<T>();
+  constexpr RPlan P = make_rplan(T, 0);
+  constexpr int LR = P.nr - 1;
+  static_assert(P.pos[LR][0] == 0, "vector groups in the last round");
+  constexpr int VW = P.pos[LR][1] == 1 ? 4 : 2;
+  constexpr int NQ = 32 / VW;
+  constexpr uint32_t kAll = (NW >= 32) ? 0xffffffffu : ((1u << NW) - 1u);
+  extern __shared__ __align__(16) unsigned char smraw[];
+  unsigned char* const base = smraw + ((1024u - (smem_u32(smraw) & 1023u)) & 1023u);
+  uint64_t* const full = reinterpret_cast<uint64_t*>(base + kStages * SB);
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    for (int s = 0; s < kStages; ++s) mbar_init(&full[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  const int64_t stride = gridDim.x;
+  auto owner_of = [&](int64_t t) { return shard_owner((int)((t << T) >> a.shard_shift), a.r, NW); };
+  auto ok_of = [&](int64_t t) { return (__ldg(a.tile_ok2 + t) | (1u << owner_of(t))) & kAll; };
+  // issue cursor (thread 0 only): the tile of every job, kStages ahead
+  int64_t it = blockIdx.x;
+  int ij = 0, in = it < a.ntiles ? 1 + __popc(kAll & ~ok_of(it)) : 0;
+  auto issue_next = [&](int s) {
+    if (it >= a.ntiles) return;
+    tile_issue_contig<T, TS_GATHER>(a, 0, it, base + (size_t)s * SB, &full[s]);
+    if (++ij == in) {
+      ij = 0;
+      it += stride;
+      in = it < a.ntiles ? 1 + __popc(kAll & ~ok_of(it)) : 0;
+    }
+  };
+  if (tid == 0)
+    for (int s = 0; s < kStages; ++s) issue_next(s);
+  const SnkBuf::B nosnk{nullptr, 1.f};
+  int64_t k = 0;
+  for (int64_t t = blockIdx.x; t < a.ntiles; t += stride) {
+    const int owner = owner_of(t);
+    const uint32_t ok = ok_of(t);
+    uint32_t todo = kAll & ~ok;
+    for (bool first = true;; first = false) {
+      const int s = (int)(k % kStages);
+      mbar_wait(&full[s], (uint32_t)((k / kStages) & 1));
+      int q = owner;
+      uint32_t dests = ok;
+      if (!first) {
+        q = __ffs(todo) - 1;
+        todo &= todo - 1;
+        dests = 1u << q;
+      }
+      tma_tile<T, false, TS_GATHER, SnkBuf, 3>(
+          nullptr, nullptr, a, nosnk, q, nullptr, t, base + (size_t)s * SB, [&]() { issue_next(s); },
+          [&](const float (&v)[32], int b2) {
+            for (uint32_t d = dests; d; d &= d - 1) {
+              float* const yo = ys.y[__ffs(d) - 1] + (t << T);
+#pragma unroll
+              for (int m = 0; m < NQ; ++m) {
+                const int i = b2 + roff(P, LR, VW * m);
+                if constexpr (VW == 4)
+                  st4(yo + i, make_float4(v[4 * m], v[4 * m + 1], v[4 * m + 2], v[4 * m + 3]));
+                else
+                  *reinterpret_cast<float2*>(yo + i) = make_float2(v[2 * m], v[2 * m + 1]);
+              }
+            }
+          },
+          first);
+      ++k;
+      if (!todo) break;
+    }
+  }
+}
+
 __device__ __forceinline__ void fence_proxy_async_global() {
   asm volatile("fence.proxy.async.global;" ::: "memory");
 }
