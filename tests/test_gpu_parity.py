@@ -333,6 +333,27 @@ def test_fast_plan_vs_oracle_d23(dev):
         np.testing.assert_array_equal(got[node].astype(bool), tar[node][1])
 
 
+@pytest.mark.parametrize("n,L,p,gen", [(4, 4_500_001, 0.01, 3), (2, 9_000_000, 0.05, 1), (2, 17_000_000, 0.02, 2)])
+def test_fast_plan_shared_decode_vs_oracle(dev, n, L, p, gen):
+    """The fast plan without received flags: the stage-2 receive + contiguous
+    decode runs once per tile for every receiver its packets reached intact
+    (tma_gather_shared_kernel; 2^13 tiles at D = 2^23 / 2^24, 2^14 at 2^25)
+    -- per node within 1e-5 of the oracle, received counts bit-exact."""
+    seed, coin_seed = 23, 777 + gen
+    r = gen % n
+    dim = O.next_pow2(L)
+    buckets = O.make_buckets(seed, n, L)
+    masks = O.datagram_masks(coin_seed, dim, n, r, p)
+    want = O.run_generation(buckets, seed, gen, True, masks=masks, r=r, threads=n)
+    outs, counts, got = _run_local(buckets, r, True, seed, gen, MaskSpec.coin(coin_seed, p), dev,
+                                   want_received=False)
+    assert got is None
+    for node in range(n):
+        assert rel_err(outs[node], want[node]) < REL, node
+    for (stage, dst), (rcv, _exp) in O.stage_counts(masks, dim, n, r, 350).items():
+        assert counts[stage - 1, dst] == rcv
+
+
 def test_tar_allreduce_reference_signature(dev):
     """collectives.tar_allreduce (the reference's name and result type) is
     bit-exact with the reference's masked TAR on encoded vectors."""
