@@ -184,7 +184,7 @@ def step_alg_bytes(buckets, n_workers, s_in, s_out, ht):
 NCU_NAMES = {  # regexes for the one-GPU fast plan (stage count free: it depends on the tile shape)
     "enc_first": r"tma_pass_kernel<\d+, \d, 1, 1,",
     "enc_mean": r"tma_mean_kernel",
-    "dec_first": r"tma_pass_kernel<\d+, \d, 0, 2,",
+    "dec_first": r"tma_gather_shared_kernel|tma_pass_kernel<\d+, \d, 0, 2,",
     "dec_last": r"tma_pass_kernel<\d+, \d, 1, 0, SnkDecode",
     "aggregate": r"tma_agg_kernel",
     "prep": r"prep_kernel",
