@@ -1067,16 +1067,13 @@ bool local_fast_plan(int64_t L, int64_t dim, int n, int ht, const void* const* x
   return true;
 }
 
-static int env_stages(const char* name) {
-  const char* e = getenv(name);
-  return (e && atoi(e) == 3) ? 3 : 2;
-}
-
-template <int T, int NW, int S>
+template <int T, int NW>
 int launch_mean_t(const TmaArgs& a, const MeanArgs& m, cudaStream_t st) {
   // two CTAs per SM (<= 128 registers: the fp64 accumulators take 64) with a
   // two-stage ring: 61.5 us per 2^23 bucket of 4 workers against 71.6 us for
-  // one CTA with three stages (140 registers; profiles/r02_quick_mean_ab.txt)
+  // one CTA with three stages (140 registers; profiles/r02_quick_mean_ab.txt);
+  // three stages at two CTAs per SM measured the same (0.795 vs 0.798 ms)
+  constexpr int S = 2;
   const size_t smem = tma_smem_bytes<T, S>();
   auto kern = tma_mean_kernel<T, S, NW>;
   int rc = set_smem_attr(kern, smem);
@@ -1097,8 +1094,9 @@ int launch_mean_t(const TmaArgs& a, const MeanArgs& m, cudaStream_t st) {
 
 // stage-2 receive + contiguous decode of every co-resident worker, shared
 // across the receivers with clean tiles (tma_gather_shared_kernel)
-template <int T, int NW, int S>
+template <int T, int NW>
 int launch_gather_shared_t(const TmaArgs& a, const GatherSharedArgs& ys, cudaStream_t st) {
+  constexpr int S = 2;  // (three stages: the same, 47.8 vs 47.4 us)
   const size_t smem = tma_smem_bytes<T, S>();
   auto kern = tma_gather_shared_kernel<T, S, NW>;
   int rc = set_smem_attr(kern, smem);
@@ -1118,32 +1116,22 @@ int launch_gather_shared_t(const TmaArgs& a, const GatherSharedArgs& ys, cudaStr
 
 template <int T>
 int launch_gather_shared(const TmaArgs& a, const GatherSharedArgs& ys, cudaStream_t st) {
-  static const int S = env_stages("OPTR_GS_STAGES");
-  switch (a.n * 10 + S) {
-    case 22: return launch_gather_shared_t<T, 2, 2>(a, ys, st);
-    case 42: return launch_gather_shared_t<T, 4, 2>(a, ys, st);
-    case 82: return launch_gather_shared_t<T, 8, 2>(a, ys, st);
-    case 162: return launch_gather_shared_t<T, 16, 2>(a, ys, st);
-    case 23: return launch_gather_shared_t<T, 2, 3>(a, ys, st);
-    case 43: return launch_gather_shared_t<T, 4, 3>(a, ys, st);
-    case 83: return launch_gather_shared_t<T, 8, 3>(a, ys, st);
-    case 163: return launch_gather_shared_t<T, 16, 3>(a, ys, st);
+  switch (a.n) {
+    case 2: return launch_gather_shared_t<T, 2>(a, ys, st);
+    case 4: return launch_gather_shared_t<T, 4>(a, ys, st);
+    case 8: return launch_gather_shared_t<T, 8>(a, ys, st);
+    case 16: return launch_gather_shared_t<T, 16>(a, ys, st);
     default: return OPTR_EINVAL;
   }
 }
 
 template <int T>
 int launch_mean_n(const TmaArgs& a, const MeanArgs& m, cudaStream_t st) {
-  static const int S = env_stages("OPTR_MEAN_STAGES");
-  switch (m.n * 10 + S) {
-    case 22: return launch_mean_t<T, 2, 2>(a, m, st);
-    case 42: return launch_mean_t<T, 4, 2>(a, m, st);
-    case 82: return launch_mean_t<T, 8, 2>(a, m, st);
-    case 162: return launch_mean_t<T, 16, 2>(a, m, st);
-    case 23: return launch_mean_t<T, 2, 3>(a, m, st);
-    case 43: return launch_mean_t<T, 4, 3>(a, m, st);
-    case 83: return launch_mean_t<T, 8, 3>(a, m, st);
-    case 163: return launch_mean_t<T, 16, 3>(a, m, st);
+  switch (m.n) {
+    case 2: return launch_mean_t<T, 2>(a, m, st);
+    case 4: return launch_mean_t<T, 4>(a, m, st);
+    case 8: return launch_mean_t<T, 8>(a, m, st);
+    case 16: return launch_mean_t<T, 16>(a, m, st);
     default: return OPTR_EINVAL;
   }
 }
