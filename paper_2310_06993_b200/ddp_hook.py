@@ -88,7 +88,7 @@ def optireduce_hook(state: OptiReduceState, bucket):
         buf = buf.contiguous()
     comm = state.communicator(buf.device, buf.numel())
     out = torch.empty_like(buf)
-    rec = torch.zeros(2, dtype=torch.int64, device=buf.device)
+    rec = torch.empty(2, dtype=torch.int64, device=buf.device)  # both entries written by the call
     world = comm.world
     comm.allreduce(buf, out, rotation=state.generation % world, ht=state.ht, job_seed=state.seed,
                    generation=state.generation, bucket_id=bucket.index(), masks=state.masks(bucket.index()),

@@ -47,6 +47,7 @@ def main():
     ap.add_argument("--model", default="resnet50", choices=["resnet50", "gpt2"])
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--ctas", default="32", help="comma list of fused-kernel CTA caps to time as extra modes")
     args = ap.parse_args()
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", "0")))
@@ -57,8 +58,9 @@ def main():
     from paper_2310_06993_b200.ddp_hook import OptiReduceState, max_bucket_len_for, optireduce_hook
 
     modes = [("nccl_allreduce", None), ("optireduce_lossless", dict(drop_prob=0.0)),
-             ("optireduce_1pct_drops", dict(drop_prob=0.01)),
-             ("optireduce_lossless_32ctas", dict(drop_prob=0.0, fused_ctas=32))]
+             ("optireduce_1pct_drops", dict(drop_prob=0.01))]
+    modes += [(f"optireduce_lossless_{c}ctas", dict(drop_prob=0.0, fused_ctas=int(c)))
+              for c in args.ctas.split(",") if c]
     for name, hook_kw in modes:
         torch.manual_seed(0)
         model, loss_fn = build(args.model, dev)
