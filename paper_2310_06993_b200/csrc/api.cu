@@ -300,6 +300,7 @@ bool make_map3(CUtensorMap* m, const void* base, uint64_t d0, uint64_t d1, uint6
 }
 bool make_map3_uncached(CUtensorMap* m, const void* base, uint64_t d0, uint64_t d1, uint64_t d2, uint32_t box1,
                         int dtype, uint32_t box0) {
+  if (((uintptr_t)base) & 15) return false;  // TMA needs a 16-byte aligned global address: LSU path
   const uint64_t esz = dtype == OPTR_BF16 ? 2 : 4;
   cuuint64_t dims[3] = {d0, d1, d2};
   cuuint64_t strides[2] = {d0 * esz, d0 * d1 * esz};

@@ -386,8 +386,12 @@ struct SrcEncode {
       if (g >= L) return 0.f;
       return sgn(__ldg(signs + (g >> 5)), (int)(g & 31), load_elem(x, dtype, g));
     }
+    // vector loads need x 16-byte (fp32) / 8-byte (bf16) aligned
+    __device__ __forceinline__ bool vec_ok() const {
+      return (((uintptr_t)x) & (dtype == OPTR_F32 ? 15 : 7)) == 0;
+    }
     __device__ __forceinline__ float4 load4(int64_t g) const {
-      if (g + 4 <= L) {
+      if (g + 4 <= L && vec_ok()) {
         float4 v;
         if (dtype == OPTR_F32) {
           v = ldg4((const float*)x + g);
@@ -578,8 +582,10 @@ struct SnkDecode {
       if (g >= L) return;
       store_elem(out, dtype, g, sgn(__ldg(signs + (g >> 5)), (int)(g & 31), v * scale));
     }
+    // vector stores need out 16-byte (fp32 x4) / 8-byte aligned
+    __device__ __forceinline__ bool vec_ok(int bytes) const { return (((uintptr_t)out) & (bytes - 1)) == 0; }
     __device__ __forceinline__ void store2(int64_t g, float a, float b) const {
-      if (g + 2 <= L) {
+      if (g + 2 <= L && vec_ok(dtype == OPTR_F32 ? 8 : 4)) {
         uint32_t w = __ldg(signs + (g >> 5));
         int b0 = (int)(g & 31);
         a = sgn(w, b0, a * scale);
@@ -594,7 +600,7 @@ struct SnkDecode {
       store1(g + 1, b);
     }
     __device__ __forceinline__ void store4(int64_t g, float4 v) const {
-      if (g + 4 <= L) {
+      if (g + 4 <= L && vec_ok(dtype == OPTR_F32 ? 16 : 8)) {
         uint32_t w = __ldg(signs + (g >> 5));
         int b0 = (int)(g & 31);
         v.x = sgn(w, b0, v.x * scale);

@@ -365,3 +365,27 @@ def test_tar_allreduce_reference_signature(dev):
     for node in range(n):
         np.testing.assert_array_equal(res[node].entries.cpu().numpy(), want[node][0])
         np.testing.assert_array_equal(res[node].received.cpu().numpy(), want[node][1])
+
+
+@pytest.mark.parametrize("L", [60_000, 4_500_001])
+def test_local_unaligned_buffers_vs_oracle(dev, L):
+    """Co-resident workers whose buffers are offset by one float: the
+    small-bucket kernel's scalar paths (D = 2^16) and the general plan that
+    replaces the aligned-only fast plan (D = 2^23) match the oracle."""
+    n, p, gen, seed, coin_seed = 4, 0.02, 1, 31, 4242
+    r = gen % n
+    dim = O.next_pow2(L)
+    buckets = O.make_buckets(seed, n, L)
+    masks = O.datagram_masks(coin_seed, dim, n, r, p)
+    want = O.run_generation(buckets, seed, gen, True, masks=masks, r=r, threads=n)
+    xs, outs = [], []
+    for b in buckets:
+        xb = torch.zeros(L + 1, device=dev)
+        xb[1:] = torch.from_numpy(b).to(dev)
+        xs.append(xb[1:])
+        outs.append(torch.empty(L + 1, device=dev)[1:])
+    tar_allreduce_local(xs, rotation=r, ht=True, job_seed=seed, generation=gen,
+                        masks=MaskSpec.coin(coin_seed, p), out=outs)
+    torch.cuda.synchronize()
+    for node in range(n):
+        assert rel_err(outs[node].cpu().numpy(), want[node]) < REL, node
