@@ -1,6 +1,9 @@
 """Summarise bench JSON lines: python tools/show.py FILE... (one line per file)."""
 import json
+import signal
 import sys
+
+signal.signal(signal.SIGPIPE, signal.SIG_DFL)  # quiet under `| head`
 
 for f in sys.argv[1:]:
     for line in open(f):
