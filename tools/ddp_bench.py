@@ -57,7 +57,7 @@ def main():
 
     from paper_2310_06993_b200.ddp_hook import OptiReduceState, max_bucket_len_for, optireduce_hook
 
-    modes = [("nccl_allreduce", None), ("optireduce_lossless", dict(drop_prob=0.0)),
+    modes = [("nccl_allreduce", None), ("noop_hook", None), ("optireduce_lossless", dict(drop_prob=0.0)),
              ("optireduce_1pct_drops", dict(drop_prob=0.01))]
     modes += [(f"optireduce_lossless_{c}ctas", dict(drop_prob=0.0, fused_ctas=int(c)))
               for c in args.ctas.split(",") if c]
@@ -66,7 +66,14 @@ def main():
         model, loss_fn = build(args.model, dev)
         ddp = DDP(model, device_ids=[dev.index], bucket_cap_mb=25)
         state = None
-        if hook_kw is not None:
+        if name == "noop_hook":  # hook framework cost alone: no communication at all
+            def noop(_st, bucket):
+                fut = torch.futures.Future()
+                fut.set_result(bucket.buffer())
+                return fut
+            ddp.register_comm_hook(None, noop)
+            hook_kw = None
+        elif hook_kw is not None:
             state = OptiReduceState(max_bucket_len=max_bucket_len_for(model, 25), ht=True, seed=1, **hook_kw)
             ddp.register_comm_hook(state, optireduce_hook)
         opt = torch.optim.SGD(ddp.parameters(), lr=1e-3)
