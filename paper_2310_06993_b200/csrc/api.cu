@@ -328,7 +328,13 @@ int launch_tma_pass_s(int cls, const TmaMaps& maps, const TmaMaps& dmaps, const 
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     if (nsm <= 0) nsm = 148;
   }
+  // CTAs per SM by shared memory, capped by what is resident (registers can
+  // bind first: a grid past residency runs as a partial second wave)
   int per_sm = (int)((227 * 1024) / (smem + 1024));
+  int resident = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, kern, 1 << (T - 5), smem) == cudaSuccess &&
+      resident >= 1 && resident < per_sm)
+    per_sm = resident;
   if (per_sm < 1) per_sm = 1;
   int64_t gx = ((int64_t)nsm * per_sm + nworkers - 1) / nworkers;
   if (gx > a.ntiles) gx = a.ntiles;
@@ -346,6 +352,7 @@ int launch_tma_pass_s(int cls, const TmaMaps& maps, const TmaMaps& dmaps, const 
 template <int T, bool STRIDED, int SK, class Snk, int CBW = 3>
 int launch_tma_pass(int cls, const TmaMaps& maps, const TmaMaps& dmaps, const TmaArgs& a, const Snk& snk,
                     int worker, int nworkers, cudaStream_t st) {
+  // (T = 14 strided with one stage at two CTAs per SM: 242 -> 262 us at N=1)
   if constexpr (STRIDED && T >= 13)
     return launch_tma_pass_s<T, 3, STRIDED, SK, Snk, CBW>(cls, maps, dmaps, a, snk, worker, nworkers, st);
   else
