@@ -1155,41 +1155,6 @@ bool small_enabled() {
   return v == 1;
 }
 
-template <int K>
-int launch_small_local_t(const SmallLocalArgs& a, cudaStream_t st) {
-  auto kern = tar_small_local_kernel<K>;
-  const size_t smem = sizeof(float) * (size_t)pad(1 << kSmallT);
-  int rc = set_smem_attr(kern, smem);
-  if (rc) return rc;
-  int dev = 0, nsm = 148, per_sm = 1;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  // every co-resident CTA (cooperative): more tile jobs per pass in flight
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 1 << (kSmallT - 5), smem) != cudaSuccess ||
-      per_sm < 1)
-    per_sm = 1;
-  if (per_sm > 2) per_sm = 2;
-  if ((a.dim >> kSmallT) * a.n <= nsm) per_sm = 1;  // few tile jobs: cheaper barriers
-  cudaLaunchConfig_t cfg;
-  memset(&cfg, 0, sizeof(cfg));
-  cfg.gridDim = dim3((unsigned)((nsm > 0 ? nsm : 148) * per_sm));
-  cfg.blockDim = dim3(1u << (kSmallT - 5));
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeCooperative;  // grid barriers: every CTA co-resident
-  attr[0].val.cooperative = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  KScope ks(OPTR_K_SMALL, st, a.n);
-  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, a);
-  if (e != cudaSuccess) {
-    fprintf(stderr, "optr: tar_small_local_kernel<%d> launch failed: %s\n", K, cudaGetErrorString(e));
-    return OPTR_ECUDA;
-  }
-  return OPTR_OK;
-}
-
 // n co-resident workers, D = 2^13..2^20 (RHT on, n a power of two <= 8):
 // the whole call in one cooperative launch (small.cuh)
 int tar_local_small(const void* const* x, void* const* out, int n, int64_t L, int dtype_in, int dtype_out,
@@ -1226,16 +1191,9 @@ int tar_local_small(const void* const* x, void* const* out, int n, int64_t L, in
   a.r = r;
   a.shard_shift = log2_exact(dim / n);
   a.trace = (unsigned long long*)g_small_trace;
-  switch (log2_exact(dim)) {
-    case 13: rc = launch_small_local_t<13>(a, st); break;
-    case 14: rc = launch_small_local_t<14>(a, st); break;
-    case 15: rc = launch_small_local_t<15>(a, st); break;
-    case 16: rc = launch_small_local_t<16>(a, st); break;
-    case 17: rc = launch_small_local_t<17>(a, st); break;
-    case 18: rc = launch_small_local_t<18>(a, st); break;
-    case 19: rc = launch_small_local_t<19>(a, st); break;
-    case 20: rc = launch_small_local_t<20>(a, st); break;
-    default: return OPTR_EINVAL;
+  {
+    KScope ks(OPTR_K_SMALL, st, n);
+    rc = optr_small_local_launch(log2_exact(dim), a, st);
   }
   return rc;
 }
@@ -1807,44 +1765,9 @@ int launch_fused_t(const TmaArgs& ae, const TmaArgs& ad, const SnkBuf& se, const
   return launch_check(kern, "tma_fused", T, 0, grid, 1, threads, smem);
 }
 
-template <int K>
-int launch_small_t(const SmallArgs& a, int grid, cudaStream_t st) {
-  auto kern = tar_small_kernel<K>;
-  const size_t smem = sizeof(float) * (size_t)pad(1 << kSmallT);
-  int rc = set_smem_attr(kern, smem);
-  if (rc) return rc;
-  cudaLaunchConfig_t cfg;
-  memset(&cfg, 0, sizeof(cfg));
-  cfg.gridDim = dim3((unsigned)grid);
-  cfg.blockDim = dim3(1u << (kSmallT - 5));
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeCooperative;  // grid barriers: every CTA co-resident
-  attr[0].val.cooperative = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;  // (a plain launch measured the same: 2-GPU 64 KB-4 MB within 1%)
-  KScope ks(OPTR_K_SMALL, st);
-  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, a);
-  if (e != cudaSuccess) {
-    fprintf(stderr, "optr: tar_small_kernel<%d> grid=%d launch failed: %s\n", K, grid, cudaGetErrorString(e));
-    return OPTR_ECUDA;
-  }
-  return OPTR_OK;
-}
-
 int launch_small(int K, const SmallArgs& a, int grid, cudaStream_t st) {
-  switch (K) {
-    case 13: return launch_small_t<13>(a, grid, st);
-    case 14: return launch_small_t<14>(a, grid, st);
-    case 15: return launch_small_t<15>(a, grid, st);
-    case 16: return launch_small_t<16>(a, grid, st);
-    case 17: return launch_small_t<17>(a, grid, st);
-    case 18: return launch_small_t<18>(a, grid, st);
-    case 19: return launch_small_t<19>(a, grid, st);
-    case 20: return launch_small_t<20>(a, grid, st);
-    default: return OPTR_EINVAL;
-  }
+  KScope ks(OPTR_K_SMALL, st);
+  return optr_small_launch(K, a, grid, st);
 }
 
 // CTAs of the small kernel: one per SM (stage 1's NVLink loads, the signs

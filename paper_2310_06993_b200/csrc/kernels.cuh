@@ -242,11 +242,15 @@ __device__ __forceinline__ void prep_item(const PrepArgs& a, int64_t t);
 
 // One work item per thread; a capped grid strides over the items (the
 // multi-GPU path runs prep as a thin background kernel on a side stream).
+// (translation units that only need the device helpers -- small.cu --
+// define OPTR_NO_GLOBAL_KERNELS: the non-template kernels live in api.cu)
+#ifndef OPTR_NO_GLOBAL_KERNELS
 __global__ void __launch_bounds__(256) prep_kernel(const __grid_constant__ PrepArgs a) {
   const int64_t total = a.sign_threads + a.mask_threads;
   for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x)
     prep_item(a, t);
 }
+#endif
 
 __device__ __forceinline__ void prep_item(const PrepArgs& a, int64_t t) {
   if (t < a.sign_threads) {
@@ -1097,6 +1101,7 @@ struct MeanRecvArgs {
   float* out;
 };
 
+#ifndef OPTR_NO_GLOBAL_KERNELS
 __global__ void __launch_bounds__(256) mean_received_kernel(const __grid_constant__ MeanRecvArgs a) {
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < a.len; e += (int64_t)gridDim.x * blockDim.x) {
     double acc = 0.0, cnt = 0.0;
@@ -1112,6 +1117,7 @@ __global__ void __launch_bounds__(256) mean_received_kernel(const __grid_constan
     a.out[e] = cnt > 0.0 ? mean_of(acc, cnt) : 0.f;
   }
 }
+#endif
 
 // ------------------------------------------------------------- assemble
 struct AsmArgs {
@@ -1122,6 +1128,7 @@ struct AsmArgs {
   int worker_base;
 };
 
+#ifndef OPTR_NO_GLOBAL_KERNELS
 __global__ void __launch_bounds__(256) assemble_kernel(const __grid_constant__ AsmArgs a) {
   const int q = a.worker_base + blockIdx.y;
   auto s = a.gather.bind(q);
@@ -1144,8 +1151,10 @@ __global__ void __launch_bounds__(256) assemble_kernel(const __grid_constant__ A
        g += (int64_t)gridDim.x * blockDim.x)
     store_elem(out, a.dtype, g, s.load1(g));
 }
+#endif
 
 // fp32/bf16 -> fp32 copy (RHT off: the wire carries float32, runner.py:228)
+#ifndef OPTR_NO_GLOBAL_KERNELS
 __global__ void cast_copy_kernel(const void* x, int dtype, float* y, int64_t n) {
   for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < n; g += (int64_t)gridDim.x * blockDim.x)
     y[g] = load_elem(x, dtype, g);
@@ -1158,5 +1167,6 @@ __global__ void count_mask_kernel(const uint8_t* mask, int64_t n, unsigned long 
   for (int o = 16; o; o >>= 1) c += __shfl_down_sync(0xffffffffu, c, o);
   if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, c);
 }
+#endif
 
 }  // namespace optr
