@@ -1818,7 +1818,13 @@ static int tar_enqueue(optr_comm c, const void* x, void* out, int64_t L, int dty
   int epp = masks ? masks->epp : 350;
   int64_t dim = ht ? next_pow2_i(L) : L;
   if (dim > c->max_dim) return OPTR_EINVAL;
-  if (L == 0) return OPTR_OK;
+  if (L == 0) {  // nothing to exchange: zero received entries
+    if (received_out) {
+      CK(cudaSetDevice(c->device));
+      CK(cudaMemsetAsync(received_out, 0, 2 * sizeof(uint64_t), (cudaStream_t)stream));
+    }
+    return OPTR_OK;
+  }
   if (L > 0 && (!x || !out)) return OPTR_EINVAL;
   for (int i = 0; i < n; ++i)
     if (!c->peer[i]) return OPTR_EINVAL;  // optr_comm_open not called
