@@ -51,3 +51,30 @@ def test_ddp_hook_host_logic():
     st.generation += 1
     assert st.masks(1).seed != a.seed  # per generation (and bucket) coin streams
     assert st.masks(2).seed != st.masks(1).seed
+
+
+def test_reference_arm_json_contract():
+    """`bench.py --impl reference` (the driver's reference arm: the oracle port
+    on the host cores, no GPU) prints one JSON line with the contract's keys,
+    on our arm's metric / unit / config."""
+    import json
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    res = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--workload", "cfg1", "--steps", "1",
+                          "--warmup", "1"], cwd=root, capture_output=True, text=True, timeout=600)
+    assert res.returncode == 0, res.stderr[-2000:]
+    lines = [line for line in res.stdout.splitlines() if line.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
+              "vs_baseline", "dtype", "data", "config", "impl", "cpu_baseline", "e2e"):
+        assert k in d, k
+    assert d["impl"] == "reference" and d["value"] > 0 and d["higher_is_better"] is True
+    assert d["metric"] == "bucket allreduce GB/s (TAR+RHT)" and d["unit"] == "GB/s"
+    assert d["config"]["workload"] == "cfg1" and d["config"]["same_config"] is True
+    assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["value"] == d["value"]
+    for k in ("value", "unit", "cores", "kind", "sample"):
+        assert k in d["cpu_baseline"], k
