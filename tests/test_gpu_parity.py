@@ -196,7 +196,7 @@ def test_sim_capture_replay_vs_reference(dev):
 @pytest.mark.parametrize("n,L,p,gen", [
     (2, 1000, 0.05, 0), (3, 4097, 0.1, 1), (4, 1 << 16, 0.01, 2), (5, 12345, 0.02, 3),
     (8, 100000, 0.05, 4), (8, 1 << 20, 0.01, 9), (4, 1, 0.0, 0), (8, 3, 0.0, 1), (6, 7, 0.3, 2),
-    (16, 50000, 0.05, 5)])
+    (16, 50000, 0.05, 5), (2, 50000, 0.05, 6), (2, 1 << 20, 0.01, 7)])
 def test_tar_rht_coin_vs_oracle(dev, n, L, p, gen):
     seed, coin_seed = 11, 1000 + gen
     r = gen % n
