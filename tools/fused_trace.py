@@ -18,6 +18,8 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--L", type=int, default=25_000_000)
 ap.add_argument("--tag", default="tr")
 ap.add_argument("--cap", type=int, default=256)
+ap.add_argument("--steady", type=int, default=0,
+                help="trace the last of this many back-to-back async calls (steady state, no barrier skew)")
 args = ap.parse_args()
 rank = int(os.environ["RANK"])
 world = int(os.environ["WORLD_SIZE"])
@@ -35,8 +37,18 @@ grid = 148 * 4
 buf = torch.zeros(grid * args.cap * 4, dtype=torch.int32, device=dev)
 _lib.lib().optr_debug_trace(buf.data_ptr(), args.cap)
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+if args.steady:
+    outs = [torch.empty_like(x) for _ in range(args.steady)]
+    _lib.lib().optr_debug_trace(None, 0)
+    for g in range(args.steady - 1):
+        comm.allreduce(x, outs[g], rotation=g % world, ht=True, job_seed=1, generation=10 + g,
+                       masks=MaskSpec.coin(10 + g, 0.01), async_op=True)
+    _lib.lib().optr_debug_trace(buf.data_ptr(), args.cap)
 e0.record()
-comm.allreduce(x, out, rotation=0, ht=True, job_seed=1, generation=9, masks=MaskSpec.coin(9, 0.01))
+comm.allreduce(x, out, rotation=0, ht=True, job_seed=1, generation=9, masks=MaskSpec.coin(9, 0.01),
+               async_op=bool(args.steady))
+if args.steady:
+    comm.join()
 e1.record()
 torch.cuda.synchronize()
 _lib.lib().optr_debug_trace(None, 0)
