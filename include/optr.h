@@ -290,7 +290,10 @@ int64_t optr_fused_unit_entries(int64_t dim, int n);
 /* Enable (1) / disable (0) CUDA-event timing of every kernel launch. */
 int optr_timing_enable(int on);
 /* Debug: event trace of the fused multi-GPU kernel into a device buffer of
- * gridDim * per_cta uint4 records (null disables).  Not thread-safe. */
+ * gridDim * per_cta uint4 records (null disables); per_cta < 0 instead points
+ * the small-bucket kernels' phase stamps (u64 globaltimer ns: [64][16] per
+ * call epoch for tar_small_kernel, [16] for tar_small_local_kernel) at the
+ * buffer.  Not thread-safe. */
 int optr_debug_trace(void* dev_buf, int64_t per_cta);
 /* Synchronise recorded events and return, per class, the summed device
  * milliseconds, the launch count and the worker-passes those launches
